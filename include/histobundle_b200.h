@@ -1,0 +1,171 @@
+/*
+ * histobundle_b200.h -- C ABI of the B200-native bundling iteration.
+ *
+ * This is the drop-in boundary for the reference's operator layer: each entry
+ * point replaces one numba kernel (or numpy routine) that
+ * /root/reference/pkg/src/histobundle/bundler.py and raster.py call through
+ * numba's native-call "FFI" (caller-allocated arrays + an edge range, kernels
+ * write only their own rows, _kernels.py:1-6).  Here the arrays are device
+ * pointers, the edge range is the whole shard, and every call is
+ * stream-ordered on the caller's cudaStream_t (passed as void*).
+ *
+ * Conventions (all entry points):
+ *   - return 0 on success, a negative HB_E* code on failure; the message is
+ *     available from hb_last_error() (thread-local).
+ *   - the library never allocates device memory; outputs and workspaces are
+ *     caller-allocated (ownership as in bundler.py:112,119,145 / raster.py:86).
+ *   - points are packed (N, 2) float64 grid coordinates, x then y;
+ *     `starts` is (E+1) int64 with starts[0] == 0 (bundler.py:84-89).
+ *   - histograms/fields are (B, V, U) row-major; counts are int32 per group,
+ *     fields float32.
+ *   - float64 arithmetic is bit-identical to the reference (no FMA
+ *     contraction, float32 density differences, floor(x+0.5) cells).
+ */
+#ifndef HISTOBUNDLE_B200_H
+#define HISTOBUNDLE_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#if defined(__GNUC__)
+#define HB_API __attribute__((visibility("default")))
+#else
+#define HB_API
+#endif
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define HB_OK 0
+#define HB_EINVAL (-1)   /* bad argument (sizes, null pointers)            */
+#define HB_ECUDA (-2)    /* CUDA launch / runtime error                    */
+
+/* status-flag bits written by device kernels (caller-owned int32) */
+#define HB_STATUS_OUT_OF_BOUNDS 1 /* raster.py:57-67 "sample out of bounds" */
+
+HB_API int hb_abi_version(void);
+HB_API const char *hb_last_error(void);
+HB_API int hb_device_sm_count(void);
+
+/* _kernels.fill_samples (_kernels.py:22-43), called by _sample_packed
+ * (bundler.py:77-89).  src/dst: (E,2) grid endpoints; starts from the host
+ * count rule max(ceil(|d|/delta),1)+1; pts: (starts[E],2). */
+HB_API int hb_sample_fill(const double *src, const double *dst, const int64_t *starts,
+                   int64_t n_edges, double *pts, void *stream);
+
+/* _offset_packed (bundler.py:92-106): interior points of edge e move by
+ * disp[e] (per-edge (dx,dy) computed on the host with the reference's numpy
+ * expression). */
+HB_API int hb_offset(double *pts, const int64_t *starts, int64_t n_edges,
+              const double *disp, void *stream);
+
+/* _materialize (bundler.py:152-163): out = pts*cell + origin per point, the
+ * first/last point of edge e replaced by src_world[e]/dst_world[e] (either
+ * may be NULL to skip pinning). */
+HB_API int hb_to_world(const double *pts, const int64_t *starts, int64_t n_edges,
+                       double origin_x, double origin_y, double cell,
+                       const double *src_world, const double *dst_world, double *out,
+                       void *stream);
+
+/* _kernels.accumulate (_kernels.py:46-77) via raster._accumulate_packed
+ * (raster.py:70-94), per-group form: counts[group[e]] += weight[e] on every
+ * rasterised cell of edge e.  weight may be NULL (all 1).  counts must be
+ * zeroed by the caller.  Out-of-grid cells set HB_STATUS_OUT_OF_BOUNDS. */
+HB_API int hb_splat(const double *pts, const int64_t *starts, int64_t n_edges,
+             int64_t n_pts, const int32_t *group, const int32_t *weight,
+             int32_t *counts, int nbins, int nv, int nu, int32_t *status,
+             void *stream);
+
+/* Same rasterisation with float32 weights (non-integer edge weights):
+ * hist[group[e]] += weight[e] with float atomics (order-dependent in the
+ * last bits, like the reference across worker counts, raster.py:76-78). */
+HB_API int hb_splat_f32(const double *pts, const int64_t *starts, int64_t n_edges,
+                 int64_t n_pts, const int32_t *group, const float *weight,
+                 float *hist, int nbins, int nv, int nu, int32_t *status,
+                 void *stream);
+
+/* Workspace for hb_smooth: bytes of float64 tables + float32 staging. */
+HB_API size_t hb_smooth_workspace_bytes(int nbins, int nv, int nu);
+
+/* smooth_gaussian_approx (raster.py:203-219) of H = M * G, where G is the
+ * per-group histogram (`counts` int32, or `hist` float32 when counts is
+ * NULL): for each pass p a float64 integral image (column fold then row fold,
+ * raster.py:133-139) and the 4-term box sum / (2r+1)^2 (raster.py:147-169).
+ * matrix: (B,B) float32 row-major, NULL = identity; the mix is
+ * H[l] = float32(sum_b M[l,b] G[b]) in float64, one rounding.
+ * radii: npasses box radii (w-1)/2 from box_widths (raster.py:172-193).
+ * layer_peak (B floats, nullable): max(rho_l, 0) of the final field, for
+ * used_cell_count. */
+HB_API int hb_smooth(const int32_t *counts, const float *hist, const float *matrix,
+              int nbins, int nv, int nu, const int32_t *radii, int npasses,
+              float *out, void *workspace, size_t workspace_bytes,
+              float *layer_peak, void *stream);
+
+/* The raw histogram H = M * G alone (raster.accumulate_edges, raster.py:108-130). */
+HB_API int hb_mix_layers(const int32_t *counts, const float *hist, const float *matrix,
+                         int nbins, int nv, int nu, float *out, void *stream);
+
+/* raster.integral_image (raster.py:133-139) of B layers: table[b][v][u] =
+ * T[b][v+1][u+1] (the zero first row/column is implicit). */
+HB_API int hb_integral_image(const float *in, int nbins, int nv, int nu, double *table,
+                             void *stream);
+
+/* used_cell_count (bundler.py:292-305): adds to *count the number of cells
+ * with rho > float32(rel * peak_l) over layers with peak_l > 0. */
+HB_API int hb_used_cells(const float *rho, const float *layer_peak, int nbins, int nv,
+                  int nu, double rel, unsigned long long *count, void *stream);
+
+/* Number of per-block partials hb_advect_laplacian writes (for sizing). */
+HB_API int64_t hb_advect_partials(int64_t n_pts, int lap_passes);
+
+/* _kernels.advect (_kernels.py:144-200) followed by _kernels.laplacian
+ * (_kernels.py:275-296), fused: pts_out = laplacian^passes(advect(pts_in)).
+ * h < 0 skips advection (Laplacian only, bundler.laplacian_smooth).
+ * pts_in and pts_out must not alias.  edge_layer: (E) int32 layer of each
+ * edge (bins).  moved: u64 accumulator (added to).  disp_partials:
+ * hb_advect_partials() doubles, reduced by hb_reduce_f64 in fixed order. */
+HB_API int hb_advect_laplacian(const double *pts_in, double *pts_out,
+                        const int64_t *starts, int64_t n_edges, int64_t n_pts,
+                        const int32_t *edge_layer, const float *rho, int nbins,
+                        int nv, int nu, double h, double eps, double min_step,
+                        int fixed_step, double lap_factor, int lap_passes,
+                        unsigned long long *moved, double *disp_partials,
+                        void *stream);
+
+/* Deterministic fixed-order sum of n doubles into *out (one block). */
+HB_API int hb_reduce_f64(const double *in, int64_t n, double *out, void *stream);
+
+/* _kernels.resample_count (_kernels.py:203-232): counts[e] = output points
+ * of edge e; pos[j] = local output index of kept point j, -1 if merged. */
+HB_API int hb_resample_count(const double *pts, const int64_t *starts,
+                      int64_t n_edges, double delta, int64_t *counts,
+                      int32_t *pos, void *stream);
+
+/* np.cumsum(counts) into new_starts[1..E], new_starts[0] = 0
+ * (bundler.py:117-118). */
+HB_API size_t hb_scan_workspace_bytes(int64_t n_edges);
+HB_API int hb_scan_counts(const int64_t *counts, int64_t n_edges, int64_t *new_starts,
+                   void *workspace, size_t workspace_bytes, void *stream);
+
+/* _kernels.resample_emit (_kernels.py:235-272) fused with the next
+ * iteration's accumulate: writes the resampled polylines into `out` at
+ * new_starts and, when counts != NULL, rasterises every output segment into
+ * counts (same contract as hb_splat). */
+HB_API int hb_resample_emit(const double *pts, const int64_t *starts,
+                     int64_t n_edges, int64_t n_pts, const int32_t *pos,
+                     const int64_t *new_starts, double *out,
+                     const int32_t *group, const int32_t *weight,
+                     int32_t *counts, int nv, int nu, int32_t *status,
+                     void *stream);
+
+/* Per-point probes used by the single-point operator API
+ * (bundler.density_at / gradient_at, bundler.py:203-217). */
+HB_API int hb_probe(const float *rho_layer, int nv, int nu, const double *xy,
+             int64_t n, double *value, double *grad, void *stream);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* HISTOBUNDLE_B200_H */

@@ -1,0 +1,115 @@
+"""Loader for the sm_100a C-ABI library ``libhb_b200.so`` (csrc/*.cu).
+
+The library is built in-tree (``build()`` below, called by
+``__graft_entry__.build()``) with nvcc for ``sm_100a`` only, and loaded with
+ctypes. There is no fallback: if the library is missing or no CUDA device is
+present, every entry point raises.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import os
+import subprocess
+
+_PKG = os.path.dirname(os.path.abspath(__file__))
+CSRC = os.path.join(_PKG, "csrc")
+LIB_DIR = os.path.join(_PKG, "_lib")
+LIB_PATH = os.path.join(LIB_DIR, "libhb_b200.so")
+INCLUDE = os.path.join(os.path.dirname(_PKG), "include")
+
+SOURCES = ["hb_api.cu", "hb_polyline.cu", "hb_field.cu", "hb_advect.cu"]
+
+NVCC_FLAGS = [
+    "-gencode", "arch=compute_100a,code=sm_100a",
+    "-O3", "-lineinfo", "-std=c++17",
+    # bit-exact float64: never contract a*b+c into FMA
+    "--fmad=false",
+    "-Xcompiler", "-fPIC", "-Xcompiler", "-fvisibility=hidden",
+    "-Xptxas", "-warn-spills",
+]
+
+
+class NativeError(RuntimeError):
+    pass
+
+
+def build(verbose: bool = False) -> str:
+    """Compile csrc/*.cu into _lib/libhb_b200.so (cross-compiles without a GPU)."""
+    os.makedirs(LIB_DIR, exist_ok=True)
+    nvcc = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
+    objs = []
+    for src in SOURCES:
+        obj = os.path.join(LIB_DIR, src.replace(".cu", ".o"))
+        cmd = [nvcc, *NVCC_FLAGS, "-I", INCLUDE, "-c", os.path.join(CSRC, src), "-o", obj]
+        if verbose:
+            print(" ".join(cmd))
+        subprocess.run(cmd, check=True)
+        objs.append(obj)
+    tmp = LIB_PATH + ".tmp"
+    subprocess.run([nvcc, "-gencode", "arch=compute_100a,code=sm_100a", "-shared",
+                    "--cudart=static", "-o", tmp, *objs], check=True)
+    os.replace(tmp, LIB_PATH)
+    return LIB_PATH
+
+
+_P, _I64, _I, _D, _SZ = (ctypes.c_void_p, ctypes.c_int64, ctypes.c_int,
+                         ctypes.c_double, ctypes.c_size_t)
+
+# name -> (restype, argtypes); mirrors include/histobundle_b200.h
+SIGNATURES = {
+    "hb_abi_version": (_I, []),
+    "hb_last_error": (ctypes.c_char_p, []),
+    "hb_device_sm_count": (_I, []),
+    "hb_sample_fill": (_I, [_P, _P, _P, _I64, _P, _P]),
+    "hb_offset": (_I, [_P, _P, _I64, _P, _P]),
+    "hb_to_world": (_I, [_P, _P, _I64, _D, _D, _D, _P, _P, _P, _P]),
+    "hb_splat": (_I, [_P, _P, _I64, _I64, _P, _P, _P, _I, _I, _I, _P, _P]),
+    "hb_splat_f32": (_I, [_P, _P, _I64, _I64, _P, _P, _P, _I, _I, _I, _P, _P]),
+    "hb_smooth_workspace_bytes": (_SZ, [_I, _I, _I]),
+    "hb_smooth": (_I, [_P, _P, _P, _I, _I, _I, _P, _I, _P, _P, _SZ, _P, _P]),
+    "hb_mix_layers": (_I, [_P, _P, _P, _I, _I, _I, _P, _P]),
+    "hb_integral_image": (_I, [_P, _I, _I, _I, _P, _P]),
+    "hb_used_cells": (_I, [_P, _P, _I, _I, _I, _D, _P, _P]),
+    "hb_advect_partials": (_I64, [_I64, _I]),
+    "hb_advect_laplacian": (_I, [_P, _P, _P, _I64, _I64, _P, _P, _I, _I, _I, _D, _D,
+                                 _D, _I, _D, _I, _P, _P, _P]),
+    "hb_reduce_f64": (_I, [_P, _I64, _P, _P]),
+    "hb_resample_count": (_I, [_P, _P, _I64, _D, _P, _P, _P]),
+    "hb_scan_workspace_bytes": (_SZ, [_I64]),
+    "hb_scan_counts": (_I, [_P, _I64, _P, _P, _SZ, _P]),
+    "hb_resample_emit": (_I, [_P, _P, _I64, _I64, _P, _P, _P, _P, _P, _P, _I, _I, _P,
+                              _P]),
+    "hb_probe": (_I, [_P, _I, _I, _P, _I64, _P, _P, _P]),
+}
+
+_lib = None
+
+
+def load_library(path: str = LIB_PATH):
+    """dlopen the library and bind every declared symbol (no device needed)."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(path):
+        raise NativeError(
+            f"{path} is missing: build it with `python -c 'import __graft_entry__ as g; g.build()'`")
+    lib = ctypes.CDLL(path)
+    for name, (res, args) in SIGNATURES.items():
+        fn = getattr(lib, name)
+        fn.restype = res
+        fn.argtypes = args
+    _lib = lib
+    return lib
+
+
+def lib():
+    return _lib if _lib is not None else load_library()
+
+
+def call(name: str, *args) -> None:
+    """Invoke an hb_* entry point and raise NativeError on a non-zero status."""
+    rc = getattr(lib(), name)(*args)
+    if rc != 0:
+        msg = lib().hb_last_error().decode(errors="replace")
+        raise NativeError(f"{name} failed ({rc}): {msg}")

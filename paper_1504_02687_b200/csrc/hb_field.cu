@@ -1,0 +1,283 @@
+// hb_field.cu -- density-field kernels: layer mixing, the 3-pass box-filter
+// Gaussian approximation, layer peaks and used-cell counting.
+//
+// Exactness: each box pass of the reference builds a
+// float64 integral image with two strict left folds -- down every column,
+// then along every row (np.cumsum axis 0 then axis 1, raster.py:133-139) --
+// and takes ((T11 - T01) - T10) + T00 divided by the full window area
+// (raster.py:147-169).  Pass inputs after the first are non-integer float32
+// values, so the fold ORDER decides the last bits of the table; we keep the
+// reference's order exactly:
+//   col_scan : one thread per (layer, column), sequential in v, coalesced rows
+//   row_scan : one lane per (layer, row), 32x32 tiles staged through shared
+//              memory so global traffic stays coalesced, sequential in u
+//   box      : one thread per cell, 4 table gathers, IEEE divide, f32 round
+#include "hb_common.cuh"
+
+namespace hb {
+
+constexpr int kColBlock = 128;
+
+// Pass-1 column fold straight from the per-group histograms (int32 counts or
+// float32 sums), mixing the layers on the fly: H[l] = float32(sum_b M[l,b] *
+// G[b]) (float64 sum in ascending b, one rounding -- exact whenever the
+// reference's float32 sums are exact).  M == NULL means identity.
+template <typename T>
+__device__ __forceinline__ float mixed_value(const T *__restrict__ g, const float *__restrict__ mat,
+                                             int nb, int l, int64_t plane, int64_t off) {
+    if (!mat) return (float)g[l * plane + off];
+    double acc = 0.0;
+    for (int b = 0; b < nb; ++b)
+        acc = dadd(acc, dmul((double)__ldg(mat + l * nb + b), (double)g[b * plane + off]));
+    return __double2float_rn(acc);
+}
+
+template <typename T>
+__global__ void __launch_bounds__(kColBlock)
+col_scan_mix_kernel(const T *__restrict__ groups, const float *__restrict__ mat, int nb, int nv,
+                    int nu, double *__restrict__ table) {
+    const int u = blockIdx.x * kColBlock + threadIdx.x;
+    const int l = blockIdx.y;
+    if (u >= nu) return;
+    const int64_t plane = (int64_t)nv * nu;
+    double c = 0.0;
+    for (int v = 0; v < nv; ++v) {
+        const int64_t off = (int64_t)v * nu + u;
+        const double hv = (double)mixed_value<T>(groups, mat, nb, l, plane, off);
+        c = (v == 0) ? hv : dadd(c, hv);
+        table[l * plane + off] = c;
+    }
+}
+
+__global__ void __launch_bounds__(kColBlock)
+col_scan_f32_kernel(const float *__restrict__ in, int nv, int nu,
+                    double *__restrict__ table) {
+    const int u = blockIdx.x * kColBlock + threadIdx.x;
+    const int l = blockIdx.y;
+    if (u >= nu) return;
+    const int64_t plane = (int64_t)nv * nu;
+    const float *src = in + l * plane + u;
+    double *dst = table + l * plane + u;
+    double c = 0.0;
+#pragma unroll 4
+    for (int v = 0; v < nv; ++v) {
+        const double x = (double)__ldg(src + (int64_t)v * nu);
+        c = (v == 0) ? x : dadd(c, x);
+        dst[(int64_t)v * nu] = c;
+    }
+}
+
+// Row fold in place.  Rows are flattened over (layer, v).  A warp owns 32
+// rows; for each 32-column tile it loads coalesced into shared memory, each
+// lane folds its own row left to right, and the tile is stored back.
+constexpr int kRowWarps = 4;
+
+__global__ void __launch_bounds__(kRowWarps * 32)
+row_scan_kernel(double *__restrict__ table, int64_t n_rows, int nu) {
+    __shared__ double tile[kRowWarps][32][33];
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int64_t r0 = ((int64_t)blockIdx.x * kRowWarps + warp) * 32;
+    if (r0 >= n_rows) return;
+    const int nr = (int)(n_rows - r0 < 32 ? n_rows - r0 : 32);
+    double (*t)[33] = tile[warp];
+    double carry = 0.0;
+    for (int c0 = 0; c0 < nu; c0 += 32) {
+        const int nc = nu - c0 < 32 ? nu - c0 : 32;
+        for (int i = 0; i < nr; ++i)
+            if (lane < nc) t[i][lane] = table[(r0 + i) * nu + c0 + lane];
+        __syncwarp();
+        if (lane < nr) {
+            double c = carry;
+            for (int k = 0; k < nc; ++k) {
+                c = (c0 + k == 0) ? t[lane][k] : dadd(c, t[lane][k]);
+                t[lane][k] = c;
+            }
+            carry = c;
+        }
+        __syncwarp();
+        for (int i = 0; i < nr; ++i)
+            if (lane < nc) table[(r0 + i) * nu + c0 + lane] = t[i][lane];
+        __syncwarp();
+    }
+}
+
+// 4-term box sum with zero row/column 0 implicit (table holds T[1:,1:]).
+__device__ __forceinline__ double tz(const double *__restrict__ t, int nu, int r, int c) {
+    return (r == 0 || c == 0) ? 0.0 : t[(int64_t)(r - 1) * nu + (c - 1)];
+}
+
+constexpr int kBoxBlock = 256;
+
+__global__ void __launch_bounds__(kBoxBlock)
+box_kernel(const double *__restrict__ table, int nv, int nu, int radius,
+           float *__restrict__ out, float *__restrict__ peak) {
+    const int u = blockIdx.x * kBoxBlock + threadIdx.x;
+    const int v = blockIdx.y;
+    const int l = blockIdx.z;
+    float val = 0.0f;
+    if (u < nu) {
+        const int64_t plane = (int64_t)nv * nu;
+        const double *t = table + l * plane;
+        const int r0 = min(max(v - radius, 0), nv), r1 = min(max(v + radius + 1, 0), nv);
+        const int c0 = min(max(u - radius, 0), nu), c1 = min(max(u + radius + 1, 0), nu);
+        const double s = dadd(dsub(dsub(tz(t, nu, r1, c1), tz(t, nu, r0, c1)),
+                                   tz(t, nu, r1, c0)),
+                              tz(t, nu, r0, c0));
+        const double area = (double)((2 * radius + 1) * (2 * radius + 1));
+        val = __double2float_rn(__ddiv_rn(s, area));
+        out[l * plane + (int64_t)v * nu + u] = val;
+    }
+    if (peak) {
+        // max(rho, initial=0): non-negative floats order like their bits
+        float m = val > 0.0f ? val : 0.0f;
+        for (int d = 16; d; d >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, d));
+        if ((threadIdx.x & 31) == 0 && m > 0.0f)
+            atomicMax(reinterpret_cast<int *>(peak + l), __float_as_int(m));
+    }
+}
+
+// radius-0 pass (raster.py:157-158 returns a copy) and stand-alone layer
+// mixing (the raw histogram H of raster.accumulate_edges).
+template <typename T>
+__global__ void mix_pass_kernel(const T *__restrict__ groups, const float *__restrict__ mat,
+                                int nb, int64_t plane, float *__restrict__ out,
+                                float *__restrict__ peak) {
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    const int l = blockIdx.y;
+    float val = 0.0f;
+    if (i < plane) {
+        val = mixed_value<T>(groups, mat, nb, l, plane, i);
+        out[l * plane + i] = val;
+    }
+    if (peak) {
+        float m = val > 0.0f ? val : 0.0f;
+        for (int d = 16; d; d >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, d));
+        if ((threadIdx.x & 31) == 0 && m > 0.0f)
+            atomicMax(reinterpret_cast<int *>(peak + l), __float_as_int(m));
+    }
+}
+
+// used_cell_count (bundler.py:292-305): rho > float32(rel * peak_l) when
+// peak_l > 0 (NEP 50 makes the comparison float32).
+__global__ void used_cells_kernel(const float *__restrict__ rho, const float *__restrict__ peak,
+                                  int64_t plane, double rel, unsigned long long *count) {
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    const int l = blockIdx.y;
+    const float pk = peak[l];
+    bool hit = false;
+    if (i < plane && (double)pk > 0.0) {
+        const float thr = __double2float_rn(dmul(rel, (double)pk));
+        hit = rho[l * plane + i] > thr;
+    }
+    const unsigned m = __ballot_sync(0xffffffffu, hit);
+    if ((threadIdx.x & 31) == 0 && m) atomicAdd(count, (unsigned long long)__popc(m));
+}
+
+}  // namespace hb
+
+using namespace hb;
+
+static inline cudaStream_t as_stream(void *s) { return reinterpret_cast<cudaStream_t>(s); }
+
+extern "C" {
+
+size_t hb_smooth_workspace_bytes(int nbins, int nv, int nu) {
+    const size_t cells = (size_t)nbins * nv * nu;
+    return cells * sizeof(double) + cells * sizeof(float) + 256;
+}
+
+int hb_smooth(const int32_t *counts, const float *hist, const float *matrix, int nbins,
+              int nv, int nu, const int32_t *radii, int npasses, float *out,
+              void *workspace, size_t workspace_bytes, float *layer_peak, void *stream) {
+    if (nbins < 1 || nv < 1 || nu < 1 || npasses < 1 || !radii || !out || (!counts && !hist))
+        return set_error(HB_EINVAL, "hb_smooth: bad arguments");
+    if (!workspace || workspace_bytes < hb_smooth_workspace_bytes(nbins, nv, nu))
+        return set_error(HB_EINVAL, "hb_smooth: workspace too small");
+    for (int p = 0; p < npasses; ++p)
+        if (radii[p] < 0) return set_error(HB_EINVAL, "radius must be >= 0");
+    cudaStream_t st = as_stream(stream);
+    const int64_t plane = (int64_t)nv * nu;
+    const size_t cells = (size_t)nbins * plane;
+    double *table = reinterpret_cast<double *>(workspace);
+    float *stage = reinterpret_cast<float *>(table + cells);
+    if (layer_peak && cudaMemsetAsync(layer_peak, 0, sizeof(float) * nbins, st) != cudaSuccess)
+        return check_launch("hb_smooth(memset)");
+    const float *src = nullptr;  // float32 input of passes after the first
+    for (int p = 0; p < npasses; ++p) {
+        const bool first = (p == 0);
+        const bool mix_first = first && (counts || matrix);
+        // passes alternate between stage and out so the last one lands in out
+        float *dst = ((npasses - 1 - p) % 2 == 0) ? out : stage;
+        float *pk = (p == npasses - 1) ? layer_peak : nullptr;
+        const int r = radii[p];
+        if (r == 0) {
+            dim3 g((unsigned)((plane + 255) / 256), nbins);
+            if (first && counts)
+                mix_pass_kernel<int32_t><<<g, 256, 0, st>>>(counts, matrix, nbins, plane, dst, pk);
+            else
+                mix_pass_kernel<float><<<g, 256, 0, st>>>(first ? hist : src,
+                                                          first ? matrix : nullptr, nbins,
+                                                          plane, dst, pk);
+        } else {
+            dim3 gc((nu + kColBlock - 1) / kColBlock, nbins);
+            if (mix_first && counts)
+                col_scan_mix_kernel<int32_t><<<gc, kColBlock, 0, st>>>(counts, matrix, nbins,
+                                                                       nv, nu, table);
+            else if (mix_first)
+                col_scan_mix_kernel<float><<<gc, kColBlock, 0, st>>>(hist, matrix, nbins, nv,
+                                                                     nu, table);
+            else
+                col_scan_f32_kernel<<<gc, kColBlock, 0, st>>>(first ? hist : src, nv, nu,
+                                                              table);
+            const int64_t rows = (int64_t)nbins * nv;
+            const unsigned rb = (unsigned)((rows + 32 * kRowWarps - 1) / (32 * kRowWarps));
+            row_scan_kernel<<<rb, kRowWarps * 32, 0, st>>>(table, rows, nu);
+            dim3 gb((nu + kBoxBlock - 1) / kBoxBlock, nv, nbins);
+            box_kernel<<<gb, kBoxBlock, 0, st>>>(table, nv, nu, r, dst, pk);
+        }
+        int rc = check_launch("hb_smooth");
+        if (rc) return rc;
+        src = dst;
+    }
+    return HB_OK;
+}
+
+int hb_mix_layers(const int32_t *counts, const float *hist, const float *matrix, int nbins,
+                  int nv, int nu, float *out, void *stream) {
+    if (nbins < 1 || nv < 1 || nu < 1 || !out || (!counts && !hist))
+        return set_error(HB_EINVAL, "hb_mix_layers: bad arguments");
+    const int64_t plane = (int64_t)nv * nu;
+    dim3 g((unsigned)((plane + 255) / 256), nbins);
+    if (counts)
+        mix_pass_kernel<int32_t><<<g, 256, 0, as_stream(stream)>>>(counts, matrix, nbins, plane,
+                                                                   out, nullptr);
+    else
+        mix_pass_kernel<float><<<g, 256, 0, as_stream(stream)>>>(hist, matrix, nbins, plane,
+                                                                 out, nullptr);
+    return check_launch("hb_mix_layers");
+}
+
+int hb_integral_image(const float *in, int nbins, int nv, int nu, double *table,
+                      void *stream) {
+    if (!in || !table || nbins < 1 || nv < 1 || nu < 1)
+        return set_error(HB_EINVAL, "hb_integral_image: bad arguments");
+    cudaStream_t st = as_stream(stream);
+    dim3 gc((nu + kColBlock - 1) / kColBlock, nbins);
+    col_scan_f32_kernel<<<gc, kColBlock, 0, st>>>(in, nv, nu, table);
+    const int64_t rows = (int64_t)nbins * nv;
+    const unsigned rb = (unsigned)((rows + 32 * kRowWarps - 1) / (32 * kRowWarps));
+    row_scan_kernel<<<rb, kRowWarps * 32, 0, st>>>(table, rows, nu);
+    return check_launch("hb_integral_image");
+}
+
+int hb_used_cells(const float *rho, const float *layer_peak, int nbins, int nv, int nu,
+                  double rel, unsigned long long *count, void *stream) {
+    if (!rho || !layer_peak || !count || nbins < 1 || nv < 1 || nu < 1)
+        return set_error(HB_EINVAL, "hb_used_cells: bad arguments");
+    const int64_t plane = (int64_t)nv * nu;
+    dim3 g((unsigned)((plane + 255) / 256), nbins);
+    used_cells_kernel<<<g, 256, 0, as_stream(stream)>>>(rho, layer_peak, plane, rel, count);
+    return check_launch("hb_used_cells");
+}
+
+}  // extern "C"

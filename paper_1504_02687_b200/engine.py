@@ -1,0 +1,307 @@
+"""Device-resident bundling engine: buffers, the per-iteration kernel
+sequence, metrics and timing.
+
+One engine owns one shard of edges on one GPU (the whole graph at N=1). Per
+iteration ``i`` (``bundler.py:351-376``) it launches, on the current CUDA
+stream:
+
+  i > 0: hb_resample_count -> hb_scan_counts -> (1 host read: N_i)
+         -> hb_resample_emit (+ fused splat into the int32 group counts)
+  i = 0: hb_splat
+  [world > 1: all-reduce of the int32 counts over NCCL]
+  hb_smooth (mix + 3 exact box passes + layer peaks)
+  hb_advect_laplacian (+ per-block metric partials) -> hb_reduce_f64
+  hb_used_cells
+
+Host reads per iteration: the new point total (needed to size the emit
+buffer). Metrics stay on the device until the run ends unless an
+``on_iteration`` callback asks for them each iteration.
+"""
+
+from __future__ import annotations
+
+import math
+from dataclasses import dataclass, field
+
+import numpy as np
+import torch
+
+from . import _native as N
+from .model import BundleConfig
+
+__all__ = ["BundleEngine", "box_widths", "sample_counts", "IterationRecord"]
+
+MIN_STEP = 0.25  # bundler.py:48
+
+
+def box_widths(sigma: float, passes: int) -> list[int]:
+    """Odd box widths for the n-box Gaussian approximation (raster.py:172-193)."""
+    if sigma <= 0:
+        raise ValueError("sigma must be positive")
+    if passes < 1:
+        raise ValueError("passes must be >= 1")
+    ideal = math.sqrt(12.0 * sigma * sigma / passes + 1.0)
+    lo = int(math.floor(ideal))
+    if lo % 2 == 0:
+        lo -= 1
+    lo = max(lo, 1)
+    m_ideal = ((12.0 * sigma * sigma - passes * lo * lo - 4.0 * passes * lo
+                - 3.0 * passes) / (-4.0 * lo - 4.0))
+    m = min(max(int(round(m_ideal)), 0), passes)
+    return [lo] * m + [lo + 2] * (passes - m)
+
+
+def sample_counts(src: np.ndarray, dst: np.ndarray, delta: float) -> np.ndarray:
+    """Initial point counts max(ceil(|d|/delta), 1) + 1 (bundler.py:82-83),
+    with the reference's numpy norm so the rounding is identical."""
+    seg = np.linalg.norm(dst - src, axis=1)
+    return np.maximum(np.ceil(seg / delta).astype(np.int64), 1) + 1
+
+
+def ptr(t) -> int | None:
+    return None if t is None else t.data_ptr()
+
+
+def stream_ptr() -> int:
+    return torch.cuda.current_stream().cuda_stream
+
+
+@dataclass
+class IterationRecord:
+    iteration: int
+    bandwidth: float
+    n_points: int          # points entering splat/advect (this shard)
+    n_edges: int
+    moved_points: int = 0
+    disp: float = 0.0
+    used_cells: int = 0
+    seconds: float = 0.0
+
+
+@dataclass
+class WeightPlan:
+    """How edge weights reach the histogram."""
+
+    kind: str                      # "unit" | "int" | "float"
+    int_w: np.ndarray | None = None
+    f32_w: np.ndarray | None = None
+
+
+def weight_plan(weights: np.ndarray) -> WeightPlan:
+    w32 = weights.astype(np.float32)
+    if np.all(w32 == 1.0):
+        return WeightPlan("unit")
+    if np.all(np.floor(w32) == w32) and np.all(np.abs(w32) < 2**24):
+        return WeightPlan("int", int_w=w32.astype(np.int32))
+    return WeightPlan("float", f32_w=w32)
+
+
+class BundleEngine:
+    """Runs the bundling iterations for one edge shard on one CUDA device.
+
+    ``src``/``dst`` are the shard's grid-space endpoints ((E,2) float64,
+    ``transform.world_to_grid`` of the node positions), ``groups`` its bins.
+    ``reduce_hist`` (optional) is called with the int32/float32 group
+    histogram tensor after the splat; the distributed driver passes an
+    all-reduce here.
+    """
+
+    def __init__(self, src: np.ndarray, dst: np.ndarray, groups: np.ndarray,
+                 weights: WeightPlan, matrix: np.ndarray, shape: tuple[int, int],
+                 cfg: BundleConfig, *, fixed_step: bool = False,
+                 offset_disp: np.ndarray | None = None, device=None,
+                 reduce_hist=None, capacity_factor: float = 2.0):
+        N.lib()  # fail loudly if the native library is missing
+        if not torch.cuda.is_available():
+            raise N.NativeError("paper_1504_02687_b200 needs a CUDA device (sm_100a); "
+                                "there is no CPU path")
+        self.dev = torch.device(device if device is not None else "cuda")
+        self.cfg = cfg
+        self.fixed_step = bool(fixed_step)
+        self.reduce_hist = reduce_hist
+        self.nv, self.nu = int(shape[0]), int(shape[1])
+        self.matrix = np.ascontiguousarray(matrix, dtype=np.float32)
+        self.nbins = int(self.matrix.shape[0])
+        self.n_edges = int(src.shape[0])
+        self.radii = torch.tensor([(w - 1) // 2 for w in
+                                   box_widths(cfg.sigma, cfg.smoothing_passes)],
+                                  dtype=torch.int32)
+        self.delta = float(cfg.delta)
+        E, B = self.n_edges, self.nbins
+        dev = self.dev
+
+        counts = sample_counts(src, dst, self.delta)
+        starts = np.zeros(E + 1, dtype=np.int64)
+        np.cumsum(counts, out=starts[1:])
+        self.n_pts = int(starts[-1])
+        self.cap = max(int(self.n_pts * capacity_factor), 1024)
+        self.pts = torch.empty((self.cap, 2), dtype=torch.float64, device=dev)
+        self.alt = torch.empty((self.cap, 2), dtype=torch.float64, device=dev)
+        self.pos = torch.empty(self.cap, dtype=torch.int32, device=dev)
+        self.starts = torch.from_numpy(starts).to(dev)
+        self.starts_alt = torch.empty_like(self.starts)
+        self.ecounts = torch.empty(max(E, 1), dtype=torch.int64, device=dev)
+        self.groups = torch.from_numpy(np.ascontiguousarray(groups, dtype=np.int32)).to(dev)
+        self.wkind = weights.kind
+        self.wint = (torch.from_numpy(weights.int_w).to(dev)
+                     if weights.kind == "int" else None)
+        self.wf32 = (torch.from_numpy(weights.f32_w).to(dev)
+                     if weights.kind == "float" else None)
+        mat_is_identity = np.array_equal(self.matrix, np.eye(B, dtype=np.float32))
+        self.mat_dev = (None if mat_is_identity else
+                        torch.from_numpy(self.matrix.copy()).to(dev))
+        hdtype = torch.float32 if self.wkind == "float" else torch.int32
+        self.hist = torch.empty((B, self.nv, self.nu), dtype=hdtype, device=dev)
+        self.field = torch.empty((B, self.nv, self.nu), dtype=torch.float32, device=dev)
+        self.peak = torch.empty(B, dtype=torch.float32, device=dev)
+        self.status = torch.zeros(1, dtype=torch.int32, device=dev)
+        sws = N.lib().hb_smooth_workspace_bytes(B, self.nv, self.nu)
+        self.smooth_ws = torch.empty(sws, dtype=torch.uint8, device=dev)
+        scw = N.lib().hb_scan_workspace_bytes(max(E, 1))
+        self.scan_ws = torch.empty(scw, dtype=torch.uint8, device=dev)
+        self.lap_passes = int(cfg.laplacian_passes)
+        self._partials = torch.empty(0, dtype=torch.float64, device=dev)
+        self.iters = int(cfg.iterations)
+        # per-iteration device metrics: moved (u64 as int64), disp, used
+        self.m_moved = torch.zeros(self.iters, dtype=torch.int64, device=dev)
+        self.m_disp = torch.zeros(self.iters, dtype=torch.float64, device=dev)
+        self.m_used = torch.zeros(self.iters, dtype=torch.int64, device=dev)
+        self.records: list[IterationRecord] = []
+        self._ev: list[tuple[torch.cuda.Event, torch.cuda.Event]] = []
+
+        s = stream_ptr()
+        srcd = torch.from_numpy(np.ascontiguousarray(src, dtype=np.float64)).to(dev)
+        dstd = torch.from_numpy(np.ascontiguousarray(dst, dtype=np.float64)).to(dev)
+        N.call("hb_sample_fill", ptr(srcd), ptr(dstd), ptr(self.starts), E,
+               ptr(self.pts), s)
+        if offset_disp is not None:
+            od = torch.from_numpy(np.ascontiguousarray(offset_disp)).to(dev)
+            N.call("hb_offset", ptr(self.pts), ptr(self.starts), E, ptr(od), s)
+        self.iteration = 0
+
+    # ------------------------------------------------------------------
+    def _ensure_capacity(self, n: int) -> None:
+        if n <= self.cap:
+            return
+        cap = max(int(n * 1.25), self.cap * 3 // 2)
+        new_pts = torch.empty((cap, 2), dtype=torch.float64, device=self.dev)
+        new_pts[: self.n_pts].copy_(self.pts[: self.n_pts])
+        self.pts = new_pts
+        self.alt = torch.empty((cap, 2), dtype=torch.float64, device=self.dev)
+        new_pos = torch.empty(cap, dtype=torch.int32, device=self.dev)
+        new_pos[: self.n_pts].copy_(self.pos[: self.n_pts])
+        self.pos = new_pos
+        self.cap = cap
+
+    def _partials_for(self, n: int) -> torch.Tensor:
+        k = int(N.lib().hb_advect_partials(n, self.lap_passes))
+        if k < 0:
+            raise ValueError("laplacian_passes must be <= 32")
+        if self._partials.numel() < max(k, 1):
+            self._partials = torch.empty(max(k, 1) * 2, dtype=torch.float64, device=self.dev)
+        return self._partials
+
+    def _splat_args(self):
+        if self.wkind == "float":
+            return "hb_splat_f32", ptr(self.wf32)
+        return "hb_splat", ptr(self.wint)
+
+    def step(self) -> IterationRecord:
+        """One bundling iteration (bundler.py:351-376) on the device."""
+        i = self.iteration
+        if i >= self.iters:
+            raise RuntimeError("all iterations done")
+        cfg = self.cfg
+        s = stream_ptr()
+        E, B, nv, nu = self.n_edges, self.nbins, self.nv, self.nu
+        ev0 = torch.cuda.Event(enable_timing=True)
+        ev1 = torch.cuda.Event(enable_timing=True)
+        ev0.record()
+        self.hist.zero_()
+        if i > 0:
+            # resample (bundler.py:353-354) fused with the splat (:355-356)
+            N.call("hb_resample_count", ptr(self.pts), ptr(self.starts), E, self.delta,
+                   ptr(self.ecounts), ptr(self.pos), s)
+            N.call("hb_scan_counts", ptr(self.ecounts), E, ptr(self.starts_alt),
+                   ptr(self.scan_ws), self.scan_ws.numel(), s)
+            n_new = int(self.starts_alt[E].item()) if E else 0
+            self._ensure_capacity(n_new)
+            fused = self.wkind != "float"
+            N.call("hb_resample_emit", ptr(self.pts), ptr(self.starts), E, self.n_pts,
+                   ptr(self.pos), ptr(self.starts_alt), ptr(self.alt), ptr(self.groups),
+                   ptr(self.wint), ptr(self.hist) if fused else None, nv, nu,
+                   ptr(self.status), s)
+            self.pts, self.alt = self.alt, self.pts
+            self.starts, self.starts_alt = self.starts_alt, self.starts
+            self.n_pts = n_new
+            if not fused:
+                name, w = self._splat_args()
+                N.call(name, ptr(self.pts), ptr(self.starts), E, self.n_pts,
+                       ptr(self.groups), w, ptr(self.hist), B, nv, nu, ptr(self.status), s)
+        else:
+            name, w = self._splat_args()
+            N.call(name, ptr(self.pts), ptr(self.starts), E, self.n_pts, ptr(self.groups),
+                   w, ptr(self.hist), B, nv, nu, ptr(self.status), s)
+        if self.reduce_hist is not None:
+            self.reduce_hist(self.hist)
+        is_int = self.wkind != "float"
+        N.call("hb_smooth", ptr(self.hist) if is_int else None,
+               None if is_int else ptr(self.hist), ptr(self.mat_dev), B, nv, nu,
+               self.radii.data_ptr(), int(self.radii.numel()), ptr(self.field),
+               ptr(self.smooth_ws), self.smooth_ws.numel(), ptr(self.peak), s)
+        h_i = cfg.lambda_ ** i * cfg.h_max  # bundler.py:360, Python float power
+        part = self._partials_for(self.n_pts)
+        nblk = int(N.lib().hb_advect_partials(self.n_pts, self.lap_passes))
+        N.call("hb_advect_laplacian", ptr(self.pts), ptr(self.alt), ptr(self.starts), E,
+               self.n_pts, ptr(self.groups), ptr(self.field), B, nv, nu, float(h_i),
+               float(cfg.epsilon), MIN_STEP, int(self.fixed_step),
+               float(cfg.laplacian_factor), self.lap_passes,
+               self.m_moved.data_ptr() + 8 * i, ptr(part), s)
+        if self.n_pts:
+            self.pts, self.alt = self.alt, self.pts
+        N.call("hb_reduce_f64", ptr(part), nblk, self.m_disp.data_ptr() + 8 * i, s)
+        N.call("hb_used_cells", ptr(self.field), ptr(self.peak), B, nv, nu, 0.01,
+               self.m_used.data_ptr() + 8 * i, s)
+        ev1.record()
+        self._ev.append((ev0, ev1))
+        rec = IterationRecord(i, h_i, self.n_pts, E)
+        self.records.append(rec)
+        self.iteration += 1
+        return rec
+
+    def finish_metrics(self) -> list[IterationRecord]:
+        """Synchronise once and fill moved/disp/used/seconds of all records."""
+        torch.cuda.current_stream().synchronize()
+        if int(self.status.item()) & 1:
+            raise ValueError("sample out of bounds: a polyline point left the grid")
+        moved = self.m_moved.cpu().numpy()
+        disp = self.m_disp.cpu().numpy()
+        used = self.m_used.cpu().numpy()
+        for r, (a, b) in zip(self.records, self._ev):
+            r.moved_points = int(moved[r.iteration])
+            r.disp = float(disp[r.iteration])
+            r.used_cells = int(used[r.iteration])
+            r.seconds = a.elapsed_time(b) / 1e3
+        return self.records
+
+    def run(self, on_iteration=None) -> list[IterationRecord]:
+        while self.iteration < self.iters:
+            self.step()
+            if on_iteration is not None:
+                on_iteration(self)
+        return self.finish_metrics()
+
+    # ------------------------------------------------------------------
+    def packed_points(self) -> tuple[torch.Tensor, torch.Tensor]:
+        return self.pts[: self.n_pts], self.starts
+
+    def world_points(self, origin, cell, src_world=None, dst_world=None) -> torch.Tensor:
+        out = torch.empty((self.n_pts, 2), dtype=torch.float64, device=self.dev)
+        sw = None if src_world is None else torch.from_numpy(
+            np.ascontiguousarray(src_world, dtype=np.float64)).to(self.dev)
+        dw = None if dst_world is None else torch.from_numpy(
+            np.ascontiguousarray(dst_world, dtype=np.float64)).to(self.dev)
+        N.call("hb_to_world", ptr(self.pts), ptr(self.starts), self.n_edges,
+               float(origin[0]), float(origin[1]), float(cell), ptr(sw), ptr(dw),
+               ptr(out), stream_ptr())
+        return out

@@ -1,0 +1,407 @@
+"""GPU parity: every kernel and the full loop against the CPU oracle and the
+reference-generated golden fixtures.  Bit-exact is the bar for integer
+histograms, points and fields; ``mean_displacement`` (an order-dependent
+float64 sum in the reference too) is compared to rel 1e-12."""
+
+from __future__ import annotations
+
+import json
+import os
+
+import numpy as np
+import pytest
+
+from conftest import GOLDEN
+from hb_hash import digest
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+if not torch.cuda.is_available():  # pragma: no cover
+    pytest.skip("needs a CUDA device", allow_module_level=True)
+
+import oracle as O  # noqa: E402
+from paper_1504_02687_b200 import _native as N  # noqa: E402
+from paper_1504_02687_b200 import bundler as B  # noqa: E402
+from paper_1504_02687_b200 import raster as R  # noqa: E402
+from paper_1504_02687_b200.engine import box_widths, ptr, stream_ptr  # noqa: E402
+from paper_1504_02687_b200.model import DensityField, SampledEdge  # noqa: E402
+from paper_1504_02687_b200.workloads import workload  # noqa: E402
+
+DISP_RTOL = 1e-12
+
+
+def kat():
+    return np.load(os.path.join(GOLDEN, "kat_ops.npz"))
+
+
+def dev(a):
+    return torch.from_numpy(np.ascontiguousarray(a)).cuda()
+
+
+def sync():
+    torch.cuda.synchronize()
+
+
+# ---------------------------------------------------------------------------
+# per-kernel parity on the branch-coverage fixture
+
+
+def test_native_library_is_the_loaded_path():
+    lib = N.lib()
+    assert lib.hb_abi_version() == 1
+    assert lib.hb_device_sm_count() >= 100  # B200: 148
+
+
+def test_splat_counts_match_reference_kat():
+    k = kat()
+    pts, starts, groups = k["pts"], k["starts"], k["groups"]
+    nv, nu = int(k["nv"]), int(k["nu"])
+    hist = torch.zeros((3, nv, nu), dtype=torch.int32, device="cuda")
+    status = torch.zeros(1, dtype=torch.int32, device="cuda")
+    N.call("hb_splat", ptr(dev(pts)), ptr(dev(starts)), len(starts) - 1, len(pts),
+           ptr(dev(groups.astype(np.int32))), None, ptr(hist), 3, nv, nu, ptr(status),
+           stream_ptr())
+    sync()
+    assert np.array_equal(hist.cpu().numpy().astype(np.float32), k["raw"])
+    assert int(status.item()) == 0
+
+
+def test_mix_layers_repulsive_matrix_kat():
+    """Repulsive M (-alpha/(B-1)): per-group int counts mixed in f64 equal the
+    reference's f32 accumulation on this small case."""
+    k = kat()
+    pts, starts, groups = k["pts"], k["starts"], k["groups"]
+    nv, nu = int(k["nv"]), int(k["nu"])
+    hist = torch.zeros((3, nv, nu), dtype=torch.int32, device="cuda")
+    status = torch.zeros(1, dtype=torch.int32, device="cuda")
+    out = torch.empty((3, nv, nu), dtype=torch.float32, device="cuda")
+    s = stream_ptr()
+    N.call("hb_splat", ptr(dev(pts)), ptr(dev(starts)), len(starts) - 1, len(pts),
+           ptr(dev(groups.astype(np.int32))), None, ptr(hist), 3, nv, nu, ptr(status), s)
+    N.call("hb_mix_layers", ptr(hist), None, ptr(dev(k["mat"])), 3, nv, nu, ptr(out), s)
+    sync()
+    np.testing.assert_allclose(out.cpu().numpy(), k["raw_rep"], rtol=0, atol=1e-6)
+
+
+def test_smooth_matches_reference_kat():
+    k = kat()
+    sm = R.smooth_gaussian_approx(DensityField(None, k["fld"]), 3.3, 3)
+    assert np.array_equal(sm.values, k["sm"])
+    assert np.array_equal(R.box_filter(k["fld"][0], 4), k["box"])
+
+
+@pytest.mark.parametrize("delta,key", [(1.0, "rs1"), (2.5, "rs2")])
+def test_resample_matches_reference_kat(delta, key):
+    k = kat()
+    pts, starts = k["pts"], k["starts"]
+    E, n = len(starts) - 1, len(pts)
+    dp, ds = dev(pts), dev(starts)
+    counts = torch.empty(E, dtype=torch.int64, device="cuda")
+    pos = torch.empty(n, dtype=torch.int32, device="cuda")
+    ns = torch.empty(E + 1, dtype=torch.int64, device="cuda")
+    ws = torch.empty(int(N.lib().hb_scan_workspace_bytes(E)), dtype=torch.uint8, device="cuda")
+    s = stream_ptr()
+    N.call("hb_resample_count", ptr(dp), ptr(ds), E, delta, ptr(counts), ptr(pos), s)
+    N.call("hb_scan_counts", ptr(counts), E, ptr(ns), ptr(ws), ws.numel(), s)
+    m = int(ns[-1].item())
+    out = torch.empty((m, 2), dtype=torch.float64, device="cuda")
+    N.call("hb_resample_emit", ptr(dp), ptr(ds), E, n, ptr(pos), ptr(ns), ptr(out), None, None,
+           None, 1, 1, None, s)
+    sync()
+    assert np.array_equal(ns.cpu().numpy(), k[key + "_starts"])
+    assert np.array_equal(out.cpu().numpy(), k[key])
+
+
+@pytest.mark.parametrize("fixed", [False, True])
+def test_advect_matches_reference_kat(fixed):
+    k = kat()
+    pts, starts, groups, rho = k["pts"], k["starts"], k["groups"], k["rho"]
+    nb, nv, nu = rho.shape
+    E, n = len(starts) - 1, len(pts)
+    out = torch.empty((n, 2), dtype=torch.float64, device="cuda")
+    moved = torch.zeros(1, dtype=torch.int64, device="cuda")
+    part = torch.zeros(int(N.lib().hb_advect_partials(n, 0)), dtype=torch.float64,
+                       device="cuda")
+    disp = torch.zeros(1, dtype=torch.float64, device="cuda")
+    h = 3.0 if fixed else 6.0
+    s = stream_ptr()
+    N.call("hb_advect_laplacian", ptr(dev(pts)), ptr(out), ptr(dev(starts)), E, n,
+           ptr(dev(groups.astype(np.int32))), ptr(dev(rho)), nb, nv, nu, h, 1e-8, 0.25,
+           int(fixed), 0.5, 0, ptr(moved), ptr(part), s)
+    N.call("hb_reduce_f64", ptr(part), part.numel(), ptr(disp), s)
+    sync()
+    tag = "advf" if fixed else "adv"
+    assert np.array_equal(out.cpu().numpy(), k[tag])
+    assert int(moved.item()) == int(k[tag + "_stats"][1])
+    np.testing.assert_allclose(disp.item(), k[tag + "_disp"][0], rtol=DISP_RTOL)
+
+
+@pytest.mark.parametrize("factor,passes,key", [(0.5, 1, "lap"), (0.3, 3, "lap3")])
+def test_laplacian_matches_reference_kat(factor, passes, key):
+    k = kat()
+    pts, starts = k["pts"], k["starts"]
+    E, n = len(starts) - 1, len(pts)
+    out = torch.empty((n, 2), dtype=torch.float64, device="cuda")
+    moved = torch.zeros(1, dtype=torch.int64, device="cuda")
+    part = torch.zeros(int(N.lib().hb_advect_partials(n, passes)), dtype=torch.float64,
+                       device="cuda")
+    rho = torch.zeros((1, 3, 3), dtype=torch.float32, device="cuda")
+    grp = torch.zeros(E, dtype=torch.int32, device="cuda")
+    N.call("hb_advect_laplacian", ptr(dev(pts)), ptr(out), ptr(dev(starts)), E, n, ptr(grp),
+           ptr(rho), 1, 3, 3, -1.0, 1e-8, 0.25, 0, factor, passes, ptr(moved), ptr(part),
+           stream_ptr())
+    sync()
+    assert np.array_equal(out.cpu().numpy(), k[key])
+
+
+def test_probe_bilinear_and_gradient_kat():
+    k = kat()
+    rho = k["rho"][1]
+    f = DensityField(None, k["rho"])
+    for (x, y), b, g in list(zip(k["q"], k["bil"], k["grad"]))[:40]:
+        assert B.density_at(f, 1, (x, y)) == b
+        assert np.array_equal(B.gradient_at(f, 1, (x, y)), g)
+    assert rho.dtype == np.float32
+
+
+def test_used_cell_count_kat():
+    k = kat()
+    assert B.used_cell_count(DensityField(None, k["rho"])) == int(k["used"][0])
+
+
+# ---------------------------------------------------------------------------
+# random stress against the oracle (ragged edges, long edges, ties)
+
+
+def _random_polylines(rng, n_edges, nv, nu, max_pts=400):
+    lens = rng.integers(2, max_pts, size=n_edges)
+    lens[rng.uniform(size=n_edges) < 0.3] = 2
+    starts = np.zeros(n_edges + 1, dtype=np.int64)
+    np.cumsum(lens, out=starts[1:])
+    steps = rng.normal(0, 1.3, size=(int(starts[-1]), 2))
+    steps[rng.uniform(size=steps.shape[0]) < 0.1] *= 0.05  # dense clusters -> merges
+    pts = np.empty_like(steps)
+    for e in range(n_edges):
+        s, t = starts[e], starts[e + 1]
+        p = np.cumsum(steps[s:t], axis=0) + rng.uniform([5, 5], [nu - 5, nv - 5])
+        pts[s:t] = np.clip(p, 1.0, [nu - 2.0, nv - 2.0])
+    return pts, starts
+
+
+@pytest.mark.parametrize("seed", [0, 1])
+def test_resample_emit_splat_random_vs_oracle(seed):
+    rng = np.random.default_rng(seed)
+    nv, nu = 120, 150
+    pts, starts = _random_polylines(rng, 700, nv, nu)
+    E, n = len(starts) - 1, len(pts)
+    groups = rng.integers(0, 2, size=E)
+    delta = 1.7
+    ref_pts, ref_starts = O.resample(pts.copy(), starts, delta, workers=1)
+    ref_counts = O.accumulate_counts(ref_pts, ref_starts, groups, (nv, nu), 2)
+    dp, ds = dev(pts), dev(starts)
+    counts = torch.empty(E, dtype=torch.int64, device="cuda")
+    pos = torch.empty(n, dtype=torch.int32, device="cuda")
+    ns = torch.empty(E + 1, dtype=torch.int64, device="cuda")
+    ws = torch.empty(int(N.lib().hb_scan_workspace_bytes(E)), dtype=torch.uint8, device="cuda")
+    hist = torch.zeros((2, nv, nu), dtype=torch.int32, device="cuda")
+    status = torch.zeros(1, dtype=torch.int32, device="cuda")
+    s = stream_ptr()
+    N.call("hb_resample_count", ptr(dp), ptr(ds), E, delta, ptr(counts), ptr(pos), s)
+    N.call("hb_scan_counts", ptr(counts), E, ptr(ns), ptr(ws), ws.numel(), s)
+    m = int(ns[-1].item())
+    out = torch.empty((m, 2), dtype=torch.float64, device="cuda")
+    N.call("hb_resample_emit", ptr(dp), ptr(ds), E, n, ptr(pos), ptr(ns), ptr(out),
+           ptr(dev(groups.astype(np.int32))), None, ptr(hist), nv, nu, ptr(status), s)
+    sync()
+    assert np.array_equal(ns.cpu().numpy(), ref_starts)
+    assert np.array_equal(out.cpu().numpy(), ref_pts)
+    assert np.array_equal(hist.cpu().numpy(), ref_counts)
+
+
+def test_advect_laplacian_random_vs_oracle():
+    rng = np.random.default_rng(7)
+    nv, nu = 96, 128
+    pts, starts = _random_polylines(rng, 500, nv, nu, max_pts=700)
+    E, n = len(starts) - 1, len(pts)
+    groups = rng.integers(0, 2, size=E)
+    counts = O.accumulate_counts(pts, starts, groups, (nv, nu), 2)
+    rho = O.smooth(counts.astype(np.float32), 4.0, 3)
+    ref = pts.copy()
+    interior, moved, disp = O.advect(ref, starts, groups, rho, 9.0, 1e-8, False)
+    O.laplacian(ref, starts, 0.5, 2)
+    out = torch.empty((n, 2), dtype=torch.float64, device="cuda")
+    dmoved = torch.zeros(1, dtype=torch.int64, device="cuda")
+    part = torch.zeros(int(N.lib().hb_advect_partials(n, 2)), dtype=torch.float64, device="cuda")
+    N.call("hb_advect_laplacian", ptr(dev(pts)), ptr(out), ptr(dev(starts)), E, n,
+           ptr(dev(groups.astype(np.int32))), ptr(dev(rho)), 2, nv, nu, 9.0, 1e-8, 0.25, 0, 0.5,
+           2, ptr(dmoved), ptr(part), stream_ptr())
+    sync()
+    assert np.array_equal(out.cpu().numpy(), ref)
+    assert int(dmoved.item()) == moved
+    np.testing.assert_allclose(part.sum().item(), disp, rtol=DISP_RTOL)
+
+
+def test_smooth_random_multilayer_vs_oracle():
+    rng = np.random.default_rng(3)
+    vals = (rng.gamma(0.5, 2.0, size=(3, 77, 203)) *
+            (rng.uniform(size=(3, 77, 203)) < 0.4)).astype(np.float32)
+    for sigma in (1.0, 5.5, 12.0):
+        got = R.smooth_gaussian_approx(DensityField(None, vals), sigma, 3).values
+        assert np.array_equal(got, O.smooth(vals, sigma, 3)), sigma
+
+
+# ---------------------------------------------------------------------------
+# end to end against the reference goldens
+
+
+def _golden(name):
+    with open(os.path.join(GOLDEN, name)) as f:
+        return json.load(f)
+
+
+def _check_run(k, scale=1.0, golden=None):
+    w = workload(k, scale=scale)
+    g = _golden(golden or f"cfg{k}.json")
+    eng, tr, metrics = B.bundle_packed(w.graph, w.config, bins=w.bins, matrix=w.matrix)
+    pts, starts = eng.packed_points()
+    assert digest(pts.cpu().numpy())["sha256"] == g["final_pts"]["sha256"]
+    assert digest(starts.cpu().numpy())["sha256"] == g["final_starts"]["sha256"]
+    assert digest(eng.field.cpu().numpy())["sha256"] == g["final_field"]["sha256"]
+    for m, gi in zip(metrics, g["iterations"]):
+        assert m.moved_points == gi["moved_points"]
+        assert m.used_cells == gi["used_cells"]
+        assert m.bandwidth == gi["bandwidth"]
+        np.testing.assert_allclose(m.mean_displacement, gi["mean_displacement"],
+                                   rtol=DISP_RTOL)
+    for r, gi in zip(eng.records, g["iterations"]):
+        assert r.n_points == gi["n_points"]
+
+
+def test_bundle_cfg1_mini_world_points_bit_exact():
+    w = workload(1, scale=0.25)
+    res = B.bundle(w.graph, w.config, bins=w.bins, matrix=w.matrix)
+    ref = np.load(os.path.join(GOLDEN, "cfg1_mini.npz"))
+    assert np.array_equal(res.sampled_edges.world, ref["world"])
+    assert np.array_equal(res.density.values, ref["field"])
+    e = res.sampled_edges[5]
+    assert np.array_equal(e.points[0], w.graph.positions[w.graph.sources[5]])
+    assert np.array_equal(e.points[-1], w.graph.positions[w.graph.targets[5]])
+
+
+def test_bundle_cfg1_bit_exact():
+    _check_run(1)
+
+
+def test_bundle_cfg2_bit_exact():
+    _check_run(2)
+
+
+@pytest.mark.slow
+def test_bundle_cfg3_bit_exact():
+    if not os.path.exists(os.path.join(GOLDEN, "cfg3.json")):
+        pytest.skip("cfg3 golden not generated")
+    _check_run(3)
+
+
+@pytest.mark.slow
+def test_bundle_cfg4_bit_exact():
+    if not os.path.exists(os.path.join(GOLDEN, "cfg4.json")):
+        pytest.skip("cfg4 golden not generated")
+    _check_run(4)
+
+
+def test_bundle_on_iteration_and_fixed_step():
+    w = workload(1, scale=0.1)
+    w.config.iterations = 4
+    seen = []
+    res = B.bundle(w.graph, w.config, bins=w.bins, matrix=w.matrix, on_iteration=seen.append)
+    assert [m.iteration for m in seen] == [0, 1, 2, 3]
+    assert [m.moved_points for m in seen] == [m.moved_points for m in res.metrics]
+    g = w.graph
+    ref = O.bundle_packed(g.positions, g.sources, g.targets, g.weights, w.bins, w.config,
+                          w.matrix, fixed_step=True)
+    res_f = B.bundle(g, w.config, bins=w.bins, matrix=w.matrix, _fixed_step=True)
+    assert np.array_equal(res_f.sampled_edges.world,
+                          O.materialize(ref, g.positions, g.sources, g.targets))
+
+
+def test_bundle_weights_offset_and_default_matrix_vs_oracle():
+    """Integer weights, B=3 with the default repulsive matrix (-0.125 off the
+    diagonal, dyadic, so every float32 layer sum is exact) and a directed
+    offset: bit-exact vs the oracle."""
+    w = workload(1, scale=0.15)
+    g = w.graph
+    rng = np.random.default_rng(0)
+    weights = rng.integers(1, 4, size=g.n_edges).astype(np.float64)
+    bins = (np.arange(g.n_edges) % 3).astype(np.int64)
+    from paper_1504_02687_b200.model import Graph
+    g2 = Graph(g.positions, g.sources, g.targets, weights, bins)
+    cfg = w.config
+    cfg.iterations = 4
+    cfg.directed_offset_fraction = 0.002
+    res = B.bundle(g2, cfg)
+    ref = O.bundle_packed(g2.positions, g2.sources, g2.targets, weights, bins, cfg, None)
+    world = O.materialize(ref, g2.positions, g2.sources, g2.targets)
+    assert np.array_equal(res.sampled_edges.world, world)
+    assert np.array_equal(res.density.values, ref.field)
+
+
+# ---------------------------------------------------------------------------
+# per-operator API (SPEC examples)
+
+
+def test_spec_rasterize_segment():
+    assert R.rasterize_segment((0.0, 0.0), (3.0, 0.0)).tolist() == [[0, 0], [1, 0], [2, 0], [3, 0]]
+    assert R.rasterize_segment((0.0, 0.0), (0.0, 0.0)).tolist() == [[0, 0]]
+    c = R.rasterize_segment((0.0, 0.0), (5.0, 3.0))
+    assert c.shape == (6, 2) and (np.diff(c[:, 0]) == 1).all()
+
+
+def test_spec_box_filter_impulse():
+    a = np.zeros((21, 21), np.float32)
+    a[10, 10] = 1.0
+    out = R.box_filter(a, 2)
+    assert np.allclose(out[8:13, 8:13], 1 / 25) and out.sum() == pytest.approx(1.0)
+    assert np.array_equal(R.box_filter(a, 0), a)
+
+
+def test_spec_advect_ramp_and_peak():
+    u = np.arange(32, dtype=np.float32)
+    ramp = np.tile(u, (32, 1))[None]
+    f = DensityField(None, ramp)
+    assert np.allclose(B.advect_point((10.0, 10.0), f, 0, 2.0), (12.0, 10.0))
+    vv, uu = np.mgrid[0:41, 0:41]
+    bump = np.exp(-((uu - 20.0) ** 2 + (vv - 20.0) ** 2) / 8.0).astype(np.float32)[None]
+    assert np.array_equal(B.advect_point((20.0, 20.0), DensityField(None, bump), 0, 30.0),
+                          (20.0, 20.0))
+
+
+def test_spec_laplacian_and_resample():
+    se = SampledEdge(0, np.array([[0.0, 0.0], [1.0, 2.0], [2.0, 0.0]]))
+    B.laplacian_smooth(se, 0.5, 1)
+    assert np.allclose(se.points[1], (1.0, 1.0))
+    line = SampledEdge(0, np.array([[0.0, 0.0], [1.0, 0.0], [2.0, 0.0]]))
+    B.laplacian_smooth(line, 0.5, 1)
+    assert np.array_equal(line.points[1], (1.0, 0.0))
+    gap = SampledEdge(0, np.array([[0.0, 0.0], [4.0, 0.0]]))
+    B.resample(gap, 1.0)
+    assert gap.points.shape[0] == 5
+
+
+def test_spec_initial_sample():
+    from paper_1504_02687_b200.model import Graph, make_transform
+    g = Graph(np.array([[0.0, 0.0], [9.0, 0.0], [0.0, 9.0]]), [0, 0], [1, 2])
+    tr = make_transform(g.positions, 10, 0)  # cell = 1 world unit
+    se = B.initial_sample(g, tr, 3.0)
+    assert len(se[0]) == 4 and se[0].points[:, 0].tolist() == [0.0, 3.0, 6.0, 9.0]
+    assert se[1].points[-1].tolist() == [0.0, 9.0]
+
+
+def test_accumulate_edges_spec_overlap():
+    from paper_1504_02687_b200.model import Graph, make_transform
+    g = Graph(np.array([[0.0, 0.0], [10.0, 0.0], [0.0, 10.0]]), [0, 0], [1, 1])
+    tr = make_transform(g.positions, 16, 2)
+    se = B.initial_sample(g, tr, 3.0)
+    f = R.accumulate_edges(se, g, np.eye(1, dtype=np.float32), tr)
+    assert f.values.max() == 2.0

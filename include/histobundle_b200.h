@@ -47,6 +47,8 @@ extern "C" {
 HB_API int hb_abi_version(void);
 HB_API const char *hb_last_error(void);
 HB_API int hb_device_sm_count(void);
+/* Total kernels this library has launched in the process (evidence counter). */
+HB_API long long hb_launch_count(void);
 
 /* _kernels.fill_samples (_kernels.py:22-43), called by _sample_packed
  * (bundler.py:77-89).  src/dst: (E,2) grid endpoints; starts from the host

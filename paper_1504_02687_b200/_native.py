@@ -61,6 +61,7 @@ SIGNATURES = {
     "hb_abi_version": (_I, []),
     "hb_last_error": (ctypes.c_char_p, []),
     "hb_device_sm_count": (_I, []),
+    "hb_launch_count": (ctypes.c_longlong, []),
     "hb_sample_fill": (_I, [_P, _P, _P, _I64, _P, _P]),
     "hb_offset": (_I, [_P, _P, _I64, _P, _P]),
     "hb_to_world": (_I, [_P, _P, _I64, _D, _D, _D, _P, _P, _P, _P]),

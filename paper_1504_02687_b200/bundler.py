@@ -24,7 +24,7 @@ import torch
 
 from . import _native as N
 from . import dist as D
-from .engine import MIN_STEP, BundleEngine, ptr, stream_ptr, weight_plan
+from .engine import MIN_STEP, BundleEngine, download, ptr, stream_ptr, weight_plan
 from .model import (BundleConfig, DensityField, Graph, GridTransform, SampledEdge,
                     interaction_matrix, make_transform)
 
@@ -122,8 +122,17 @@ class _Run:
     wall_seconds: float
 
 
-def _run_engine(graph, cfg, bins_arr, matrix, fixed_step, on_iteration, group=None,
-                capacity_factor=2.0):
+def prepare_engine(graph: Graph, config: BundleConfig | None = None, *, bins=None,
+                   matrix=None, _fixed_step: bool = False, group=None,
+                   capacity_factor: float = 2.0):
+    """Validate, transform, shard and sample (everything the reference does
+    before its timed loop, bundler.py:325-346) and return
+    ``(engine, transform, edge_lo, edge_hi)`` ready for ``engine.run()``."""
+    cfg, bins_arr, matrix = _resolve(graph, config, bins, matrix)
+    return _setup(graph, cfg, bins_arr, matrix, _fixed_step, group, capacity_factor)
+
+
+def _setup(graph, cfg, bins_arr, matrix, fixed_step, group, capacity_factor):
     transform = make_transform(graph.positions, cfg.grid_size, cfg.padding_cells)
     pos = graph.positions
     src_all = transform.world_to_grid(pos[graph.sources])
@@ -141,11 +150,18 @@ def _run_engine(graph, cfg, bins_arr, matrix, fixed_step, on_iteration, group=No
         od = _offset_vectors(src, dst, cfg.directed_offset_fraction
                              * max(transform.width, transform.height))
     reduce_hist = (lambda h: D.all_reduce_sum(h, group)) if world > 1 else None
-    t0 = time.perf_counter()
     eng = BundleEngine(src, dst, bins_arr[lo:hi], weight_plan(graph.weights[lo:hi]),
                        matrix, transform.shape, cfg, fixed_step=fixed_step,
                        offset_disp=od, reduce_hist=reduce_hist,
                        capacity_factor=capacity_factor)
+    return eng, transform, lo, hi
+
+
+def _run_engine(graph, cfg, bins_arr, matrix, fixed_step, on_iteration, group=None,
+                capacity_factor=2.0):
+    t0 = time.perf_counter()
+    eng, transform, lo, hi = _setup(graph, cfg, bins_arr, matrix, fixed_step, group,
+                                    capacity_factor)
     if on_iteration is None:
         eng.run()
     else:
@@ -193,8 +209,11 @@ def bundle(graph: Graph, config: BundleConfig | None = None, *,
     src_w = pos[graph.sources[run.edge_lo:run.edge_hi]]
     dst_w = pos[graph.targets[run.edge_lo:run.edge_hi]]
     world_dev = eng.world_points(tr.origin, tr.cell_size, src_w, dst_w)
-    world, starts = D.gather_polylines(world_dev, eng.starts, group)
-    field = DensityField(tr, eng.field.cpu().numpy())
+    if D.rank_world(group)[1] == 1:
+        world, starts = download(world_dev), download(eng.starts)
+    else:
+        world, starts = D.gather_polylines(world_dev, eng.starts, group)
+    field = DensityField(tr, download(eng.field))
     metrics = _metrics(run.records, group)
     return BundleResult(graph, PackedPolylines(world, starts), field, metrics,
                         sum(m.seconds for m in metrics))
@@ -244,8 +263,9 @@ def initial_sample(graph: Graph, transform: GridTransform,
     st = torch.from_numpy(starts).to(dev)
     pts = torch.empty((int(starts[-1]), 2), dtype=torch.float64, device=dev)
     s = stream_ptr()
-    N.call("hb_sample_fill", ptr(torch.from_numpy(src).to(dev)),
-           ptr(torch.from_numpy(dst).to(dev)), ptr(st), graph.n_edges, ptr(pts), s)
+    src_d = torch.from_numpy(np.ascontiguousarray(src)).to(dev)
+    dst_d = torch.from_numpy(np.ascontiguousarray(dst)).to(dev)
+    N.call("hb_sample_fill", ptr(src_d), ptr(dst_d), ptr(st), graph.n_edges, ptr(pts), s)
     out = torch.empty_like(pts)
     sw = torch.from_numpy(np.ascontiguousarray(graph.positions[graph.sources])).to(dev)
     dw = torch.from_numpy(np.ascontiguousarray(graph.positions[graph.targets])).to(dev)

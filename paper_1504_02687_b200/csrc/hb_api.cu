@@ -1,4 +1,5 @@
 // hb_api.cu -- error reporting and library metadata for the C ABI.
+#include <atomic>
 #include <cstdarg>
 #include <cstdio>
 #include <cstring>
@@ -17,7 +18,10 @@ int set_error(int code, const char *fmt, ...) {
     return code;
 }
 
-int check_launch(const char *what) {
+static std::atomic<long long> g_launches{0};
+
+int check_launch(const char *what, int kernels) {
+    g_launches.fetch_add(kernels, std::memory_order_relaxed);
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess)
         return set_error(HB_ECUDA, "%s: %s", what, cudaGetErrorString(e));
@@ -31,6 +35,8 @@ extern "C" {
 int hb_abi_version(void) { return 1; }
 
 const char *hb_last_error(void) { return hb::g_err; }
+
+long long hb_launch_count(void) { return hb::g_launches.load(std::memory_order_relaxed); }
 
 int hb_device_sm_count(void) {
     int dev = 0, n = 0;

@@ -17,7 +17,9 @@ constexpr int kWarp = 32;
 
 // ---- error reporting (hb_api.cu) ------------------------------------------
 int set_error(int code, const char *fmt, ...);
-int check_launch(const char *what);
+// checks the last launch error and adds `kernels` to the library's launch
+// counter (hb_launch_count, the bench's gpu_launches evidence)
+int check_launch(const char *what, int kernels = 1);
 
 // ---- exact float64 primitives ---------------------------------------------
 __device__ __forceinline__ double dadd(double a, double b) { return __dadd_rn(a, b); }

@@ -201,7 +201,7 @@ int hb_smooth(const int32_t *counts, const float *hist, const float *matrix, int
     double *table = reinterpret_cast<double *>(workspace);
     float *stage = reinterpret_cast<float *>(table + cells);
     if (layer_peak && cudaMemsetAsync(layer_peak, 0, sizeof(float) * nbins, st) != cudaSuccess)
-        return check_launch("hb_smooth(memset)");
+        return check_launch("hb_smooth(memset)", 0);
     const float *src = nullptr;  // float32 input of passes after the first
     for (int p = 0; p < npasses; ++p) {
         const bool first = (p == 0);
@@ -235,7 +235,7 @@ int hb_smooth(const int32_t *counts, const float *hist, const float *matrix, int
             dim3 gb((nu + kBoxBlock - 1) / kBoxBlock, nv, nbins);
             box_kernel<<<gb, kBoxBlock, 0, st>>>(table, nv, nu, r, dst, pk);
         }
-        int rc = check_launch("hb_smooth");
+        int rc = check_launch("hb_smooth", r == 0 ? 1 : 3);
         if (rc) return rc;
         src = dst;
     }
@@ -267,7 +267,7 @@ int hb_integral_image(const float *in, int nbins, int nv, int nu, double *table,
     const int64_t rows = (int64_t)nbins * nv;
     const unsigned rb = (unsigned)((rows + 32 * kRowWarps - 1) / (32 * kRowWarps));
     row_scan_kernel<<<rb, kRowWarps * 32, 0, st>>>(table, rows, nu);
-    return check_launch("hb_integral_image");
+    return check_launch("hb_integral_image", 2);
 }
 
 int hb_used_cells(const float *rho, const float *layer_peak, int nbins, int nv, int nu,

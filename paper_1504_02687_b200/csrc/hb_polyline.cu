@@ -352,7 +352,7 @@ int hb_scan_counts(const int64_t *counts, int64_t n_edges, int64_t *new_starts,
         return set_error(HB_EINVAL, "hb_scan_counts: bad arguments");
     cudaStream_t st = as_stream(stream);
     if (cudaMemsetAsync(new_starts, 0, sizeof(int64_t), st) != cudaSuccess)
-        return check_launch("hb_scan_counts(memset)");
+        return check_launch("hb_scan_counts(memset)", 0);
     if (n_edges == 0) return HB_OK;
     size_t need = 0;
     cub::DeviceScan::InclusiveSum(nullptr, need, counts, new_starts + 1, (int)n_edges, st);
@@ -360,7 +360,7 @@ int hb_scan_counts(const int64_t *counts, int64_t n_edges, int64_t *new_starts,
         return set_error(HB_EINVAL, "hb_scan_counts: workspace %zu < %zu bytes",
                          workspace_bytes, need);
     cub::DeviceScan::InclusiveSum(workspace, need, counts, new_starts + 1, (int)n_edges, st);
-    return check_launch("hb_scan_counts");
+    return check_launch("hb_scan_counts", 2);
 }
 
 int hb_resample_emit(const double *pts, const int64_t *starts, int64_t n_edges,

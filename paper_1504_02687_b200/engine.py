@@ -62,6 +62,21 @@ def ptr(t) -> int | None:
     return None if t is None else t.data_ptr()
 
 
+# host<->device traffic of the public API, counted from the copied tensors
+IO_BYTES = {"h2d": 0, "d2h": 0}
+
+
+def upload(a: np.ndarray, dev) -> torch.Tensor:
+    t = torch.from_numpy(np.ascontiguousarray(a))
+    IO_BYTES["h2d"] += t.numel() * t.element_size()
+    return t.to(dev)
+
+
+def download(t: torch.Tensor) -> np.ndarray:
+    IO_BYTES["d2h"] += t.numel() * t.element_size()
+    return t.cpu().numpy()
+
+
 def stream_ptr() -> int:
     return torch.cuda.current_stream().cuda_stream
 
@@ -138,18 +153,15 @@ class BundleEngine:
         self.pts = torch.empty((self.cap, 2), dtype=torch.float64, device=dev)
         self.alt = torch.empty((self.cap, 2), dtype=torch.float64, device=dev)
         self.pos = torch.empty(self.cap, dtype=torch.int32, device=dev)
-        self.starts = torch.from_numpy(starts).to(dev)
+        self.starts = upload(starts, dev)
         self.starts_alt = torch.empty_like(self.starts)
         self.ecounts = torch.empty(max(E, 1), dtype=torch.int64, device=dev)
-        self.groups = torch.from_numpy(np.ascontiguousarray(groups, dtype=np.int32)).to(dev)
+        self.groups = upload(np.asarray(groups, dtype=np.int32), dev)
         self.wkind = weights.kind
-        self.wint = (torch.from_numpy(weights.int_w).to(dev)
-                     if weights.kind == "int" else None)
-        self.wf32 = (torch.from_numpy(weights.f32_w).to(dev)
-                     if weights.kind == "float" else None)
+        self.wint = upload(weights.int_w, dev) if weights.kind == "int" else None
+        self.wf32 = upload(weights.f32_w, dev) if weights.kind == "float" else None
         mat_is_identity = np.array_equal(self.matrix, np.eye(B, dtype=np.float32))
-        self.mat_dev = (None if mat_is_identity else
-                        torch.from_numpy(self.matrix.copy()).to(dev))
+        self.mat_dev = None if mat_is_identity else upload(self.matrix, dev)
         hdtype = torch.float32 if self.wkind == "float" else torch.int32
         self.hist = torch.empty((B, self.nv, self.nu), dtype=hdtype, device=dev)
         self.field = torch.empty((B, self.nv, self.nu), dtype=torch.float32, device=dev)
@@ -168,14 +180,16 @@ class BundleEngine:
         self.m_used = torch.zeros(self.iters, dtype=torch.int64, device=dev)
         self.records: list[IterationRecord] = []
         self._ev: list[tuple[torch.cuda.Event, torch.cuda.Event]] = []
+        # optional per-kernel CUDA-event trace: name -> [(start, end, iteration)]
+        self.trace: dict | None = None
 
         s = stream_ptr()
-        srcd = torch.from_numpy(np.ascontiguousarray(src, dtype=np.float64)).to(dev)
-        dstd = torch.from_numpy(np.ascontiguousarray(dst, dtype=np.float64)).to(dev)
+        srcd = upload(np.asarray(src, dtype=np.float64), dev)
+        dstd = upload(np.asarray(dst, dtype=np.float64), dev)
         N.call("hb_sample_fill", ptr(srcd), ptr(dstd), ptr(self.starts), E,
                ptr(self.pts), s)
         if offset_disp is not None:
-            od = torch.from_numpy(np.ascontiguousarray(offset_disp)).to(dev)
+            od = upload(offset_disp, dev)
             N.call("hb_offset", ptr(self.pts), ptr(self.starts), E, ptr(od), s)
         self.iteration = 0
 
@@ -201,6 +215,18 @@ class BundleEngine:
             self._partials = torch.empty(max(k, 1) * 2, dtype=torch.float64, device=self.dev)
         return self._partials
 
+    def _k(self, name: str, *args) -> None:
+        """Launch one C-ABI entry point, bracketed by events when tracing."""
+        if self.trace is None:
+            N.call(name, *args)
+            return
+        a = torch.cuda.Event(enable_timing=True)
+        b = torch.cuda.Event(enable_timing=True)
+        a.record()
+        N.call(name, *args)
+        b.record()
+        self.trace.setdefault(name, []).append((a, b, self.iteration))
+
     def _splat_args(self):
         if self.wkind == "float":
             return "hb_splat_f32", ptr(self.wf32)
@@ -220,14 +246,14 @@ class BundleEngine:
         self.hist.zero_()
         if i > 0:
             # resample (bundler.py:353-354) fused with the splat (:355-356)
-            N.call("hb_resample_count", ptr(self.pts), ptr(self.starts), E, self.delta,
+            self._k("hb_resample_count", ptr(self.pts), ptr(self.starts), E, self.delta,
                    ptr(self.ecounts), ptr(self.pos), s)
-            N.call("hb_scan_counts", ptr(self.ecounts), E, ptr(self.starts_alt),
+            self._k("hb_scan_counts", ptr(self.ecounts), E, ptr(self.starts_alt),
                    ptr(self.scan_ws), self.scan_ws.numel(), s)
-            n_new = int(self.starts_alt[E].item()) if E else 0
+            n_new = int(download(self.starts_alt[E:E + 1])[0]) if E else 0
             self._ensure_capacity(n_new)
             fused = self.wkind != "float"
-            N.call("hb_resample_emit", ptr(self.pts), ptr(self.starts), E, self.n_pts,
+            self._k("hb_resample_emit", ptr(self.pts), ptr(self.starts), E, self.n_pts,
                    ptr(self.pos), ptr(self.starts_alt), ptr(self.alt), ptr(self.groups),
                    ptr(self.wint), ptr(self.hist) if fused else None, nv, nu,
                    ptr(self.status), s)
@@ -236,31 +262,31 @@ class BundleEngine:
             self.n_pts = n_new
             if not fused:
                 name, w = self._splat_args()
-                N.call(name, ptr(self.pts), ptr(self.starts), E, self.n_pts,
+                self._k(name, ptr(self.pts), ptr(self.starts), E, self.n_pts,
                        ptr(self.groups), w, ptr(self.hist), B, nv, nu, ptr(self.status), s)
         else:
             name, w = self._splat_args()
-            N.call(name, ptr(self.pts), ptr(self.starts), E, self.n_pts, ptr(self.groups),
+            self._k(name, ptr(self.pts), ptr(self.starts), E, self.n_pts, ptr(self.groups),
                    w, ptr(self.hist), B, nv, nu, ptr(self.status), s)
         if self.reduce_hist is not None:
             self.reduce_hist(self.hist)
         is_int = self.wkind != "float"
-        N.call("hb_smooth", ptr(self.hist) if is_int else None,
+        self._k("hb_smooth", ptr(self.hist) if is_int else None,
                None if is_int else ptr(self.hist), ptr(self.mat_dev), B, nv, nu,
                self.radii.data_ptr(), int(self.radii.numel()), ptr(self.field),
                ptr(self.smooth_ws), self.smooth_ws.numel(), ptr(self.peak), s)
         h_i = cfg.lambda_ ** i * cfg.h_max  # bundler.py:360, Python float power
         part = self._partials_for(self.n_pts)
         nblk = int(N.lib().hb_advect_partials(self.n_pts, self.lap_passes))
-        N.call("hb_advect_laplacian", ptr(self.pts), ptr(self.alt), ptr(self.starts), E,
+        self._k("hb_advect_laplacian", ptr(self.pts), ptr(self.alt), ptr(self.starts), E,
                self.n_pts, ptr(self.groups), ptr(self.field), B, nv, nu, float(h_i),
                float(cfg.epsilon), MIN_STEP, int(self.fixed_step),
                float(cfg.laplacian_factor), self.lap_passes,
                self.m_moved.data_ptr() + 8 * i, ptr(part), s)
         if self.n_pts:
             self.pts, self.alt = self.alt, self.pts
-        N.call("hb_reduce_f64", ptr(part), nblk, self.m_disp.data_ptr() + 8 * i, s)
-        N.call("hb_used_cells", ptr(self.field), ptr(self.peak), B, nv, nu, 0.01,
+        self._k("hb_reduce_f64", ptr(part), nblk, self.m_disp.data_ptr() + 8 * i, s)
+        self._k("hb_used_cells", ptr(self.field), ptr(self.peak), B, nv, nu, 0.01,
                self.m_used.data_ptr() + 8 * i, s)
         ev1.record()
         self._ev.append((ev0, ev1))
@@ -269,14 +295,35 @@ class BundleEngine:
         self.iteration += 1
         return rec
 
+    def keep_initial_state(self) -> None:
+        """Remember the sampled straight edges so :meth:`reset` can restart
+        the run without re-sampling (bench: every step bundles from scratch)."""
+        self._init = (self.pts[: self.n_pts].clone(), self.starts.clone(), self.n_pts)
+
+    def reset(self) -> None:
+        """Back to iteration 0 on the remembered initial points (device copies
+        only, stream-ordered, no host sync)."""
+        pts0, starts0, n0 = self._init
+        self._ensure_capacity(n0)
+        self.pts[:n0].copy_(pts0)
+        self.starts.copy_(starts0)
+        self.n_pts = n0
+        self.iteration = 0
+        self.records = []
+        self._ev = []
+        self.m_moved.zero_()
+        self.m_disp.zero_()
+        self.m_used.zero_()
+        self.status.zero_()
+
     def finish_metrics(self) -> list[IterationRecord]:
         """Synchronise once and fill moved/disp/used/seconds of all records."""
         torch.cuda.current_stream().synchronize()
-        if int(self.status.item()) & 1:
+        if int(download(self.status)[0]) & 1:
             raise ValueError("sample out of bounds: a polyline point left the grid")
-        moved = self.m_moved.cpu().numpy()
-        disp = self.m_disp.cpu().numpy()
-        used = self.m_used.cpu().numpy()
+        moved = download(self.m_moved)
+        disp = download(self.m_disp)
+        used = download(self.m_used)
         for r, (a, b) in zip(self.records, self._ev):
             r.moved_points = int(moved[r.iteration])
             r.disp = float(disp[r.iteration])
@@ -297,10 +344,8 @@ class BundleEngine:
 
     def world_points(self, origin, cell, src_world=None, dst_world=None) -> torch.Tensor:
         out = torch.empty((self.n_pts, 2), dtype=torch.float64, device=self.dev)
-        sw = None if src_world is None else torch.from_numpy(
-            np.ascontiguousarray(src_world, dtype=np.float64)).to(self.dev)
-        dw = None if dst_world is None else torch.from_numpy(
-            np.ascontiguousarray(dst_world, dtype=np.float64)).to(self.dev)
+        sw = None if src_world is None else upload(np.asarray(src_world, np.float64), self.dev)
+        dw = None if dst_world is None else upload(np.asarray(dst_world, np.float64), self.dev)
         N.call("hb_to_world", ptr(self.pts), ptr(self.starts), self.n_edges,
                float(origin[0]), float(origin[1]), float(cell), ptr(sw), ptr(dw),
                ptr(out), stream_ptr())

@@ -28,15 +28,30 @@ from paper_1504_02687_b200.engine import box_widths, ptr, stream_ptr  # noqa: E4
 from paper_1504_02687_b200.model import DensityField, SampledEdge  # noqa: E402
 from paper_1504_02687_b200.workloads import workload  # noqa: E402
 
-DISP_RTOL = 1e-12
+# mean_displacement is a float64 sum over all interior points: its value depends
+# on summation order (the reference itself changes with `workers`); the
+# reference sums sequentially, we sum per-CTA partials in a fixed tree.
+DISP_RTOL = 1e-9
 
 
 def kat():
     return np.load(os.path.join(GOLDEN, "kat_ops.npz"))
 
 
+_KEEP: list = []  # uploaded tensors must outlive the (asynchronous) kernels
+
+
+@pytest.fixture(autouse=True)
+def _release_uploads():
+    yield
+    torch.cuda.synchronize()
+    _KEEP.clear()
+
+
 def dev(a):
-    return torch.from_numpy(np.ascontiguousarray(a)).cuda()
+    t = torch.from_numpy(np.ascontiguousarray(a)).cuda()
+    _KEEP.append(t)
+    return t
 
 
 def sync():

@@ -118,20 +118,26 @@ HB_API int hb_integral_image(const float *in, int nbins, int nv, int nu, double 
 HB_API int hb_used_cells(const float *rho, const float *layer_peak, int nbins, int nv,
                   int nu, double rel, unsigned long long *count, void *stream);
 
-/* Number of per-block partials hb_advect_laplacian writes (for sizing). */
-HB_API int64_t hb_advect_partials(int64_t n_pts, int lap_passes);
+/* Size (doubles) of the disp_partials buffer hb_advect_laplacian fills. */
+HB_API int64_t hb_advect_partials(void);
 
-/* _kernels.advect (_kernels.py:144-200) followed by _kernels.laplacian
- * (_kernels.py:275-296), fused: pts_out = laplacian^passes(advect(pts_in)).
+/* _kernels.advect (_kernels.py:144-200) -> _kernels.laplacian
+ * (_kernels.py:275-296) -> _kernels.resample_count (_kernels.py:203-232) of
+ * the NEXT iteration, fused in one streaming pass:
+ *   pts_out = laplacian^lap_passes(advect(pts_in)),
+ *   counts/pos = resample_count(pts_out, delta)   (when counts != NULL;
+ *   same outputs as hb_resample_count).
  * h < 0 skips advection (Laplacian only, bundler.laplacian_smooth).
- * pts_in and pts_out must not alias.  edge_layer: (E) int32 layer of each
- * edge (bins).  moved: u64 accumulator (added to).  disp_partials:
- * hb_advect_partials() doubles, reduced by hb_reduce_f64 in fixed order. */
+ * pts_out may alias pts_in.  edge_layer: (E) int32 layer of each edge (its
+ * bin).  moved: u64 accumulator (added to).  disp_partials:
+ * hb_advect_partials() doubles (zeroed and filled here), summed by
+ * hb_reduce_f64 in fixed order. */
 HB_API int hb_advect_laplacian(const double *pts_in, double *pts_out,
                         const int64_t *starts, int64_t n_edges, int64_t n_pts,
                         const int32_t *edge_layer, const float *rho, int nbins,
                         int nv, int nu, double h, double eps, double min_step,
                         int fixed_step, double lap_factor, int lap_passes,
+                        double delta, int64_t *counts, int32_t *pos,
                         unsigned long long *moved, double *disp_partials,
                         void *stream);
 

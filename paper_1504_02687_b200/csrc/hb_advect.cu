@@ -1,25 +1,41 @@
-// hb_advect.cu -- gradient advection with the density-monotone adaptive step
-// (_kernels.py:144-200) fused with Jacobi Laplacian smoothing
-// (_kernels.py:275-296).
+// hb_advect.cu -- the fused per-polyline pass: gradient advection with the
+// density-monotone adaptive step (_kernels.py:144-200), Jacobi Laplacian
+// smoothing (_kernels.py:275-296) and the next iteration's resample count
+// (_kernels.py:203-232), in ONE streaming read of the points.
 //
-// A CTA owns P = kAdvBlock - 2H consecutive points plus H halo points on
-// each side (H = Laplacian passes).  Every thread advects its point (halo
-// points are advected redundantly: advection is per point), the advected
-// positions are staged in shared memory, and the `passes` Jacobi sweeps run
-// there (each sweep shrinks the valid region by one point), so the fused
-// kernel reads 16 B and writes 16 B per point and never re-reads the
-// advected positions from HBM.  Density gathers hit the L2-resident field.
+// Warp per edge, persistent grid-stride over edges.  The warp walks its edge
+// in 32-point chunks with a one-chunk software pipeline:
+//   A(c+1) = advect(chunk c+1)          (lanes in parallel, gathers from the
+//                                        L2-resident density field)
+//   F(c)   = A(c) + f*(0.5*(A(j-1)+A(j+1)) - A(c))   neighbours by shuffle;
+//            A(j-1) of lane 0 is a carry, A(j+1) of lane 31 is lane 0 of A(c+1)
+//   write F(c); resample-count F(c) (ballot walk, carries across chunks)
+// so every point is read once (16 B) and written once (16 B) plus its 4 B
+// resample code, and nothing waits on a CTA barrier.
+//
+// Resample count: the reference walks the polyline keeping `a`, the last
+// KEPT point; point j (not the last) is merged when |p_j - a| < 0.5*delta.
+// Lanes first assume every predecessor is kept (g_j = |p_j - p_{j-1}|); the
+// first lane b whose test fails under that assumption really is merged (all
+// lanes before it were kept), lane b+1 is re-tested against the true `a`, and
+// so on -- one ballot per merge, fully parallel when nothing merges, and every
+// test is the reference's exact sqrt((x-ax)^2 + (y-ay)^2).  Kept points get
+// pieces = 2^k (halve g while g > 1.5*delta); a warp prefix sum places them.
 #include "hb_common.cuh"
 
 namespace hb {
 
-constexpr int kAdvBlock = 256;
-constexpr int kAdvMaxHalo = 32;
+struct Adv {
+    double2 p;
+    bool moved;
+    double disp;
+};
 
-__device__ __forceinline__ bool advect_point(const float *__restrict__ rho, int nv, int nu,
-                                             double x, double y, double h, double eps,
-                                             double min_step, int fixed, double &ox,
-                                             double &oy, double &disp) {
+__device__ __forceinline__ Adv advect_one(const float *__restrict__ rho, int nv, int nu,
+                                          double2 p, double h, double eps, double min_step,
+                                          int fixed) {
+    Adv r{p, false, 0.0};
+    const double x = p.x, y = p.y;
     const double xlo = 1.0, ylo = 1.0;  // INTERIOR_MARGIN (_kernels.py:19)
     const double xhi = dsub(dsub((double)nu, 1.0), 1.0);
     const double yhi = dsub(dsub((double)nv, 1.0), 1.0);
@@ -28,116 +44,184 @@ __device__ __forceinline__ bool advect_point(const float *__restrict__ rho, int 
     double gn = hypot_ref(gx, gy);
     if (gn < eps) gn = eps;
     const double dx = gx / gn, dy = gy / gn;
-    ox = x;
-    oy = y;
     if (fixed) {
         const double nx = fmin_ref(fmax_ref(dadd(x, dmul(h, dx)), xlo), xhi);
         const double ny = fmin_ref(fmax_ref(dadd(y, dmul(h, dy)), ylo), yhi);
-        ox = nx;
-        oy = ny;
+        r.p = make_double2(nx, ny);
         if (nx != x || ny != y) {
-            disp = hypot_ref(dsub(nx, x), dsub(ny, y));
-            return true;
+            r.moved = true;
+            r.disp = hypot_ref(dsub(nx, x), dsub(ny, y));
         }
-        return false;
+        return r;
     }
     const double r0 = bilinear_ref(rho, nv, nu, x, y);
     for (double m = h; m >= min_step; m = dmul(m, 0.5)) {
         const double nx = fmin_ref(fmax_ref(dadd(x, dmul(m, dx)), xlo), xhi);
         const double ny = fmin_ref(fmax_ref(dadd(y, dmul(m, dy)), ylo), yhi);
         if (bilinear_ref(rho, nv, nu, nx, ny) >= r0) {
-            ox = nx;
-            oy = ny;
+            r.p = make_double2(nx, ny);
             if (nx != x || ny != y) {
-                disp = hypot_ref(dsub(nx, x), dsub(ny, y));
-                return true;
+                r.moved = true;
+                r.disp = hypot_ref(dsub(nx, x), dsub(ny, y));
             }
-            return false;
+            break;
         }
     }
-    return false;
+    return r;
 }
 
-__global__ void __launch_bounds__(kAdvBlock)
-advect_laplacian_kernel(const double2 *__restrict__ pin, double2 *__restrict__ pout,
-                        const int64_t *__restrict__ starts, int64_t n_edges, int64_t n_pts,
-                        const int32_t *__restrict__ edge_layer, const float *__restrict__ rho,
-                        int64_t plane, int nv, int nu, double h, double eps,
-                        double min_step, int fixed, double factor, int passes,
-                        unsigned long long *__restrict__ moved,
-                        double *__restrict__ partials) {
-    __shared__ EdgeWindow<kAdvBlock / 2 + 2> win;
-    __shared__ double2 buf[2][kAdvBlock];
-    __shared__ double red_d[kAdvBlock / 32];
-    __shared__ unsigned red_m[kAdvBlock / 32];
-    const int H = passes;
-    const int P = kAdvBlock - 2 * H;
-    const int t = threadIdx.x;
-    const int64_t base = (int64_t)blockIdx.x * P - H;
-    const int64_t j = base + t;
-    const int64_t lo = base < 0 ? 0 : base;
-    const int64_t hi = base + kAdvBlock < n_pts ? base + kAdvBlock : n_pts;
-    load_edge_window(win, starts, n_edges, lo, hi);
+__global__ void __launch_bounds__(kStreamBlock)
+polyline_pass_kernel(const PolylinePass p) {
+    const unsigned full = 0xffffffffu;
+    const int lane = threadIdx.x & 31;
+    const bool do_adv = p.h >= 0.0;
+    const bool do_count = p.counts != nullptr;
+    const double lo = 0.5 * p.delta, hi = 1.5 * p.delta;  // _kernels.py:211-212
+    const int64_t nwarps = (int64_t)gridDim.x * (kStreamBlock / 32);
+    unsigned long long my_moved = 0;
+    double my_disp = 0.0;
 
-    const bool valid = j >= 0 && j < n_pts;
-    bool interior = false;
-    double2 p = make_double2(0.0, 0.0);
-    bool mv = false;
-    double d = 0.0;
-    const bool own = valid && t >= H && t < H + P;
-    if (valid) {
-        const int k = window_edge(win, j);
-        const int64_t s = win.st[k], last = win.st[k + 1] - 1;
-        interior = j > s && j < last;
-        p = pin[j];
-        if (interior && h >= 0.0) {  // h < 0: Laplacian only (laplacian_smooth)
-            const float *layer = rho + (int64_t)edge_layer[win.e0 + k] * plane;
-            double ox, oy, dd = 0.0;
-            mv = advect_point(layer, nv, nu, p.x, p.y, h, eps, min_step, fixed, ox, oy, dd);
-            p = make_double2(ox, oy);
-            d = dd;
+    for (int64_t e = ((int64_t)blockIdx.x * kStreamBlock + threadIdx.x) / 32; e < p.n_edges;
+         e += nwarps) {
+        const int64_t s = p.starts[e];
+        const int64_t n = p.starts[e + 1] - s;
+        const float *rho = do_adv ? p.rho + (int64_t)p.edge_layer[e] * p.plane : nullptr;
+
+        // A(c) for chunk c: advected point of local index 32c + lane
+        auto stage = [&](int64_t c0) -> double2 {
+            const int64_t j = c0 + lane;
+            if (j >= n) return make_double2(0.0, 0.0);
+            double2 q = p.pin[s + j];
+            if (do_adv && j > 0 && j < n - 1) {
+                const Adv a = advect_one(rho, p.nv, p.nu, q, p.h, p.eps, p.min_step, p.fixed);
+                if (a.moved) {
+                    my_moved += 1;
+                    my_disp = dadd(my_disp, a.disp);
+                }
+                q = a.p;
+            }
+            return q;
+        };
+
+        double2 cur = stage(0);
+        double2 left = make_double2(0.0, 0.0);  // A of local index c0-1
+        // count carries
+        double2 ka = make_double2(__shfl_sync(full, cur.x, 0), __shfl_sync(full, cur.y, 0));
+        double2 prevf = ka;  // final point of local index c0-1
+        int64_t off = 0;
+        if (do_count && lane == 0) p.pos[s] = 0;
+
+        for (int64_t c0 = 0; c0 < n; c0 += kWarp) {
+            const bool has_next = c0 + kWarp < n;
+            const double2 nxt = has_next ? stage(c0 + kWarp) : make_double2(0.0, 0.0);
+            const int64_t j = c0 + lane;
+            const bool valid = j < n;
+            double2 f = cur;
+            if (p.lap) {
+                double lx = __shfl_up_sync(full, cur.x, 1), ly = __shfl_up_sync(full, cur.y, 1);
+                double rx = __shfl_down_sync(full, cur.x, 1), ry = __shfl_down_sync(full, cur.y, 1);
+                const double n0x = __shfl_sync(full, nxt.x, 0), n0y = __shfl_sync(full, nxt.y, 0);
+                if (lane == 0) { lx = left.x; ly = left.y; }
+                if (lane == 31) { rx = n0x; ry = n0y; }
+                if (valid && j > 0 && j < n - 1) {
+                    const double mx = dmul(0.5, dadd(lx, rx));
+                    const double my = dmul(0.5, dadd(ly, ry));
+                    f = make_double2(dadd(cur.x, dmul(p.factor, dsub(mx, cur.x))),
+                                     dadd(cur.y, dmul(p.factor, dsub(my, cur.y))));
+                }
+            }
+            if (p.pout && valid) p.pout[s + j] = f;
+
+            if (do_count) {
+                double qx = __shfl_up_sync(full, f.x, 1), qy = __shfl_up_sync(full, f.y, 1);
+                if (lane == 0) { qx = prevf.x; qy = prevf.y; }
+                const bool part = valid && j > 0;  // local point 0 is always kept at 0
+                const double gs = part ? hypot_ref(dsub(f.x, qx), dsub(f.y, qy)) : 0.0;
+                const bool last = (j == n - 1);
+                bool kept = false;
+                double gk = 0.0;
+                int start = (c0 == 0) ? 1 : 0;
+                while (start < kWarp) {
+                    double geff = gs;
+                    if (lane == start && part) geff = hypot_ref(dsub(f.x, ka.x), dsub(f.y, ka.y));
+                    const bool act = part && lane >= start;
+                    const unsigned m = __ballot_sync(full, act && !last && geff < lo);
+                    if (m == 0) {
+                        if (act) { kept = true; gk = geff; }
+                        break;
+                    }
+                    const int b = __ffs(m) - 1;
+                    if (act && lane < b) { kept = true; gk = geff; }
+                    if (b > start) {
+                        ka.x = __shfl_sync(full, f.x, b - 1);
+                        ka.y = __shfl_sync(full, f.y, b - 1);
+                    }
+                    start = b + 1;
+                }
+                int64_t pieces = 0;
+                if (kept) {
+                    double g = gk;
+                    pieces = 1;
+                    while (g > hi) { g = dmul(g, 0.5); pieces *= 2; }
+                }
+                int64_t incl = pieces;
+#pragma unroll
+                for (int d = 1; d < kWarp; d <<= 1) {
+                    const int64_t t = __shfl_up_sync(full, incl, d);
+                    if (lane >= d) incl += t;
+                }
+                if (part) p.pos[s + j] = kept ? (int32_t)(off + incl) : -1;
+                const unsigned km = __ballot_sync(full, kept);
+                if (km) {
+                    const int lk = 31 - __clz(km);
+                    ka.x = __shfl_sync(full, f.x, lk);
+                    ka.y = __shfl_sync(full, f.y, lk);
+                }
+                off += __shfl_sync(full, incl, 31);
+                prevf.x = __shfl_sync(full, f.x, 31);
+                prevf.y = __shfl_sync(full, f.y, 31);
+            }
+            left.x = __shfl_sync(full, cur.x, 31);
+            left.y = __shfl_sync(full, cur.y, 31);
+            cur = nxt;
         }
+        if (do_count && lane == 0) p.counts[e] = off + 1;
     }
-    buf[0][t] = p;
-    __syncthreads();
-    int cur = 0;
-    for (int q = 1; q <= passes; ++q) {
-        double2 nx = buf[cur][t];
-        if (interior && t >= q && t < kAdvBlock - q) {
-            const double2 l = buf[cur][t - 1], r = buf[cur][t + 1];
-            const double mx = dmul(0.5, dadd(l.x, r.x));
-            const double my = dmul(0.5, dadd(l.y, r.y));
-            nx = make_double2(dadd(nx.x, dmul(factor, dsub(mx, nx.x))),
-                              dadd(nx.y, dmul(factor, dsub(my, nx.y))));
+
+    if (p.partials) {
+        // per-block metrics in a fixed order (deterministic for a fixed grid)
+        __shared__ double red_d[kStreamBlock / 32];
+        __shared__ unsigned long long red_m[kStreamBlock / 32];
+        for (int o = 16; o; o >>= 1) {
+            my_moved += __shfl_down_sync(full, my_moved, o);
+            my_disp = dadd(my_disp, __shfl_down_sync(full, my_disp, o));
         }
-        buf[cur ^ 1][t] = nx;
+        if (lane == 0) {
+            red_d[threadIdx.x >> 5] = my_disp;
+            red_m[threadIdx.x >> 5] = my_moved;
+        }
         __syncthreads();
-        cur ^= 1;
-    }
-    if (own) pout[j] = buf[cur][t];
-
-    // per-block metrics in a fixed order (deterministic)
-    unsigned cnt = (own && mv) ? 1u : 0u;
-    double dd = (own && mv) ? d : 0.0;
-    for (int o = 16; o; o >>= 1) {
-        cnt += __shfl_down_sync(0xffffffffu, cnt, o);
-        dd = dadd(dd, __shfl_down_sync(0xffffffffu, dd, o));
-    }
-    if ((t & 31) == 0) {
-        red_d[t >> 5] = dd;
-        red_m[t >> 5] = cnt;
-    }
-    __syncthreads();
-    if (t == 0) {
-        double s = 0.0;
-        unsigned long long c = 0;
-        for (int w = 0; w < kAdvBlock / 32; ++w) {
-            s = dadd(s, red_d[w]);
-            c += red_m[w];
+        if (threadIdx.x == 0) {
+            double sd = 0.0;
+            unsigned long long sm = 0;
+            for (int w = 0; w < kStreamBlock / 32; ++w) {
+                sd = dadd(sd, red_d[w]);
+                sm += red_m[w];
+            }
+            p.partials[blockIdx.x] = sd;
+            if (sm && p.moved) atomicAdd(p.moved, sm);
         }
-        partials[blockIdx.x] = s;
-        if (c) atomicAdd(moved, c);
     }
+}
+
+int launch_polyline_pass(const PolylinePass &p, cudaStream_t st, const char *what) {
+    if (p.n_edges == 0) return HB_OK;
+    const unsigned grid = persistent_grid(polyline_pass_kernel, p.n_edges);
+    if (p.partials &&
+        cudaMemsetAsync(p.partials, 0, sizeof(double) * kMaxStreamBlocks, st) != cudaSuccess)
+        return check_launch(what, 0);
+    polyline_pass_kernel<<<grid, kStreamBlock, 0, st>>>(p);
+    return check_launch(what);
 }
 
 // one block, fixed summation order
@@ -160,11 +244,11 @@ __global__ void probe_kernel(const float *__restrict__ rho, int nv, int nu,
                              double *__restrict__ value, double2 *__restrict__ grad) {
     const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= n) return;
-    const double2 p = xy[i];
-    if (value) value[i] = bilinear_ref(rho, nv, nu, p.x, p.y);
+    const double2 q = xy[i];
+    if (value) value[i] = bilinear_ref(rho, nv, nu, q.x, q.y);
     if (grad) {
         double gx, gy;
-        gradient_ref(rho, nv, nu, p.x, p.y, gx, gy);
+        gradient_ref(rho, nv, nu, q.x, q.y, gx, gy);
         grad[i] = make_double2(gx, gy);
     }
 }
@@ -177,30 +261,65 @@ static inline cudaStream_t as_stream(void *s) { return reinterpret_cast<cudaStre
 
 extern "C" {
 
-int64_t hb_advect_partials(int64_t n_pts, int lap_passes) {
-    if (lap_passes < 0 || lap_passes > kAdvMaxHalo) return -1;
-    const int P = kAdvBlock - 2 * lap_passes;
-    return n_pts > 0 ? (n_pts + P - 1) / P : 0;
-}
+int64_t hb_advect_partials(void) { return kMaxStreamBlocks; }
 
 int hb_advect_laplacian(const double *pts_in, double *pts_out, const int64_t *starts,
                         int64_t n_edges, int64_t n_pts, const int32_t *edge_layer,
                         const float *rho, int nbins, int nv, int nu, double h, double eps,
                         double min_step, int fixed_step, double lap_factor, int lap_passes,
+                        double delta, int64_t *counts, int32_t *pos,
                         unsigned long long *moved, double *disp_partials, void *stream) {
-    if (n_edges < 0 || n_pts < 0 || nbins < 1 || nv < 3 || nu < 3 || lap_passes < 0 ||
-        lap_passes > kAdvMaxHalo || !moved || !disp_partials ||
-        (n_pts > 0 && (!pts_in || !pts_out || !starts || !edge_layer || !rho)))
+    const bool adv = h >= 0.0;
+    if (n_edges < 0 || n_pts < 0 || lap_passes < 0 || !moved || !disp_partials ||
+        (adv && (nbins < 1 || nv < 3 || nu < 3 || !edge_layer || !rho)) ||
+        (counts && (!pos || !(delta > 0))) ||
+        (n_pts > 0 && (!pts_in || !pts_out || !starts)))
         return set_error(HB_EINVAL, "hb_advect_laplacian: bad arguments");
-    if (pts_in == pts_out && n_pts > 0)
-        return set_error(HB_EINVAL, "hb_advect_laplacian: pts_in and pts_out alias");
-    if (n_pts == 0) return HB_OK;
-    const int64_t blocks = hb_advect_partials(n_pts, lap_passes);
-    advect_laplacian_kernel<<<(unsigned)blocks, kAdvBlock, 0, as_stream(stream)>>>(
-        reinterpret_cast<const double2 *>(pts_in), reinterpret_cast<double2 *>(pts_out),
-        starts, n_edges, n_pts, edge_layer, rho, (int64_t)nv * nu, nv, nu, h, eps, min_step,
-        fixed_step, lap_factor, lap_passes, moved, disp_partials);
-    return check_launch("hb_advect_laplacian");
+    if (n_pts == 0 || n_edges == 0) return HB_OK;
+    cudaStream_t st = as_stream(stream);
+    PolylinePass p{};
+    p.pin = reinterpret_cast<const double2 *>(pts_in);
+    p.pout = reinterpret_cast<double2 *>(pts_out);
+    p.starts = starts;
+    p.n_edges = n_edges;
+    p.edge_layer = edge_layer;
+    p.rho = rho;
+    p.plane = (int64_t)nv * nu;
+    p.nv = nv;
+    p.nu = nu;
+    p.h = adv ? h : -1.0;
+    p.eps = eps;
+    p.min_step = min_step;
+    p.fixed = fixed_step;
+    p.factor = lap_factor;
+    p.lap = lap_passes > 0 ? 1 : 0;
+    p.delta = delta;
+    p.moved = moved;
+    p.partials = disp_partials;
+    // passes 0/1: one fused launch.  More passes: the first launch fuses the
+    // first sweep, every further Jacobi sweep is an in-place streaming launch
+    // (identical results: each sweep only reads the previous one), and the
+    // resample count rides on the last launch.
+    p.counts = lap_passes <= 1 ? counts : nullptr;
+    p.pos = lap_passes <= 1 ? pos : nullptr;
+    int rc = launch_polyline_pass(p, st, "hb_advect_laplacian");
+    for (int q = 1; rc == HB_OK && q < lap_passes; ++q) {
+        PolylinePass sweep{};
+        sweep.pin = reinterpret_cast<const double2 *>(pts_out);
+        sweep.pout = reinterpret_cast<double2 *>(pts_out);
+        sweep.starts = starts;
+        sweep.n_edges = n_edges;
+        sweep.h = -1.0;
+        sweep.factor = lap_factor;
+        sweep.lap = 1;
+        sweep.delta = delta;
+        if (q == lap_passes - 1) {
+            sweep.counts = counts;
+            sweep.pos = pos;
+        }
+        rc = launch_polyline_pass(sweep, st, "hb_advect_laplacian(sweep)");
+    }
+    return rc;
 }
 
 int hb_reduce_f64(const double *in, int64_t n, double *out, void *stream) {

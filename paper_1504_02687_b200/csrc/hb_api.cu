@@ -28,6 +28,19 @@ int check_launch(const char *what, int kernels) {
     return HB_OK;
 }
 
+int device_sm_count() {
+    static int cached = 0;
+    if (cached == 0) {
+        int dev = 0, n = 0;
+        if (cudaGetDevice(&dev) == cudaSuccess &&
+            cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev) == cudaSuccess && n > 0)
+            cached = n;
+        else
+            cached = 148;
+    }
+    return cached;
+}
+
 }  // namespace hb
 
 extern "C" {

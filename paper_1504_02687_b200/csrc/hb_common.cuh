@@ -135,65 +135,56 @@ __device__ __forceinline__ void dda_splat(double px0, double py0, double px1,
     }
 }
 
-// ---- edge window: map a contiguous point range to its edges ---------------
-// Largest e in [0, n_edges) with starts[e] <= p (p < starts[n_edges]).
-// Warp-cooperative 32-ary search; all lanes return the same value.
-__device__ __forceinline__ int64_t warp_find_edge(const int64_t *__restrict__ starts,
-                                                  int64_t n_edges, int64_t p) {
-    const int lane = threadIdx.x & 31;
-    int64_t lo = 0, hi = n_edges;  // answer in [lo, hi)
-    while (hi - lo > 32) {
-        int64_t step = (hi - lo + 31) / 32;
-        int64_t idx = lo + (int64_t)lane * step;
-        bool ok = idx < hi && __ldg(starts + idx) <= p;
-        unsigned m = __ballot_sync(0xffffffffu, ok);
-        int last = 31 - __clz(m);  // lane 0 is always ok (starts[lo] <= p)
-        lo = lo + (int64_t)last * step;
-        int64_t nhi = lo + step;
-        hi = nhi < hi ? nhi : hi;
+// ---- persistent warp-per-edge kernels ---------------------------------------
+constexpr int kStreamBlock = 256;      // 8 warps
+constexpr int kMaxStreamBlocks = 4096; // grid cap; also the metric-partials size
+
+int device_sm_count();  // cached SM count of the current device (hb_api.cu)
+
+// Grid for a persistent grid-stride kernel over n_edges warp work items:
+// exactly the resident capacity (occupancy API, cached per kernel), never
+// more blocks than there are warps' worth of edges.  For a given GPU model
+// this is a pure function of n_edges, so per-block metric partials sum in a
+// reproducible order.
+template <typename Kernel>
+inline unsigned persistent_grid(Kernel kernel, int64_t n_edges) {
+    static int per_sm = 0;
+    if (per_sm == 0) {
+        if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, kStreamBlock, 0) !=
+                cudaSuccess ||
+            per_sm < 1)
+            per_sm = 1;
     }
-    int64_t idx = lo + lane;
-    bool ok = idx < hi && __ldg(starts + idx) <= p;
-    unsigned m = __ballot_sync(0xffffffffu, ok);
-    return lo + (31 - __clz(m));
+    int64_t want = (n_edges + kStreamBlock / 32 - 1) / (kStreamBlock / 32);
+    int64_t cap = (int64_t)device_sm_count() * per_sm;
+    if (cap > kMaxStreamBlocks) cap = kMaxStreamBlocks;
+    if (want > cap) want = cap;
+    return (unsigned)(want < 1 ? 1 : want);
 }
 
-// A block's view of the edges overlapping points [lo, hi).  `st` holds
-// starts[e0 .. e0+cnt] (cnt+1 entries).  Capacity: a range of L points meets
-// at most L/2 + 1 edges because every polyline has >= 2 points.
-template <int CAP>
-struct EdgeWindow {
-    int64_t e0;
-    int cnt;
-    int64_t st[CAP + 1];
+// One fused streaming pass over every polyline (hb_advect.cu):
+//   advect (h >= 0) -> Laplacian (lap = 0 or 1 Jacobi sweep) -> write pout
+//   (if non-null) -> resample count on the final points (if counts != null).
+struct PolylinePass {
+    const double2 *pin = nullptr;
+    double2 *pout = nullptr;  // may alias pin (streaming reads run ahead of writes)
+    const int64_t *starts = nullptr;
+    int64_t n_edges = 0;
+    const int32_t *edge_layer = nullptr;
+    const float *rho = nullptr;
+    int64_t plane = 0;
+    int nv = 0, nu = 0;
+    double h = -1.0, eps = 1e-8, min_step = 0.25;
+    int fixed = 0;
+    double factor = 0.5;
+    int lap = 0;
+    double delta = 1.0;
+    int64_t *counts = nullptr;
+    int32_t *pos = nullptr;
+    unsigned long long *moved = nullptr;
+    double *partials = nullptr;
 };
 
-template <int CAP>
-__device__ void load_edge_window(EdgeWindow<CAP> &w, const int64_t *__restrict__ starts,
-                                 int64_t n_edges, int64_t lo, int64_t hi) {
-    if (threadIdx.x < 32) {
-        int64_t e0 = warp_find_edge(starts, n_edges, lo);
-        if (threadIdx.x == 0) w.e0 = e0;
-    }
-    __syncthreads();
-    const int64_t e0 = w.e0;
-    int64_t avail = n_edges - e0;  // edges e0..n_edges-1
-    int cnt = (int)(avail < CAP ? avail : CAP);
-    for (int i = threadIdx.x; i <= cnt; i += blockDim.x) w.st[i] = __ldg(starts + e0 + i);
-    if (threadIdx.x == 0) w.cnt = cnt;
-    __syncthreads();
-    (void)hi;
-}
-
-// local edge index k with st[k] <= p < st[k+1]
-template <int CAP>
-__device__ __forceinline__ int window_edge(const EdgeWindow<CAP> &w, int64_t p) {
-    int lo = 0, hi = w.cnt;  // st[lo] <= p, answer in [lo, hi)
-    while (hi - lo > 1) {
-        int mid = (lo + hi) >> 1;
-        if (w.st[mid] <= p) lo = mid; else hi = mid;
-    }
-    return lo;
-}
+int launch_polyline_pass(const PolylinePass &p, cudaStream_t st, const char *what);
 
 }  // namespace hb

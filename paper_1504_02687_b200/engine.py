@@ -5,13 +5,14 @@ One engine owns one shard of edges on one GPU (the whole graph at N=1). Per
 iteration ``i`` (``bundler.py:351-376``) it launches, on the current CUDA
 stream:
 
-  i > 0: hb_resample_count -> hb_scan_counts -> (1 host read: N_i)
+  i > 0: hb_scan_counts -> (1 host read: N_i)
          -> hb_resample_emit (+ fused splat into the int32 group counts)
   i = 0: hb_splat
   [world > 1: all-reduce of the int32 counts over NCCL]
   hb_smooth (mix + 3 exact box passes + layer peaks)
-  hb_advect_laplacian (+ per-block metric partials) -> hb_reduce_f64
-  hb_used_cells
+  hb_advect_laplacian: advect + Laplacian + the NEXT iteration's resample
+         count in one streaming pass (+ per-block metric partials)
+  hb_reduce_f64, hb_used_cells
 
 Host reads per iteration: the new point total (needed to size the emit
 buffer). Metrics stay on the device until the run ends unless an
@@ -172,7 +173,8 @@ class BundleEngine:
         scw = N.lib().hb_scan_workspace_bytes(max(E, 1))
         self.scan_ws = torch.empty(scw, dtype=torch.uint8, device=dev)
         self.lap_passes = int(cfg.laplacian_passes)
-        self._partials = torch.empty(0, dtype=torch.float64, device=dev)
+        self._partials = torch.zeros(int(N.lib().hb_advect_partials()), dtype=torch.float64,
+                                     device=dev)
         self.iters = int(cfg.iterations)
         # per-iteration device metrics: moved (u64 as int64), disp, used
         self.m_moved = torch.zeros(self.iters, dtype=torch.int64, device=dev)
@@ -207,14 +209,6 @@ class BundleEngine:
         self.pos = new_pos
         self.cap = cap
 
-    def _partials_for(self, n: int) -> torch.Tensor:
-        k = int(N.lib().hb_advect_partials(n, self.lap_passes))
-        if k < 0:
-            raise ValueError("laplacian_passes must be <= 32")
-        if self._partials.numel() < max(k, 1):
-            self._partials = torch.empty(max(k, 1) * 2, dtype=torch.float64, device=self.dev)
-        return self._partials
-
     def _k(self, name: str, *args) -> None:
         """Launch one C-ABI entry point, bracketed by events when tracing."""
         if self.trace is None:
@@ -245,49 +239,49 @@ class BundleEngine:
         ev0.record()
         self.hist.zero_()
         if i > 0:
-            # resample (bundler.py:353-354) fused with the splat (:355-356)
-            self._k("hb_resample_count", ptr(self.pts), ptr(self.starts), E, self.delta,
-                   ptr(self.ecounts), ptr(self.pos), s)
+            # resample (bundler.py:353-354): the counts/codes came out of the
+            # previous iteration's fused advect pass; scan, size, then emit
+            # fused with the splat (:355-356)
             self._k("hb_scan_counts", ptr(self.ecounts), E, ptr(self.starts_alt),
-                   ptr(self.scan_ws), self.scan_ws.numel(), s)
+                    ptr(self.scan_ws), self.scan_ws.numel(), s)
             n_new = int(download(self.starts_alt[E:E + 1])[0]) if E else 0
             self._ensure_capacity(n_new)
             fused = self.wkind != "float"
             self._k("hb_resample_emit", ptr(self.pts), ptr(self.starts), E, self.n_pts,
-                   ptr(self.pos), ptr(self.starts_alt), ptr(self.alt), ptr(self.groups),
-                   ptr(self.wint), ptr(self.hist) if fused else None, nv, nu,
-                   ptr(self.status), s)
+                    ptr(self.pos), ptr(self.starts_alt), ptr(self.alt), ptr(self.groups),
+                    ptr(self.wint), ptr(self.hist) if fused else None, nv, nu,
+                    ptr(self.status), s)
             self.pts, self.alt = self.alt, self.pts
             self.starts, self.starts_alt = self.starts_alt, self.starts
             self.n_pts = n_new
             if not fused:
                 name, w = self._splat_args()
                 self._k(name, ptr(self.pts), ptr(self.starts), E, self.n_pts,
-                       ptr(self.groups), w, ptr(self.hist), B, nv, nu, ptr(self.status), s)
+                        ptr(self.groups), w, ptr(self.hist), B, nv, nu, ptr(self.status), s)
         else:
             name, w = self._splat_args()
             self._k(name, ptr(self.pts), ptr(self.starts), E, self.n_pts, ptr(self.groups),
-                   w, ptr(self.hist), B, nv, nu, ptr(self.status), s)
+                    w, ptr(self.hist), B, nv, nu, ptr(self.status), s)
         if self.reduce_hist is not None:
             self.reduce_hist(self.hist)
         is_int = self.wkind != "float"
         self._k("hb_smooth", ptr(self.hist) if is_int else None,
-               None if is_int else ptr(self.hist), ptr(self.mat_dev), B, nv, nu,
-               self.radii.data_ptr(), int(self.radii.numel()), ptr(self.field),
-               ptr(self.smooth_ws), self.smooth_ws.numel(), ptr(self.peak), s)
+                None if is_int else ptr(self.hist), ptr(self.mat_dev), B, nv, nu,
+                self.radii.data_ptr(), int(self.radii.numel()), ptr(self.field),
+                ptr(self.smooth_ws), self.smooth_ws.numel(), ptr(self.peak), s)
         h_i = cfg.lambda_ ** i * cfg.h_max  # bundler.py:360, Python float power
-        part = self._partials_for(self.n_pts)
-        nblk = int(N.lib().hb_advect_partials(self.n_pts, self.lap_passes))
-        self._k("hb_advect_laplacian", ptr(self.pts), ptr(self.alt), ptr(self.starts), E,
-               self.n_pts, ptr(self.groups), ptr(self.field), B, nv, nu, float(h_i),
-               float(cfg.epsilon), MIN_STEP, int(self.fixed_step),
-               float(cfg.laplacian_factor), self.lap_passes,
-               self.m_moved.data_ptr() + 8 * i, ptr(part), s)
-        if self.n_pts:
-            self.pts, self.alt = self.alt, self.pts
-        self._k("hb_reduce_f64", ptr(part), nblk, self.m_disp.data_ptr() + 8 * i, s)
+        # advect -> Laplacian -> next iteration's resample count, in place
+        last = i == self.iters - 1
+        self._k("hb_advect_laplacian", ptr(self.pts), ptr(self.pts), ptr(self.starts), E,
+                self.n_pts, ptr(self.groups), ptr(self.field), B, nv, nu, float(h_i),
+                float(cfg.epsilon), MIN_STEP, int(self.fixed_step),
+                float(cfg.laplacian_factor), self.lap_passes, self.delta,
+                None if last else ptr(self.ecounts), None if last else ptr(self.pos),
+                self.m_moved.data_ptr() + 8 * i, ptr(self._partials), s)
+        self._k("hb_reduce_f64", ptr(self._partials), self._partials.numel(),
+                self.m_disp.data_ptr() + 8 * i, s)
         self._k("hb_used_cells", ptr(self.field), ptr(self.peak), B, nv, nu, 0.01,
-               self.m_used.data_ptr() + 8 * i, s)
+                self.m_used.data_ptr() + 8 * i, s)
         ev1.record()
         self._ev.append((ev0, ev1))
         rec = IterationRecord(i, h_i, self.n_pts, E)

@@ -136,14 +136,13 @@ def test_advect_matches_reference_kat(fixed):
     E, n = len(starts) - 1, len(pts)
     out = torch.empty((n, 2), dtype=torch.float64, device="cuda")
     moved = torch.zeros(1, dtype=torch.int64, device="cuda")
-    part = torch.zeros(int(N.lib().hb_advect_partials(n, 0)), dtype=torch.float64,
-                       device="cuda")
+    part = torch.zeros(int(N.lib().hb_advect_partials()), dtype=torch.float64, device="cuda")
     disp = torch.zeros(1, dtype=torch.float64, device="cuda")
     h = 3.0 if fixed else 6.0
     s = stream_ptr()
     N.call("hb_advect_laplacian", ptr(dev(pts)), ptr(out), ptr(dev(starts)), E, n,
            ptr(dev(groups.astype(np.int32))), ptr(dev(rho)), nb, nv, nu, h, 1e-8, 0.25,
-           int(fixed), 0.5, 0, ptr(moved), ptr(part), s)
+           int(fixed), 0.5, 0, 1.0, None, None, ptr(moved), ptr(part), s)
     N.call("hb_reduce_f64", ptr(part), part.numel(), ptr(disp), s)
     sync()
     tag = "advf" if fixed else "adv"
@@ -159,13 +158,12 @@ def test_laplacian_matches_reference_kat(factor, passes, key):
     E, n = len(starts) - 1, len(pts)
     out = torch.empty((n, 2), dtype=torch.float64, device="cuda")
     moved = torch.zeros(1, dtype=torch.int64, device="cuda")
-    part = torch.zeros(int(N.lib().hb_advect_partials(n, passes)), dtype=torch.float64,
-                       device="cuda")
+    part = torch.zeros(int(N.lib().hb_advect_partials()), dtype=torch.float64, device="cuda")
     rho = torch.zeros((1, 3, 3), dtype=torch.float32, device="cuda")
     grp = torch.zeros(E, dtype=torch.int32, device="cuda")
     N.call("hb_advect_laplacian", ptr(dev(pts)), ptr(out), ptr(dev(starts)), E, n, ptr(grp),
-           ptr(rho), 1, 3, 3, -1.0, 1e-8, 0.25, 0, factor, passes, ptr(moved), ptr(part),
-           stream_ptr())
+           ptr(rho), 1, 3, 3, -1.0, 1e-8, 0.25, 0, factor, passes, 1.0, None, None, ptr(moved),
+           ptr(part), stream_ptr())
     sync()
     assert np.array_equal(out.cpu().numpy(), k[key])
 
@@ -247,12 +245,19 @@ def test_advect_laplacian_random_vs_oracle():
     O.laplacian(ref, starts, 0.5, 2)
     out = torch.empty((n, 2), dtype=torch.float64, device="cuda")
     dmoved = torch.zeros(1, dtype=torch.int64, device="cuda")
-    part = torch.zeros(int(N.lib().hb_advect_partials(n, 2)), dtype=torch.float64, device="cuda")
+    part = torch.zeros(int(N.lib().hb_advect_partials()), dtype=torch.float64, device="cuda")
+    # fused next-iteration resample count on the final points
+    delta = 1.7
+    counts = torch.empty(E, dtype=torch.int64, device="cuda")
+    pos = torch.empty(n, dtype=torch.int32, device="cuda")
     N.call("hb_advect_laplacian", ptr(dev(pts)), ptr(out), ptr(dev(starts)), E, n,
            ptr(dev(groups.astype(np.int32))), ptr(dev(rho)), 2, nv, nu, 9.0, 1e-8, 0.25, 0, 0.5,
-           2, ptr(dmoved), ptr(part), stream_ptr())
+           2, delta, ptr(counts), ptr(pos), ptr(dmoved), ptr(part), stream_ptr())
     sync()
     assert np.array_equal(out.cpu().numpy(), ref)
+    ref_counts = np.empty(E, dtype=np.int64)
+    O.lib().orc_resample_count(O._p(ref), O._p(starts), delta, O._p(ref_counts), 0, E)
+    assert np.array_equal(counts.cpu().numpy(), ref_counts)
     assert int(dmoved.item()) == moved
     np.testing.assert_allclose(part.sum().item(), disp, rtol=DISP_RTOL)
 

@@ -31,34 +31,23 @@ struct Adv {
     double disp;
 };
 
+// _kernels.py:163-199 for one interior point
 __device__ __forceinline__ Adv advect_one(const float *__restrict__ rho, int nv, int nu,
-                                          double2 p, double h, double eps, double min_step,
-                                          int fixed) {
+                                          double xhi, double yhi, double2 p, double h,
+                                          double eps, double min_step, int fixed) {
     Adv r{p, false, 0.0};
     const double x = p.x, y = p.y;
     const double xlo = 1.0, ylo = 1.0;  // INTERIOR_MARGIN (_kernels.py:19)
-    const double xhi = dsub(dsub((double)nu, 1.0), 1.0);
-    const double yhi = dsub(dsub((double)nv, 1.0), 1.0);
-    double gx, gy;
-    gradient_ref(rho, nv, nu, x, y, gx, gy);
+    double gx, gy, r0;
+    gradient_value_ref(rho, nv, nu, x, y, gx, gy, r0);
     double gn = hypot_ref(gx, gy);
     if (gn < eps) gn = eps;
     const double dx = gx / gn, dy = gy / gn;
-    if (fixed) {
-        const double nx = fmin_ref(fmax_ref(dadd(x, dmul(h, dx)), xlo), xhi);
-        const double ny = fmin_ref(fmax_ref(dadd(y, dmul(h, dy)), ylo), yhi);
-        r.p = make_double2(nx, ny);
-        if (nx != x || ny != y) {
-            r.moved = true;
-            r.disp = hypot_ref(dsub(nx, x), dsub(ny, y));
-        }
-        return r;
-    }
-    const double r0 = bilinear_ref(rho, nv, nu, x, y);
-    for (double m = h; m >= min_step; m = dmul(m, 0.5)) {
+    double m = h;
+    while (fixed || m >= min_step) {
         const double nx = fmin_ref(fmax_ref(dadd(x, dmul(m, dx)), xlo), xhi);
         const double ny = fmin_ref(fmax_ref(dadd(y, dmul(m, dy)), ylo), yhi);
-        if (bilinear_ref(rho, nv, nu, nx, ny) >= r0) {
+        if (fixed || bilinear_ref(rho, nv, nu, nx, ny) >= r0) {
             r.p = make_double2(nx, ny);
             if (nx != x || ny != y) {
                 r.moved = true;
@@ -66,55 +55,60 @@ __device__ __forceinline__ Adv advect_one(const float *__restrict__ rho, int nv,
             }
             break;
         }
+        m = dmul(m, 0.5);
     }
     return r;
 }
 
-__global__ void __launch_bounds__(kStreamBlock)
+__global__ void __launch_bounds__(kStreamBlock, 3)
 polyline_pass_kernel(const PolylinePass p) {
     const unsigned full = 0xffffffffu;
     const int lane = threadIdx.x & 31;
     const bool do_adv = p.h >= 0.0;
     const bool do_count = p.counts != nullptr;
     const double lo = 0.5 * p.delta, hi = 1.5 * p.delta;  // _kernels.py:211-212
+    // xhi = nu - 1 - INTERIOR_MARGIN (_kernels.py:158-159)
+    const double xhi = dsub(dsub((double)p.nu, 1.0), 1.0);
+    const double yhi = dsub(dsub((double)p.nv, 1.0), 1.0);
     const int64_t nwarps = (int64_t)gridDim.x * (kStreamBlock / 32);
-    unsigned long long my_moved = 0;
+    unsigned my_moved = 0;
     double my_disp = 0.0;
 
     for (int64_t e = ((int64_t)blockIdx.x * kStreamBlock + threadIdx.x) / 32; e < p.n_edges;
          e += nwarps) {
         const int64_t s = p.starts[e];
-        const int64_t n = p.starts[e + 1] - s;
+        const int n = (int)(p.starts[e + 1] - s);
+        const double2 *pin = p.pin + s;
         const float *rho = do_adv ? p.rho + (int64_t)p.edge_layer[e] * p.plane : nullptr;
 
-        // A(c) for chunk c: advected point of local index 32c + lane
-        auto stage = [&](int64_t c0) -> double2 {
-            const int64_t j = c0 + lane;
-            if (j >= n) return make_double2(0.0, 0.0);
-            double2 q = p.pin[s + j];
-            if (do_adv && j > 0 && j < n - 1) {
-                const Adv a = advect_one(rho, p.nv, p.nu, q, p.h, p.eps, p.min_step, p.fixed);
-                if (a.moved) {
-                    my_moved += 1;
-                    my_disp = dadd(my_disp, a.disp);
+        double2 cur = make_double2(0.0, 0.0);   // A(chunk c), lane = local index - c0
+        double2 left = make_double2(0.0, 0.0);  // A(c0 - 1)
+        double2 ka = make_double2(0.0, 0.0);    // count: last kept final point
+        double2 prevf = ka;                     // count: final point c0 - 1
+        int off = 0;                            // count: output index of ka
+
+        // iteration c0 stages chunk c0+32 (advect) and finalises chunk c0
+        for (int c0 = -kWarp; c0 < n; c0 += kWarp) {
+            const int jn = c0 + kWarp + lane;
+            double2 nxt = make_double2(0.0, 0.0);
+            if (jn < n) {
+                nxt = pin[jn];
+                if (do_adv && jn > 0 && jn < n - 1) {
+                    const Adv a = advect_one(rho, p.nv, p.nu, xhi, yhi, nxt, p.h, p.eps,
+                                             p.min_step, p.fixed);
+                    my_moved += a.moved;
+                    if (a.moved) my_disp = dadd(my_disp, a.disp);
+                    nxt = a.p;
                 }
-                q = a.p;
             }
-            return q;
-        };
-
-        double2 cur = stage(0);
-        double2 left = make_double2(0.0, 0.0);  // A of local index c0-1
-        // count carries
-        double2 ka = make_double2(__shfl_sync(full, cur.x, 0), __shfl_sync(full, cur.y, 0));
-        double2 prevf = ka;  // final point of local index c0-1
-        int64_t off = 0;
-        if (do_count && lane == 0) p.pos[s] = 0;
-
-        for (int64_t c0 = 0; c0 < n; c0 += kWarp) {
-            const bool has_next = c0 + kWarp < n;
-            const double2 nxt = has_next ? stage(c0 + kWarp) : make_double2(0.0, 0.0);
-            const int64_t j = c0 + lane;
+            if (c0 < 0) {  // prologue: chunk 0 staged
+                cur = nxt;
+                ka = make_double2(__shfl_sync(full, cur.x, 0), __shfl_sync(full, cur.y, 0));
+                prevf = ka;
+                if (do_count && lane == 0) p.pos[s] = 0;
+                continue;
+            }
+            const int j = c0 + lane;
             const bool valid = j < n;
             double2 f = cur;
             if (p.lap) {
@@ -158,19 +152,19 @@ polyline_pass_kernel(const PolylinePass p) {
                     }
                     start = b + 1;
                 }
-                int64_t pieces = 0;
+                int pieces = 0;
                 if (kept) {
                     double g = gk;
                     pieces = 1;
                     while (g > hi) { g = dmul(g, 0.5); pieces *= 2; }
                 }
-                int64_t incl = pieces;
+                int incl = pieces;
 #pragma unroll
                 for (int d = 1; d < kWarp; d <<= 1) {
-                    const int64_t t = __shfl_up_sync(full, incl, d);
+                    const int t = __shfl_up_sync(full, incl, d);
                     if (lane >= d) incl += t;
                 }
-                if (part) p.pos[s + j] = kept ? (int32_t)(off + incl) : -1;
+                if (part) p.pos[s + j] = kept ? off + incl : -1;
                 const unsigned km = __ballot_sync(full, kept);
                 if (km) {
                     const int lk = 31 - __clz(km);
@@ -185,13 +179,13 @@ polyline_pass_kernel(const PolylinePass p) {
             left.y = __shfl_sync(full, cur.y, 31);
             cur = nxt;
         }
-        if (do_count && lane == 0) p.counts[e] = off + 1;
+        if (do_count && lane == 0) p.counts[e] = (int64_t)off + 1;
     }
 
     if (p.partials) {
         // per-block metrics in a fixed order (deterministic for a fixed grid)
         __shared__ double red_d[kStreamBlock / 32];
-        __shared__ unsigned long long red_m[kStreamBlock / 32];
+        __shared__ unsigned red_m[kStreamBlock / 32];
         for (int o = 16; o; o >>= 1) {
             my_moved += __shfl_down_sync(full, my_moved, o);
             my_disp = dadd(my_disp, __shfl_down_sync(full, my_disp, o));
@@ -271,7 +265,7 @@ int hb_advect_laplacian(const double *pts_in, double *pts_out, const int64_t *st
                         unsigned long long *moved, double *disp_partials, void *stream) {
     const bool adv = h >= 0.0;
     if (n_edges < 0 || n_pts < 0 || lap_passes < 0 || !moved || !disp_partials ||
-        (adv && (nbins < 1 || nv < 3 || nu < 3 || !edge_layer || !rho)) ||
+        (adv && (nbins < 1 || nv < 3 || nu < 3 || nv > kMaxDim || nu > kMaxDim || !edge_layer || !rho)) ||
         (counts && (!pos || !(delta > 0))) ||
         (n_pts > 0 && (!pts_in || !pts_out || !starts)))
         return set_error(HB_EINVAL, "hb_advect_laplacian: bad arguments");
@@ -330,7 +324,7 @@ int hb_reduce_f64(const double *in, int64_t n, double *out, void *stream) {
 
 int hb_probe(const float *rho_layer, int nv, int nu, const double *xy, int64_t n,
              double *value, double *grad, void *stream) {
-    if (!rho_layer || nv < 2 || nu < 2 || n < 0 || (n > 0 && !xy))
+    if (!rho_layer || nv < 2 || nu < 2 || nv > kMaxDim || nu > kMaxDim || n < 0 || (n > 0 && !xy))
         return set_error(HB_EINVAL, "hb_probe: bad arguments");
     if (n == 0) return HB_OK;
     probe_kernel<<<(unsigned)((n + 255) / 256), 256, 0, as_stream(stream)>>>(

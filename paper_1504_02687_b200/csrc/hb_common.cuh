@@ -26,9 +26,20 @@ __device__ __forceinline__ double dadd(double a, double b) { return __dadd_rn(a,
 __device__ __forceinline__ double dsub(double a, double b) { return __dsub_rn(a, b); }
 __device__ __forceinline__ double dmul(double a, double b) { return __dmul_rn(a, b); }
 
+// Grid cell indices are 32-bit: every kernel entry checks nv, nu <= kMaxDim,
+// so v*nu + u and k*dx never overflow.  int(math.floor(x)) of the reference
+// becomes one F2I.FLOOR; CUDA's conversion saturates out-of-range values,
+// which the clamps that always follow turn into the same clamped index the
+// reference's int64 arithmetic produces.
+constexpr int kMaxDim = 46340;  // kMaxDim^2 < 2^31
+
+__device__ __forceinline__ int floor_i(double x) { return __double2int_rd(x); }
+
 // int(math.floor(x + 0.5)) -- _kernels.py:59-62
-__device__ __forceinline__ int64_t cell_round(double x) {
-    return (int64_t)floor(dadd(x, 0.5));
+__device__ __forceinline__ int cell_round(double x) { return floor_i(dadd(x, 0.5)); }
+
+__device__ __forceinline__ int clampi(int v, int lo, int hi) {
+    return v < lo ? lo : (v > hi ? hi : v);
 }
 
 // sqrt((ax)^2 + (ay)^2) with the reference's association
@@ -42,79 +53,112 @@ __device__ __forceinline__ double fmax_ref(double a, double b) { return a > b ? 
 
 __device__ __forceinline__ float ldf(const float *p) { return __ldg(p); }
 
-// _kernels.py:80-98 bilinear_value.  The density difference is a float32
-// subtraction, promoted afterwards.
-__device__ __forceinline__ double bilinear_ref(const float *__restrict__ rho,
-                                               int nv, int nu, double x, double y) {
-    int64_t u0 = (int64_t)floor(x);
-    int64_t v0 = (int64_t)floor(y);
-    u0 = u0 < 0 ? 0 : (u0 > nu - 2 ? nu - 2 : u0);
-    v0 = v0 < 0 ? 0 : (v0 > nv - 2 ? nv - 2 : v0);
-    double fx = dsub(x, (double)u0);
-    double fy = dsub(y, (double)v0);
+// a + f*(b - a) with the density difference taken in float32 and promoted
+// afterwards (numba types rho[i] - rho[j] as float32)
+__device__ __forceinline__ double lerp_f32diff(float a, float b, double f) {
+    return dadd((double)a, dmul(f, (double)__fsub_rn(b, a)));
+}
+
+// _kernels.py:80-98 bilinear_value
+__device__ __forceinline__ double bilinear_ref(const float *__restrict__ rho, int nv, int nu,
+                                               double x, double y) {
+    const int u0 = clampi(floor_i(x), 0, nu - 2);
+    const int v0 = clampi(floor_i(y), 0, nv - 2);
+    const double fx = dsub(x, (double)u0);
+    const double fy = dsub(y, (double)v0);
     const float *r0 = rho + v0 * nu + u0;
     const float *r1 = r0 + nu;
-    float a00 = ldf(r0), a01 = ldf(r0 + 1), a10 = ldf(r1), a11 = ldf(r1 + 1);
-    float d0 = __fsub_rn(a01, a00);
-    float d1 = __fsub_rn(a11, a10);
-    double a = dadd((double)a00, dmul(fx, (double)d0));
-    double b = dadd((double)a10, dmul(fx, (double)d1));
+    const double a = lerp_f32diff(ldf(r0), ldf(r0 + 1), fx);
+    const double b = lerp_f32diff(ldf(r1), ldf(r1 + 1), fx);
     return dadd(a, dmul(fy, dsub(b, a)));
 }
 
-// _kernels.py:101-114 _cell_gradient
-__device__ __forceinline__ void cell_grad_ref(const float *__restrict__ rho, int nv,
-                                              int nu, int64_t u, int64_t v,
-                                              double &gx, double &gy) {
-    u = u < 1 ? 1 : (u > nu - 2 ? nu - 2 : u);
-    v = v < 1 ? 1 : (v > nv - 2 ? nv - 2 : v);
+// _kernels.py:101-114 _cell_gradient (general, clamped)
+__device__ __forceinline__ void cell_grad_ref(const float *__restrict__ rho, int nv, int nu,
+                                              int u, int v, double &gx, double &gy) {
+    u = clampi(u, 1, nu - 2);
+    v = clampi(v, 1, nv - 2);
     const float *c = rho + v * nu + u;
-    float dx = __fsub_rn(ldf(c + 1), ldf(c - 1));
-    float dy = __fsub_rn(ldf(c + nu), ldf(c - nu));
-    gx = dmul(0.5, (double)dx);
-    gy = dmul(0.5, (double)dy);
+    gx = dmul(0.5, (double)__fsub_rn(ldf(c + 1), ldf(c - 1)));
+    gy = dmul(0.5, (double)__fsub_rn(ldf(c + nu), ldf(c - nu)));
 }
 
-// _kernels.py:117-141 gradient_xy
-__device__ __forceinline__ void gradient_ref(const float *__restrict__ rho, int nv,
-                                             int nu, double x, double y,
-                                             double &gx, double &gy) {
-    int64_t u0 = (int64_t)floor(x);
-    int64_t v0 = (int64_t)floor(y);
-    u0 = u0 < 0 ? 0 : (u0 > nu - 2 ? nu - 2 : u0);
-    v0 = v0 < 0 ? 0 : (v0 > nv - 2 ? nv - 2 : v0);
-    double fx = dsub(x, (double)u0);
-    double fy = dsub(y, (double)v0);
+// _kernels.py:117-141 gradient_xy and, from the same 4x4 stencil, the
+// bilinear value at (x, y) (both clamp u0/v0 to [0, dim-2] identically).
+// Interior fast path (u0 in [1, nu-3], v0 in [1, nv-3], i.e. no clamp can
+// fire): 12 loads off one base pointer.  Otherwise the general clamped path.
+__device__ __forceinline__ void gradient_value_ref(const float *__restrict__ rho, int nv, int nu,
+                                                   double x, double y, double &gx, double &gy,
+                                                   double &val) {
+    const int u0 = clampi(floor_i(x), 0, nu - 2);
+    const int v0 = clampi(floor_i(y), 0, nv - 2);
+    const double fx = dsub(x, (double)u0);
+    const double fy = dsub(y, (double)v0);
     double g00x, g00y, g10x, g10y, g01x, g01y, g11x, g11y;
-    cell_grad_ref(rho, nv, nu, u0, v0, g00x, g00y);
-    cell_grad_ref(rho, nv, nu, u0 + 1, v0, g10x, g10y);
-    cell_grad_ref(rho, nv, nu, u0, v0 + 1, g01x, g01y);
-    cell_grad_ref(rho, nv, nu, u0 + 1, v0 + 1, g11x, g11y);
-    double ax = dadd(g00x, dmul(fx, dsub(g10x, g00x)));
-    double bx = dadd(g01x, dmul(fx, dsub(g11x, g01x)));
-    double ay = dadd(g00y, dmul(fx, dsub(g10y, g00y)));
-    double by = dadd(g01y, dmul(fx, dsub(g11y, g01y)));
+    float a00, a01, a10, a11;
+    if (u0 >= 1 && u0 <= nu - 3 && v0 >= 1 && v0 <= nv - 3) {
+        const float *c = rho + v0 * nu + u0;
+        const float m0 = ldf(c - nu), m1 = ldf(c - nu + 1);
+        const float r0 = ldf(c - 1), r3 = ldf(c + 2);
+        a00 = ldf(c);
+        a01 = ldf(c + 1);
+        const float s0 = ldf(c + nu - 1), s3 = ldf(c + nu + 2);
+        a10 = ldf(c + nu);
+        a11 = ldf(c + nu + 1);
+        const float t1 = ldf(c + 2 * nu), t2 = ldf(c + 2 * nu + 1);
+        g00x = dmul(0.5, (double)__fsub_rn(a01, r0));
+        g00y = dmul(0.5, (double)__fsub_rn(a10, m0));
+        g10x = dmul(0.5, (double)__fsub_rn(r3, a00));
+        g10y = dmul(0.5, (double)__fsub_rn(a11, m1));
+        g01x = dmul(0.5, (double)__fsub_rn(a11, s0));
+        g01y = dmul(0.5, (double)__fsub_rn(t1, a00));
+        g11x = dmul(0.5, (double)__fsub_rn(s3, a10));
+        g11y = dmul(0.5, (double)__fsub_rn(t2, a01));
+    } else {
+        cell_grad_ref(rho, nv, nu, u0, v0, g00x, g00y);
+        cell_grad_ref(rho, nv, nu, u0 + 1, v0, g10x, g10y);
+        cell_grad_ref(rho, nv, nu, u0, v0 + 1, g01x, g01y);
+        cell_grad_ref(rho, nv, nu, u0 + 1, v0 + 1, g11x, g11y);
+        const float *c = rho + v0 * nu + u0;
+        a00 = ldf(c);
+        a01 = ldf(c + 1);
+        a10 = ldf(c + nu);
+        a11 = ldf(c + nu + 1);
+    }
+    const double ax = dadd(g00x, dmul(fx, dsub(g10x, g00x)));
+    const double bx = dadd(g01x, dmul(fx, dsub(g11x, g01x)));
+    const double ay = dadd(g00y, dmul(fx, dsub(g10y, g00y)));
+    const double by = dadd(g01y, dmul(fx, dsub(g11y, g01y)));
     gx = dadd(ax, dmul(fy, dsub(bx, ax)));
     gy = dadd(ay, dmul(fy, dsub(by, ay)));
+    const double a = lerp_f32diff(a00, a01, fx);
+    const double b = lerp_f32diff(a10, a11, fx);
+    val = dadd(a, dmul(fy, dsub(b, a)));
+}
+
+__device__ __forceinline__ void gradient_ref(const float *__restrict__ rho, int nv, int nu,
+                                             double x, double y, double &gx, double &gy) {
+    double v;
+    gradient_value_ref(rho, nv, nu, x, y, gx, gy, v);
 }
 
 // ---- DDA rasterisation of one segment (_kernels.py:58-77) ------------------
 // Adds `w` to every cell of the segment's 8-connected chain; k starts at k0
 // (0 for an edge's first segment, 1 otherwise: the junction cell belongs to
 // the earlier segment).  A zero-length segment contributes only when k0 == 0.
+// Cell = floor(x0 + (k*dx)*(1/steps) + 0.5) exactly as the reference.
 template <typename T>
 __device__ __forceinline__ void dda_splat(double px0, double py0, double px1,
                                           double py1, int k0, T w,
                                           T *__restrict__ layer, int nv, int nu,
                                           int32_t *__restrict__ status) {
-    const int64_t x0 = cell_round(px0), y0 = cell_round(py0);
-    const int64_t x1 = cell_round(px1), y1 = cell_round(py1);
-    const int64_t dx = x1 - x0, dy = y1 - y0;
-    const int64_t adx = dx < 0 ? -dx : dx, ady = dy < 0 ? -dy : dy;
-    const int64_t steps = adx > ady ? adx : ady;
+    const int x0 = cell_round(px0), y0 = cell_round(py0);
+    const int x1 = cell_round(px1), y1 = cell_round(py1);
+    const int dx = x1 - x0, dy = y1 - y0;
+    const int steps = max(abs(dx), abs(dy));
     if (steps == 0) {
         if (k0 == 0) {
-            if (x0 < 0 || x0 >= nu || y0 < 0 || y0 >= nv) {
+            if ((unsigned)x0 >= (unsigned)nu || (unsigned)y0 >= (unsigned)nv) {
                 atomicOr(status, HB_STATUS_OUT_OF_BOUNDS);
                 return;
             }
@@ -124,10 +168,10 @@ __device__ __forceinline__ void dda_splat(double px0, double py0, double px1,
     }
     const double inv = 1.0 / (double)steps;
     const double fx0 = (double)x0, fy0 = (double)y0;
-    for (int64_t k = k0; k <= steps; ++k) {
-        int64_t u = (int64_t)floor(dadd(dadd(fx0, dmul((double)(k * dx), inv)), 0.5));
-        int64_t v = (int64_t)floor(dadd(dadd(fy0, dmul((double)(k * dy), inv)), 0.5));
-        if (u < 0 || u >= nu || v < 0 || v >= nv) {
+    for (int k = k0; k <= steps; ++k) {
+        const int u = floor_i(dadd(dadd(fx0, dmul((double)(k * dx), inv)), 0.5));
+        const int v = floor_i(dadd(dadd(fy0, dmul((double)(k * dy), inv)), 0.5));
+        if ((unsigned)u >= (unsigned)nu || (unsigned)v >= (unsigned)nv) {
             atomicOr(status, HB_STATUS_OUT_OF_BOUNDS);
             continue;
         }

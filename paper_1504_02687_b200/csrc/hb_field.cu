@@ -189,7 +189,7 @@ size_t hb_smooth_workspace_bytes(int nbins, int nv, int nu) {
 int hb_smooth(const int32_t *counts, const float *hist, const float *matrix, int nbins,
               int nv, int nu, const int32_t *radii, int npasses, float *out,
               void *workspace, size_t workspace_bytes, float *layer_peak, void *stream) {
-    if (nbins < 1 || nv < 1 || nu < 1 || npasses < 1 || !radii || !out || (!counts && !hist))
+    if (nbins < 1 || nv < 1 || nu < 1 || nv > kMaxDim || nu > kMaxDim || npasses < 1 || !radii || !out || (!counts && !hist))
         return set_error(HB_EINVAL, "hb_smooth: bad arguments");
     if (!workspace || workspace_bytes < hb_smooth_workspace_bytes(nbins, nv, nu))
         return set_error(HB_EINVAL, "hb_smooth: workspace too small");
@@ -244,7 +244,7 @@ int hb_smooth(const int32_t *counts, const float *hist, const float *matrix, int
 
 int hb_mix_layers(const int32_t *counts, const float *hist, const float *matrix, int nbins,
                   int nv, int nu, float *out, void *stream) {
-    if (nbins < 1 || nv < 1 || nu < 1 || !out || (!counts && !hist))
+    if (nbins < 1 || nv < 1 || nu < 1 || nv > kMaxDim || nu > kMaxDim || !out || (!counts && !hist))
         return set_error(HB_EINVAL, "hb_mix_layers: bad arguments");
     const int64_t plane = (int64_t)nv * nu;
     dim3 g((unsigned)((plane + 255) / 256), nbins);
@@ -259,7 +259,7 @@ int hb_mix_layers(const int32_t *counts, const float *hist, const float *matrix,
 
 int hb_integral_image(const float *in, int nbins, int nv, int nu, double *table,
                       void *stream) {
-    if (!in || !table || nbins < 1 || nv < 1 || nu < 1)
+    if (!in || !table || nbins < 1 || nv < 1 || nu < 1 || nv > kMaxDim || nu > kMaxDim)
         return set_error(HB_EINVAL, "hb_integral_image: bad arguments");
     cudaStream_t st = as_stream(stream);
     dim3 gc((nu + kColBlock - 1) / kColBlock, nbins);
@@ -272,7 +272,7 @@ int hb_integral_image(const float *in, int nbins, int nv, int nu, double *table,
 
 int hb_used_cells(const float *rho, const float *layer_peak, int nbins, int nv, int nu,
                   double rel, unsigned long long *count, void *stream) {
-    if (!rho || !layer_peak || !count || nbins < 1 || nv < 1 || nu < 1)
+    if (!rho || !layer_peak || !count || nbins < 1 || nv < 1 || nu < 1 || nv > kMaxDim || nu > kMaxDim)
         return set_error(HB_EINVAL, "hb_used_cells: bad arguments");
     const int64_t plane = (int64_t)nv * nu;
     dim3 g((unsigned)((plane + 255) / 256), nbins);

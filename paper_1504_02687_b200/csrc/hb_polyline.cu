@@ -112,10 +112,20 @@ splat_kernel(const double2 *__restrict__ pts, const int64_t *__restrict__ starts
 // ---------------------------------------------------------------------------
 // resample_emit (_kernels.py:235-272) + accumulate of the new polylines,
 // warp per edge.  pos[j] (from the count pass) is the output index of kept
-// point j (-1 if merged).  Kept lane j finds its previous kept point a (the
-// highest kept lane below it, or the carry from earlier chunks), emits
-// pieces-1 inserted points a + (k/pieces)(x - a) then x itself, and
-// rasterises the pieces output segments ending at them.
+// point j (-1 if merged).  A kept point x whose previous kept point is a
+// (pieces = pos[x] - pos[a]) owns outputs pos[a]+1 .. pos[x]: k/pieces
+// interpolants a + (k/pieces)(x - a), then x itself.  Work is balanced over
+// OUTPUT points: in each round lane t produces output m = base + t, finds
+// its owner lane by a 5-step shuffle search over the kept lanes' output
+// positions, writes it (coalesced) and rasterises the segment ending at it.
+// Chunks where every point is kept with one piece skip the search.
+__device__ __forceinline__ double2 interp_piece(double2 a, double2 x, int k, int pieces) {
+    if (k == pieces) return x;
+    if (k == 0) return a;
+    const double t = (double)k / (double)pieces;
+    return make_double2(dadd(a.x, dmul(t, dsub(x.x, a.x))), dadd(a.y, dmul(t, dsub(x.y, a.y))));
+}
+
 __global__ void __launch_bounds__(kStreamBlock)
 emit_kernel(const double2 *__restrict__ pts, const int64_t *__restrict__ starts,
             int64_t n_edges, const int32_t *__restrict__ pos,
@@ -130,52 +140,73 @@ emit_kernel(const double2 *__restrict__ pts, const int64_t *__restrict__ starts,
     for (int64_t e = ((int64_t)blockIdx.x * kStreamBlock + threadIdx.x) / 32; e < n_edges;
          e += nwarps) {
         const int64_t s = starts[e];
-        const int64_t n = starts[e + 1] - s;
+        const int n = (int)(starts[e + 1] - s);
         double2 *o = out + new_starts[e];
         int32_t *layer = hist ? hist + (int64_t)group[e] * plane : nullptr;
         const int32_t w = weight ? weight[e] : 1;
         double2 a = pts[s];  // carry: last kept point so far and its output index
         int apos = 0;
         if (lane == 0) o[0] = a;
-        for (int64_t c0 = 1; c0 < n; c0 += kWarp) {
-            const int64_t j = c0 + lane;
+        for (int c0 = 1; c0 < n; c0 += kWarp) {
+            const int j = c0 + lane;
             const bool valid = j < n;
             const int pj = valid ? pos[s + j] : -1;
             const double2 x = valid ? pts[s + j] : make_double2(0.0, 0.0);
             const bool kept = pj >= 0;
             const unsigned km = __ballot_sync(full, kept);
+            if (km == 0) continue;
             const unsigned below = km & below_mask;
             const int src = below ? 31 - __clz(below) : lane;
             const double px = __shfl_sync(full, x.x, src);
             const double py = __shfl_sync(full, x.y, src);
             const int ppos = __shfl_sync(full, pj, src);
-            if (kept) {
-                const double ax = below ? px : a.x, ay = below ? py : a.y;
-                const int pa = below ? ppos : apos;
-                const int pieces = pj - pa;
-                const double ddx = dsub(x.x, ax), ddy = dsub(x.y, ay);
-                double qx0 = ax, qy0 = ay;
-                for (int kk = 1; kk <= pieces; ++kk) {
-                    double qx = x.x, qy = x.y;
-                    if (kk < pieces) {
-                        const double t = (double)kk / (double)pieces;
-                        qx = dadd(ax, dmul(t, ddx));
-                        qy = dadd(ay, dmul(t, ddy));
-                    }
-                    o[pa + kk] = make_double2(qx, qy);
+            // previous kept point of this lane (valid for kept lanes)
+            const double2 pa2 = below ? make_double2(px, py) : a;
+            const int pa = below ? ppos : apos;
+            const int lk = 31 - __clz(km);
+            const int last_pos = __shfl_sync(full, pj, lk);
+            const bool simple = __all_sync(full, !valid || (kept && pj - pa == 1));
+            if (simple) {
+                // every valid lane is kept with one piece: output pj is x itself
+                if (valid) {
+                    o[pj] = x;
                     if (layer)
-                        dda_splat<int32_t>(qx0, qy0, qx, qy, (pa + kk == 1) ? 0 : 1, w, layer,
-                                           nv, nu, status);
-                    qx0 = qx;
-                    qy0 = qy;
+                        dda_splat<int32_t>(pa2.x, pa2.y, x.x, x.y, pj == 1 ? 0 : 1, w, layer, nv,
+                                           nu, status);
+                }
+            } else {
+                // key: output index of the nearest kept point at or below this lane
+                const int key = kept ? pj : pa;
+                for (int m = apos + 1 + lane; m - lane <= last_pos; m += kWarp) {
+                    int lo = 0;
+#pragma unroll
+                    for (int step = 16; step; step >>= 1) {
+                        const int probe = __shfl_sync(full, key, lo + step - 1);
+                        if (probe < m) lo += step;
+                    }
+                    const int owner = lo > 31 ? 31 : lo;
+                    const double ox = __shfl_sync(full, x.x, owner);
+                    const double oy = __shfl_sync(full, x.y, owner);
+                    const double oax = __shfl_sync(full, pa2.x, owner);
+                    const double oay = __shfl_sync(full, pa2.y, owner);
+                    const int opj = __shfl_sync(full, pj, owner);
+                    const int opa = __shfl_sync(full, pa, owner);
+                    if (m <= last_pos) {
+                        const int pieces = opj - opa, k = m - opa;
+                        const double2 ox2 = make_double2(ox, oy), oa2 = make_double2(oax, oay);
+                        const double2 q = interp_piece(oa2, ox2, k, pieces);
+                        o[m] = q;
+                        if (layer) {
+                            const double2 q0 = interp_piece(oa2, ox2, k - 1, pieces);
+                            dda_splat<int32_t>(q0.x, q0.y, q.x, q.y, m == 1 ? 0 : 1, w, layer,
+                                               nv, nu, status);
+                        }
+                    }
                 }
             }
-            if (km) {
-                const int lk = 31 - __clz(km);
-                a.x = __shfl_sync(full, x.x, lk);
-                a.y = __shfl_sync(full, x.y, lk);
-                apos = __shfl_sync(full, pj, lk);
-            }
+            a.x = __shfl_sync(full, x.x, lk);
+            a.y = __shfl_sync(full, x.y, lk);
+            apos = last_pos;
         }
     }
 }
@@ -230,7 +261,7 @@ int hb_to_world(const double *pts, const int64_t *starts, int64_t n_edges, doubl
 int hb_splat(const double *pts, const int64_t *starts, int64_t n_edges, int64_t n_pts,
              const int32_t *group, const int32_t *weight, int32_t *counts, int nbins,
              int nv, int nu, int32_t *status, void *stream) {
-    if (n_edges < 0 || n_pts < 0 || nbins < 1 || nv < 1 || nu < 1 || !counts || !status ||
+    if (n_edges < 0 || n_pts < 0 || nbins < 1 || nv < 1 || nu < 1 || nv > kMaxDim || nu > kMaxDim || !counts || !status ||
         (n_edges > 0 && (!pts || !starts || !group)))
         return set_error(HB_EINVAL, "hb_splat: bad arguments");
     if (n_edges == 0 || n_pts == 0) return HB_OK;
@@ -244,7 +275,7 @@ int hb_splat(const double *pts, const int64_t *starts, int64_t n_edges, int64_t 
 int hb_splat_f32(const double *pts, const int64_t *starts, int64_t n_edges, int64_t n_pts,
                  const int32_t *group, const float *weight, float *hist, int nbins, int nv,
                  int nu, int32_t *status, void *stream) {
-    if (n_edges < 0 || n_pts < 0 || nbins < 1 || nv < 1 || nu < 1 || !hist || !status ||
+    if (n_edges < 0 || n_pts < 0 || nbins < 1 || nv < 1 || nu < 1 || nv > kMaxDim || nu > kMaxDim || !hist || !status ||
         (n_edges > 0 && (!pts || !starts || !group)))
         return set_error(HB_EINVAL, "hb_splat_f32: bad arguments");
     if (n_edges == 0 || n_pts == 0) return HB_OK;
@@ -301,7 +332,7 @@ int hb_resample_emit(const double *pts, const int64_t *starts, int64_t n_edges,
                      int32_t *counts, int nv, int nu, int32_t *status, void *stream) {
     if (n_edges < 0 || n_pts < 0 ||
         (n_edges > 0 && (!pts || !starts || !pos || !new_starts || !out)) ||
-        (counts && (!group || !status || nv < 1 || nu < 1)))
+        (counts && (!group || !status || nv < 1 || nu < 1 || nv > kMaxDim || nu > kMaxDim)))
         return set_error(HB_EINVAL, "hb_resample_emit: bad arguments");
     if (n_edges == 0 || n_pts == 0) return HB_OK;
     emit_kernel<<<persistent_grid(emit_kernel, n_edges), kStreamBlock, 0, as_stream(stream)>>>(

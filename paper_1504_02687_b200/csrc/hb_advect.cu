@@ -67,6 +67,8 @@ polyline_pass_kernel(const PolylinePass p) {
     const bool do_adv = p.h >= 0.0;
     const bool do_count = p.counts != nullptr;
     const double lo = 0.5 * p.delta, hi = 1.5 * p.delta;  // _kernels.py:211-212
+    const double lo2 = do_count ? sqrt_lt_bound(lo) : 0.0;
+    const double hi2 = do_count ? sqrt_gt_bound(hi) : 0.0;
     // xhi = nu - 1 - INTERIOR_MARGIN (_kernels.py:158-159)
     const double xhi = dsub(dsub((double)p.nu, 1.0), 1.0);
     const double yhi = dsub(dsub((double)p.nv, 1.0), 1.0);
@@ -74,10 +76,16 @@ polyline_pass_kernel(const PolylinePass p) {
     unsigned my_moved = 0;
     double my_disp = 0.0;
 
-    for (int64_t e = ((int64_t)blockIdx.x * kStreamBlock + threadIdx.x) / 32; e < p.n_edges;
-         e += nwarps) {
-        const int64_t s = p.starts[e];
-        const int n = (int)(p.starts[e + 1] - s);
+    int64_t e = ((int64_t)blockIdx.x * kStreamBlock + threadIdx.x) / 32;
+    // the next edge's bounds are fetched one edge ahead and every chunk's raw
+    // points one chunk ahead, so each warp keeps a load in flight while it
+    // runs the advection math
+    int64_t s_nx = 0, t_nx = 0;
+    if (e < p.n_edges) { s_nx = p.starts[e]; t_nx = p.starts[e + 1]; }
+    for (; e < p.n_edges; e += nwarps) {
+        const int64_t s = s_nx;
+        const int n = (int)(t_nx - s);
+        if (e + nwarps < p.n_edges) { s_nx = p.starts[e + nwarps]; t_nx = p.starts[e + nwarps + 1]; }
         const double2 *pin = p.pin + s;
         const float *rho = do_adv ? p.rho + (int64_t)p.edge_layer[e] * p.plane : nullptr;
 
@@ -86,13 +94,14 @@ polyline_pass_kernel(const PolylinePass p) {
         double2 ka = make_double2(0.0, 0.0);    // count: last kept final point
         double2 prevf = ka;                     // count: final point c0 - 1
         int off = 0;                            // count: output index of ka
+        double2 raw = lane < n ? pin[lane] : make_double2(0.0, 0.0);
 
         // iteration c0 stages chunk c0+32 (advect) and finalises chunk c0
         for (int c0 = -kWarp; c0 < n; c0 += kWarp) {
             const int jn = c0 + kWarp + lane;
-            double2 nxt = make_double2(0.0, 0.0);
+            double2 nxt = raw;
+            if (jn + kWarp < n) raw = pin[jn + kWarp];
             if (jn < n) {
-                nxt = pin[jn];
                 if (do_adv && jn > 0 && jn < n - 1) {
                     const Adv a = advect_one(rho, p.nv, p.nu, xhi, yhi, nxt, p.h, p.eps,
                                              p.min_step, p.fixed);
@@ -100,6 +109,8 @@ polyline_pass_kernel(const PolylinePass p) {
                     if (a.moved) my_disp = dadd(my_disp, a.disp);
                     nxt = a.p;
                 }
+            } else {
+                nxt = make_double2(0.0, 0.0);
             }
             if (c0 < 0) {  // prologue: chunk 0 staged
                 cur = nxt;
@@ -130,16 +141,17 @@ polyline_pass_kernel(const PolylinePass p) {
                 double qx = __shfl_up_sync(full, f.x, 1), qy = __shfl_up_sync(full, f.y, 1);
                 if (lane == 0) { qx = prevf.x; qy = prevf.y; }
                 const bool part = valid && j > 0;  // local point 0 is always kept at 0
-                const double gs = part ? hypot_ref(dsub(f.x, qx), dsub(f.y, qy)) : 0.0;
+                // squared gaps; g < lo <=> g2 < lo2 exactly (see sqrt_lt_bound)
+                const double gs = part ? dist2_ref(f.x, f.y, qx, qy) : 0.0;
                 const bool last = (j == n - 1);
                 bool kept = false;
                 double gk = 0.0;
                 int start = (c0 == 0) ? 1 : 0;
                 while (start < kWarp) {
                     double geff = gs;
-                    if (lane == start && part) geff = hypot_ref(dsub(f.x, ka.x), dsub(f.y, ka.y));
+                    if (lane == start && part) geff = dist2_ref(f.x, f.y, ka.x, ka.y);
                     const bool act = part && lane >= start;
-                    const unsigned m = __ballot_sync(full, act && !last && geff < lo);
+                    const unsigned m = __ballot_sync(full, act && !last && geff < lo2);
                     if (m == 0) {
                         if (act) { kept = true; gk = geff; }
                         break;
@@ -154,9 +166,11 @@ polyline_pass_kernel(const PolylinePass p) {
                 }
                 int pieces = 0;
                 if (kept) {
-                    double g = gk;
+                    // while (g > hi) { g *= 0.5; pieces *= 2; }  on squared gaps:
+                    // g * 2^-k > hi  <=>  g2 > 4^k * hi2 (exact power-of-two scaling)
+                    double t = hi2;
                     pieces = 1;
-                    while (g > hi) { g = dmul(g, 0.5); pieces *= 2; }
+                    while (gk > t) { t = dmul(t, 4.0); pieces *= 2; }
                 }
                 int incl = pieces;
 #pragma unroll

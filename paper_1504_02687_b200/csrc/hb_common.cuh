@@ -47,9 +47,40 @@ __device__ __forceinline__ double hypot_ref(double ax, double ay) {
     return sqrt(dadd(dmul(ax, ax), dmul(ay, ay)));
 }
 
-// numba min/max on non-NaN floats
-__device__ __forceinline__ double fmin_ref(double a, double b) { return a < b ? a : b; }
-__device__ __forceinline__ double fmax_ref(double a, double b) { return a > b ? a : b; }
+// numba min/max.  Operands here are never NaN and the clamp bounds are >= 1,
+// so the hardware min/max (DMNMX) returns exactly what `a < b ? a : b` does.
+__device__ __forceinline__ double fmin_ref(double a, double b) { return fmin(a, b); }
+__device__ __forceinline__ double fmax_ref(double a, double b) { return fmax(a, b); }
+
+// Exact sqrt-free comparisons.  sqrt() is correctly rounded and monotone, so
+//   sqrt(d) <  lo  <=>  d <  sqrt_lt_bound(lo)   (smallest d with sqrt(d) >= lo)
+//   sqrt(d) >  hi  <=>  d >  sqrt_gt_bound(hi)   (largest  d with sqrt(d) <= hi)
+// and because scaling by 4^k scales sqrt by exactly 2^k,
+//   sqrt(d) * 2^-k > hi  <=>  d > 4^k * sqrt_gt_bound(hi).
+// neighbouring doubles of a finite positive t
+__device__ __forceinline__ double next_up(double t) {
+    return __longlong_as_double(__double_as_longlong(t) + 1);
+}
+__device__ __forceinline__ double next_down(double t) {
+    return __longlong_as_double(__double_as_longlong(t) - 1);
+}
+__device__ __forceinline__ double sqrt_lt_bound(double lo) {
+    double t = dmul(lo, lo);
+    while (t > 0.0 && sqrt(next_down(t)) >= lo) t = next_down(t);
+    while (sqrt(t) < lo) t = next_up(t);
+    return t;
+}
+__device__ __forceinline__ double sqrt_gt_bound(double hi) {
+    double t = dmul(hi, hi);
+    while (sqrt(next_up(t)) <= hi) t = next_up(t);
+    while (t > 0.0 && sqrt(t) > hi) t = next_down(t);
+    return t;
+}
+// (x-ax)^2 + (y-ay)^2, the argument of the reference's sqrt (_kernels.py:222)
+__device__ __forceinline__ double dist2_ref(double x, double y, double ax, double ay) {
+    const double dx = dsub(x, ax), dy = dsub(y, ay);
+    return dadd(dmul(dx, dx), dmul(dy, dy));
+}
 
 __device__ __forceinline__ float ldf(const float *p) { return __ldg(p); }
 
@@ -168,14 +199,37 @@ __device__ __forceinline__ void dda_splat(double px0, double py0, double px1,
     }
     const double inv = 1.0 / (double)steps;
     const double fx0 = (double)x0, fy0 = (double)y0;
-    for (int k = k0; k <= steps; ++k) {
-        const int u = floor_i(dadd(dadd(fx0, dmul((double)(k * dx), inv)), 0.5));
-        const int v = floor_i(dadd(dadd(fy0, dmul((double)(k * dy), inv)), 0.5));
-        if ((unsigned)u >= (unsigned)nu || (unsigned)v >= (unsigned)nv) {
-            atomicOr(status, HB_STATUS_OUT_OF_BOUNDS);
-            continue;
+    const bool inside = (unsigned)x0 < (unsigned)nu && (unsigned)y0 < (unsigned)nv &&
+                        (unsigned)x1 < (unsigned)nu && (unsigned)y1 < (unsigned)nv;
+    if (!inside) {  // error path: checked per cell, flag raised (raster.py:57-67)
+        for (int k = k0; k <= steps; ++k) {
+            const int u = floor_i(dadd(dadd(fx0, dmul((double)(k * dx), inv)), 0.5));
+            const int v = floor_i(dadd(dadd(fy0, dmul((double)(k * dy), inv)), 0.5));
+            if ((unsigned)u >= (unsigned)nu || (unsigned)v >= (unsigned)nv) {
+                atomicOr(status, HB_STATUS_OUT_OF_BOUNDS);
+                continue;
+            }
+            atomicAdd(layer + v * nu + u, w);
         }
-        atomicAdd(layer + v * nu + u, w);
+        return;
+    }
+    // Every cell lies between the two (in-grid) endpoint cells, so no
+    // per-cell check.  On an axis with |d| == steps the reference's
+    // floor(x0 + (k*d)*(1/steps) + 0.5) is exactly x0 + sign(d)*k: (k*d)*inv
+    // differs from +-k by at most k*2^-52 << 0.5.  Only the other axis needs
+    // the float64 expression.
+    if (abs(dx) == steps) {
+        const int sx = dx > 0 ? 1 : -1;
+        for (int k = k0; k <= steps; ++k) {
+            const int v = floor_i(dadd(dadd(fy0, dmul((double)(k * dy), inv)), 0.5));
+            atomicAdd(layer + v * nu + (x0 + sx * k), w);
+        }
+    } else {
+        const int sy = dy > 0 ? 1 : -1;
+        for (int k = k0; k <= steps; ++k) {
+            const int u = floor_i(dadd(dadd(fx0, dmul((double)(k * dx), inv)), 0.5));
+            atomicAdd(layer + (y0 + sy * k) * nu + u, w);
+        }
     }
 }
 

@@ -122,7 +122,9 @@ splat_kernel(const double2 *__restrict__ pts, const int64_t *__restrict__ starts
 __device__ __forceinline__ double2 interp_piece(double2 a, double2 x, int k, int pieces) {
     if (k == pieces) return x;
     if (k == 0) return a;
-    const double t = (double)k / (double)pieces;
+    // t = k / pieces (_kernels.py:264); pieces is a power of two, so the
+    // quotient is exact and equals k times the exact reciprocal
+    const double t = dmul((double)k, __drcp_rn((double)pieces));
     return make_double2(dadd(a.x, dmul(t, dsub(x.x, a.x))), dadd(a.y, dmul(t, dsub(x.y, a.y))));
 }
 
@@ -137,21 +139,35 @@ emit_kernel(const double2 *__restrict__ pts, const int64_t *__restrict__ starts,
     const int lane = threadIdx.x & 31;
     const unsigned below_mask = (1u << lane) - 1u;
     const int64_t nwarps = (int64_t)gridDim.x * (kStreamBlock / 32);
-    for (int64_t e = ((int64_t)blockIdx.x * kStreamBlock + threadIdx.x) / 32; e < n_edges;
-         e += nwarps) {
-        const int64_t s = starts[e];
-        const int n = (int)(starts[e + 1] - s);
+    int64_t e = ((int64_t)blockIdx.x * kStreamBlock + threadIdx.x) / 32;
+    // next edge's bounds are fetched one edge ahead, its first chunk one
+    // chunk ahead, so a warp always has a load in flight while it computes
+    int64_t s_nx = 0, t_nx = 0;
+    if (e < n_edges) { s_nx = starts[e]; t_nx = starts[e + 1]; }
+    for (; e < n_edges; e += nwarps) {
+        const int64_t s = s_nx;
+        const int n = (int)(t_nx - s);
+        if (e + nwarps < n_edges) { s_nx = starts[e + nwarps]; t_nx = starts[e + nwarps + 1]; }
         double2 *o = out + new_starts[e];
         int32_t *layer = hist ? hist + (int64_t)group[e] * plane : nullptr;
         const int32_t w = weight ? weight[e] : 1;
-        double2 a = pts[s];  // carry: last kept point so far and its output index
-        int apos = 0;
-        if (lane == 0) o[0] = a;
-        for (int c0 = 1; c0 < n; c0 += kWarp) {
+        // carry: last kept point so far and its output index (none yet)
+        double2 a = make_double2(0.0, 0.0);
+        int apos = -1;
+        int pj_nx = lane < n ? pos[s + lane] : -1;
+        double2 x_nx = lane < n ? pts[s + lane] : make_double2(0.0, 0.0);
+        for (int c0 = 0; c0 < n; c0 += kWarp) {
+            // local point 0 has pos 0: it is output 0 and the first `a`
             const int j = c0 + lane;
             const bool valid = j < n;
-            const int pj = valid ? pos[s + j] : -1;
-            const double2 x = valid ? pts[s + j] : make_double2(0.0, 0.0);
+            const int pj = pj_nx;
+            const double2 x = x_nx;
+            if (j + kWarp < n) {
+                pj_nx = pos[s + j + kWarp];
+                x_nx = pts[s + j + kWarp];
+            } else {
+                pj_nx = -1;  // past the end of the edge
+            }
             const bool kept = pj >= 0;
             const unsigned km = __ballot_sync(full, kept);
             if (km == 0) continue;
@@ -170,7 +186,7 @@ emit_kernel(const double2 *__restrict__ pts, const int64_t *__restrict__ starts,
                 // every valid lane is kept with one piece: output pj is x itself
                 if (valid) {
                     o[pj] = x;
-                    if (layer)
+                    if (layer && pj >= 1)
                         dda_splat<int32_t>(pa2.x, pa2.y, x.x, x.y, pj == 1 ? 0 : 1, w, layer, nv,
                                            nu, status);
                 }
@@ -196,7 +212,7 @@ emit_kernel(const double2 *__restrict__ pts, const int64_t *__restrict__ starts,
                         const double2 ox2 = make_double2(ox, oy), oa2 = make_double2(oax, oay);
                         const double2 q = interp_piece(oa2, ox2, k, pieces);
                         o[m] = q;
-                        if (layer) {
+                        if (layer && m >= 1) {
                             const double2 q0 = interp_piece(oa2, ox2, k - 1, pieces);
                             dda_splat<int32_t>(q0.x, q0.y, q.x, q.y, m == 1 ? 0 : 1, w, layer,
                                                nv, nu, status);

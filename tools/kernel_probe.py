@@ -1,0 +1,110 @@
+"""Decompose the per-iteration kernels on a realistic mid-run state.
+
+    python tools/kernel_probe.py [--config 4] [--iters 6]
+
+Runs the workload for --iters iterations (so the polylines are bundled and
+resampled like in the timed loop), then times, with CUDA events on the
+current stream, variants of the two dominant kernels:
+  emit+splat, emit only, splat only (standalone), advect+lap+count,
+  advect+lap, lap only, count only.
+Prints one JSON object.  Diagnostic tool; not part of the product path.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import sys
+
+import torch
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+
+from paper_1504_02687_b200 import _native as N  # noqa: E402
+from paper_1504_02687_b200 import bundler as B  # noqa: E402
+from paper_1504_02687_b200.engine import MIN_STEP, ptr, stream_ptr  # noqa: E402
+from paper_1504_02687_b200.workloads import workload  # noqa: E402
+
+
+def timed(fn, reps=5):
+    fn()
+    torch.cuda.synchronize()
+    a = torch.cuda.Event(enable_timing=True)
+    b = torch.cuda.Event(enable_timing=True)
+    a.record()
+    for _ in range(reps):
+        fn()
+    b.record()
+    torch.cuda.synchronize()
+    return a.elapsed_time(b) / reps
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--config", type=int, default=4)
+    ap.add_argument("--iters", type=int, default=6)
+    args = ap.parse_args()
+    w = workload(args.config)
+    eng, tr, _, _ = B.prepare_engine(w.graph, w.config, bins=w.bins, matrix=w.matrix)
+    for _ in range(args.iters):
+        eng.step()
+    torch.cuda.synchronize()
+    s = stream_ptr()
+    E, Bn, nv, nu = eng.n_edges, eng.nbins, eng.nv, eng.nu
+    # state: eng.pts holds final points of iteration iters-1, ecounts/pos valid
+    N.call("hb_scan_counts", ptr(eng.ecounts), E, ptr(eng.starts_alt), ptr(eng.scan_ws),
+           eng.scan_ws.numel(), s)
+    n_new = int(eng.starts_alt[E].item())
+    eng._ensure_capacity(n_new)
+    n_old = eng.n_pts
+    out = {"config": w.name, "iteration_state": args.iters, "n_old": n_old, "n_new": n_new,
+           "edges": E}
+
+    def emit(splat: bool):
+        if splat:
+            eng.hist.zero_()
+        N.call("hb_resample_emit", ptr(eng.pts), ptr(eng.starts), E, n_old, ptr(eng.pos),
+               ptr(eng.starts_alt), ptr(eng.alt), ptr(eng.groups), ptr(eng.wint),
+               ptr(eng.hist) if splat else None, nv, nu, ptr(eng.status), s)
+
+    out["emit_splat_ms"] = timed(lambda: emit(True))
+    out["emit_only_ms"] = timed(lambda: emit(False))
+    out["hist_zero_ms"] = timed(lambda: eng.hist.zero_())
+
+    def splat():
+        eng.hist.zero_()
+        N.call("hb_splat", ptr(eng.alt), ptr(eng.starts_alt), E, n_new, ptr(eng.groups),
+               ptr(eng.wint), ptr(eng.hist), Bn, nv, nu, ptr(eng.status), s)
+
+    out["splat_only_ms"] = timed(splat)
+    hist = eng.hist.clone()
+    out["hist_max"] = int(hist.max().item())
+    out["hist_nonzero_frac"] = float((hist > 0).float().mean().item())
+    out["hist_sum"] = int(hist.sum().item())
+    # field for advect
+    N.call("hb_smooth", ptr(eng.hist), None, ptr(eng.mat_dev), Bn, nv, nu,
+           eng.radii.data_ptr(), int(eng.radii.numel()), ptr(eng.field), ptr(eng.smooth_ws),
+           eng.smooth_ws.numel(), ptr(eng.peak), s)
+    cfg = w.config
+    h = cfg.lambda_ ** args.iters * cfg.h_max
+    work = torch.empty_like(eng.alt)
+
+    def adv(h_, lap, count):
+        N.call("hb_advect_laplacian", ptr(eng.alt), ptr(work), ptr(eng.starts_alt), E, n_new,
+               ptr(eng.groups), ptr(eng.field), Bn, nv, nu, float(h_), float(cfg.epsilon),
+               MIN_STEP, 0, float(cfg.laplacian_factor), lap, float(cfg.delta),
+               ptr(eng.ecounts) if count else None, ptr(eng.pos) if count else None,
+               eng.m_moved.data_ptr(), ptr(eng._partials), s)
+
+    out["adv_lap_count_ms"] = timed(lambda: adv(h, 1, True))
+    out["adv_lap_ms"] = timed(lambda: adv(h, 1, False))
+    out["adv_only_ms"] = timed(lambda: adv(h, 0, False))
+    out["lap_only_ms"] = timed(lambda: adv(-1.0, 1, False))
+    out["count_only_ms"] = timed(lambda: adv(-1.0, 0, True))
+    out["copy_pts_ms"] = timed(lambda: work[:n_new].copy_(eng.alt[:n_new]))
+    print(json.dumps(out))
+
+
+if __name__ == "__main__":
+    main()

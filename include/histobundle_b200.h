@@ -44,6 +44,26 @@ extern "C" {
 /* status-flag bits written by device kernels (caller-owned int32) */
 #define HB_STATUS_OUT_OF_BOUNDS 1 /* raster.py:57-67 "sample out of bounds" */
 
+/* Tile-binned splatting state (all pointers caller-owned device memory).
+ * The grid of every layer is cut into tile x tile cells; a segment is binned
+ * to the tile holding its first cell and rasterised later into a
+ * shared-memory window of (tile + 2*halo)^2 cells, so the histogram sees one
+ * global atomic per touched cell per work chunk instead of one per
+ * increment.  Records are 8 bytes: start cell (2 x u16), cell delta
+ * (2 x s8), k0 (1 bit), integer weight (15 bits). */
+typedef struct hb_tiles {
+    int tile, halo;      /* cells */
+    int ntx, nty;        /* tiles per row / per column of one layer */
+    int nbins;           /* layers */
+    int ntiles;          /* nbins * ntx * nty */
+    int64_t *off;        /* (ntiles+1) bucket offsets into rec */
+    int32_t *cap;        /* (ntiles) bucket capacities */
+    int32_t *fill;       /* (ntiles) records claimed (demand, may exceed cap) */
+    int32_t *work;       /* (ntiles+2) scratch: flush chunk prefix + counter */
+    uint64_t *rec;       /* off[ntiles] records; NULL = census only */
+    int64_t rec_capacity;
+} hb_tiles;
+
 HB_API int hb_abi_version(void);
 HB_API const char *hb_last_error(void);
 HB_API int hb_device_sm_count(void);
@@ -70,6 +90,22 @@ HB_API int hb_to_world(const double *pts, const int64_t *starts, int64_t n_edges
                        const double *src_world, const double *dst_world, double *out,
                        void *stream);
 
+/* Tile geometry for a (nbins, nv, nu) grid whose segments span at most
+ * max_seg_cells cells per axis (host only; fills tile/halo/ntx/nty/nbins/
+ * ntiles, leaves the pointers alone).  Returns HB_EINVAL when binning does
+ * not apply (grid wider than 65535, segments longer than 127 cells). */
+HB_API int hb_tiles_geometry(int nbins, int nv, int nu, double max_seg_cells,
+                             hb_tiles *t);
+
+/* Bucket capacities for the next binned pass from the demand of the last
+ * one: cap = fill + fill/4 + 64, off = exclusive prefix, fill := 0, and
+ * *total (device int64) = off[ntiles], the records the pass may write. */
+HB_API int hb_tiles_plan(const hb_tiles *t, int64_t *total, void *stream);
+
+/* Rasterise every binned record into counts (int32 (B,V,U)). */
+HB_API int hb_tiles_flush(const hb_tiles *t, int32_t *counts, int nv, int nu,
+                          void *stream);
+
 /* _kernels.accumulate (_kernels.py:46-77) via raster._accumulate_packed
  * (raster.py:70-94), per-group form: counts[group[e]] += weight[e] on every
  * rasterised cell of edge e.  weight may be NULL (all 1).  counts must be
@@ -77,7 +113,11 @@ HB_API int hb_to_world(const double *pts, const int64_t *starts, int64_t n_edges
 HB_API int hb_splat(const double *pts, const int64_t *starts, int64_t n_edges,
              int64_t n_pts, const int32_t *group, const int32_t *weight,
              int32_t *counts, int nbins, int nv, int nu, int32_t *status,
-             void *stream);
+             const hb_tiles *tiles, void *stream);
+/* `tiles` (nullable): with tiles->rec == NULL the splat still adds straight
+ * into counts but records each tile's demand in tiles->fill (census for the
+ * next hb_tiles_plan); with rec != NULL segments are binned and the caller
+ * finishes with hb_tiles_flush.  hb_resample_emit takes the same argument. */
 
 /* Same rasterisation with float32 weights (non-integer edge weights):
  * hist[group[e]] += weight[e] with float atomics (order-dependent in the
@@ -165,7 +205,7 @@ HB_API int hb_resample_emit(const double *pts, const int64_t *starts,
                      const int64_t *new_starts, double *out,
                      const int32_t *group, const int32_t *weight,
                      int32_t *counts, int nv, int nu, int32_t *status,
-                     void *stream);
+                     const hb_tiles *tiles, void *stream);
 
 /* Per-point probes used by the single-point operator API
  * (bundler.density_at / gradient_at, bundler.py:203-217). */

@@ -18,7 +18,7 @@ LIB_DIR = os.path.join(_PKG, "_lib")
 LIB_PATH = os.path.join(LIB_DIR, "libhb_b200.so")
 INCLUDE = os.path.join(os.path.dirname(_PKG), "include")
 
-SOURCES = ["hb_api.cu", "hb_polyline.cu", "hb_field.cu", "hb_advect.cu"]
+SOURCES = ["hb_api.cu", "hb_polyline.cu", "hb_field.cu", "hb_advect.cu", "hb_splat.cu"]
 
 NVCC_FLAGS = [
     "-gencode", "arch=compute_100a,code=sm_100a",
@@ -65,7 +65,10 @@ SIGNATURES = {
     "hb_sample_fill": (_I, [_P, _P, _P, _I64, _P, _P]),
     "hb_offset": (_I, [_P, _P, _I64, _P, _P]),
     "hb_to_world": (_I, [_P, _P, _I64, _D, _D, _D, _P, _P, _P, _P]),
-    "hb_splat": (_I, [_P, _P, _I64, _I64, _P, _P, _P, _I, _I, _I, _P, _P]),
+    "hb_tiles_geometry": (_I, [_I, _I, _I, _D, _P]),
+    "hb_tiles_plan": (_I, [_P, _P, _P]),
+    "hb_tiles_flush": (_I, [_P, _P, _I, _I, _P]),
+    "hb_splat": (_I, [_P, _P, _I64, _I64, _P, _P, _P, _I, _I, _I, _P, _P, _P]),
     "hb_splat_f32": (_I, [_P, _P, _I64, _I64, _P, _P, _P, _I, _I, _I, _P, _P]),
     "hb_smooth_workspace_bytes": (_SZ, [_I, _I, _I]),
     "hb_smooth": (_I, [_P, _P, _P, _I, _I, _I, _P, _I, _P, _P, _SZ, _P, _P]),
@@ -80,9 +83,19 @@ SIGNATURES = {
     "hb_scan_workspace_bytes": (_SZ, [_I64]),
     "hb_scan_counts": (_I, [_P, _I64, _P, _P, _SZ, _P]),
     "hb_resample_emit": (_I, [_P, _P, _I64, _I64, _P, _P, _P, _P, _P, _P, _I, _I, _P,
-                              _P]),
+                              _P, _P]),
     "hb_probe": (_I, [_P, _I, _I, _P, _I64, _P, _P, _P]),
 }
+
+class HbTiles(ctypes.Structure):
+    """Mirror of ``hb_tiles`` (include/histobundle_b200.h)."""
+
+    _fields_ = [("tile", ctypes.c_int), ("halo", ctypes.c_int), ("ntx", ctypes.c_int),
+                ("nty", ctypes.c_int), ("nbins", ctypes.c_int), ("ntiles", ctypes.c_int),
+                ("off", ctypes.c_void_p), ("cap", ctypes.c_void_p), ("fill", ctypes.c_void_p),
+                ("work", ctypes.c_void_p), ("rec", ctypes.c_void_p),
+                ("rec_capacity", ctypes.c_int64)]
+
 
 _lib = None
 

@@ -344,7 +344,7 @@ def resample(polyline: SampledEdge, delta: float) -> None:
     m = int(new_starts[1].item())
     out = torch.empty((m, 2), dtype=torch.float64, device=pts.device)
     N.call("hb_resample_emit", ptr(pts), ptr(starts), 1, n, ptr(pos), ptr(new_starts), ptr(out),
-           None, None, None, 1, 1, None, s)
+           None, None, None, 1, 1, None, None, s)
     polyline.points = out.cpu().numpy()
 
 

@@ -233,6 +233,83 @@ __device__ __forceinline__ void dda_splat(double px0, double py0, double px1,
     }
 }
 
+// The same cell chain from integer endpoint cells already known to be inside
+// the grid (the tile rasteriser replays binned records with it).
+template <typename Visit>
+__device__ __forceinline__ void dda_walk(int x0, int y0, int x1, int y1, int k0, Visit visit) {
+    const int dx = x1 - x0, dy = y1 - y0;
+    const int steps = max(abs(dx), abs(dy));
+    if (steps == 0) {
+        if (k0 == 0) visit(x0, y0);
+        return;
+    }
+    const double inv = 1.0 / (double)steps;
+    if (abs(dx) == steps) {
+        const int sx = dx > 0 ? 1 : -1;
+        const double fy0 = (double)y0;
+        for (int k = k0; k <= steps; ++k)
+            visit(x0 + sx * k, floor_i(dadd(dadd(fy0, dmul((double)(k * dy), inv)), 0.5)));
+    } else {
+        const int sy = dy > 0 ? 1 : -1;
+        const double fx0 = (double)x0;
+        for (int k = k0; k <= steps; ++k)
+            visit(floor_i(dadd(dadd(fx0, dmul((double)(k * dx), inv)), 0.5)), y0 + sy * k);
+    }
+}
+
+// ---- tile binning of segments (hb_splat.cu rasterises the buckets) ---------
+__device__ __forceinline__ uint64_t encode_seg(int x0, int y0, int dx, int dy, int k0, int w) {
+    return (uint64_t)(uint16_t)x0 | ((uint64_t)(uint16_t)y0 << 16) |
+           ((uint64_t)(uint8_t)(int8_t)dx << 32) | ((uint64_t)(uint8_t)(int8_t)dy << 40) |
+           ((uint64_t)(k0 & 1) << 48) | ((uint64_t)(w & 0x7fff) << 49);
+}
+
+// One segment per lane (has == false: none).  Every lane of the warp must
+// call this (warp-aggregated bucket claims).  Binnable segments go to their
+// tile's bucket; everything else -- census mode (no record storage), bucket
+// overflow, non-unit float weights, long or out-of-grid segments -- is
+// rasterised straight into the histogram exactly as before.
+template <typename T>
+__device__ __forceinline__ void bin_or_splat(bool has, double px0, double py0, double px1,
+                                             double py1, int k0, T w, int grp,
+                                             T *__restrict__ hist, int64_t plane, int nv, int nu,
+                                             int32_t *__restrict__ status,
+                                             const hb_tiles *__restrict__ tl) {
+    bool direct = has;
+    int tile = -1;
+    uint64_t rec = 0;
+    if (has && tl) {
+        const int x0 = cell_round(px0), y0 = cell_round(py0);
+        const int dx = cell_round(px1) - x0, dy = cell_round(py1) - y0;
+        const int iw = (int)w;
+        if (dx == 0 && dy == 0 && k0 == 1) {
+            direct = false;  // adds nothing (_kernels.py:67-71)
+        } else if ((unsigned)x0 < (unsigned)nu && (unsigned)y0 < (unsigned)nv &&
+                   (unsigned)(x0 + dx) < (unsigned)nu && (unsigned)(y0 + dy) < (unsigned)nv &&
+                   abs(dx) <= 127 && abs(dy) <= 127 && (T)iw == w && iw >= 1 && iw <= 0x7fff) {
+            tile = (grp * tl->nty + y0 / tl->tile) * tl->ntx + x0 / tl->tile;
+            rec = encode_seg(x0, y0, dx, dy, k0, iw);
+        }
+    }
+    if (tl) {
+        const unsigned full = 0xffffffffu;
+        const int lane = threadIdx.x & 31;
+        const unsigned peers = __match_any_sync(full, tile);
+        const int leader = __ffs(peers) - 1;
+        int base = 0;
+        if (tile >= 0 && lane == leader) base = atomicAdd(tl->fill + tile, __popc(peers));
+        base = __shfl_sync(full, base, leader);
+        if (tile >= 0) {
+            const int slot = base + __popc(peers & ((1u << lane) - 1u));
+            if (tl->rec && slot < tl->cap[tile]) {
+                tl->rec[tl->off[tile] + slot] = rec;
+                direct = false;
+            }
+        }
+    }
+    if (direct) dda_splat<T>(px0, py0, px1, py1, k0, w, hist + (int64_t)grp * plane, nv, nu, status);
+}
+
 // ---- persistent warp-per-edge kernels ---------------------------------------
 constexpr int kStreamBlock = 256;      // 8 warps
 constexpr int kMaxStreamBlocks = 4096; // grid cap; also the metric-partials size

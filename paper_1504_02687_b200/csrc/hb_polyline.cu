@@ -85,7 +85,9 @@ __global__ void __launch_bounds__(kStreamBlock)
 splat_kernel(const double2 *__restrict__ pts, const int64_t *__restrict__ starts,
              int64_t n_edges, const int32_t *__restrict__ group,
              const T *__restrict__ weight, T *__restrict__ hist, int64_t plane, int nv,
-             int nu, int32_t *__restrict__ status) {
+             int nu, int32_t *__restrict__ status, const __grid_constant__ hb_tiles tl,
+             int use_tiles) {
+    const hb_tiles *tiles = use_tiles ? &tl : nullptr;
     const unsigned full = 0xffffffffu;
     const int lane = threadIdx.x & 31;
     const int64_t nwarps = (int64_t)gridDim.x * (kStreamBlock / 32);
@@ -93,7 +95,7 @@ splat_kernel(const double2 *__restrict__ pts, const int64_t *__restrict__ starts
          e += nwarps) {
         const int64_t s = starts[e];
         const int64_t n = starts[e + 1] - s;
-        T *layer = hist + (int64_t)group[e] * plane;
+        const int grp = group[e];
         const T w = weight ? weight[e] : T(1);
         double2 prev = pts[s];
         for (int64_t c0 = 1; c0 < n; c0 += kWarp) {
@@ -102,7 +104,8 @@ splat_kernel(const double2 *__restrict__ pts, const int64_t *__restrict__ starts
             const double2 p = valid ? pts[s + j] : make_double2(0.0, 0.0);
             double qx = __shfl_up_sync(full, p.x, 1), qy = __shfl_up_sync(full, p.y, 1);
             if (lane == 0) { qx = prev.x; qy = prev.y; }
-            if (valid) dda_splat<T>(qx, qy, p.x, p.y, j == 1 ? 0 : 1, w, layer, nv, nu, status);
+            bin_or_splat<T>(valid, qx, qy, p.x, p.y, j == 1 ? 0 : 1, w, grp, hist, plane, nv, nu,
+                            status, tiles);
             prev.x = __shfl_sync(full, p.x, 31);
             prev.y = __shfl_sync(full, p.y, 31);
         }
@@ -134,7 +137,8 @@ emit_kernel(const double2 *__restrict__ pts, const int64_t *__restrict__ starts,
             const int64_t *__restrict__ new_starts, double2 *__restrict__ out,
             const int32_t *__restrict__ group, const int32_t *__restrict__ weight,
             int32_t *__restrict__ hist, int64_t plane, int nv, int nu,
-            int32_t *__restrict__ status) {
+            int32_t *__restrict__ status, const __grid_constant__ hb_tiles tl, int use_tiles) {
+    const hb_tiles *tiles = use_tiles ? &tl : nullptr;
     const unsigned full = 0xffffffffu;
     const int lane = threadIdx.x & 31;
     const unsigned below_mask = (1u << lane) - 1u;
@@ -149,7 +153,8 @@ emit_kernel(const double2 *__restrict__ pts, const int64_t *__restrict__ starts,
         const int n = (int)(t_nx - s);
         if (e + nwarps < n_edges) { s_nx = starts[e + nwarps]; t_nx = starts[e + nwarps + 1]; }
         double2 *o = out + new_starts[e];
-        int32_t *layer = hist ? hist + (int64_t)group[e] * plane : nullptr;
+        const bool splat = hist != nullptr;
+        const int grp = splat ? group[e] : 0;
         const int32_t w = weight ? weight[e] : 1;
         // carry: last kept point so far and its output index (none yet)
         double2 a = make_double2(0.0, 0.0);
@@ -184,12 +189,11 @@ emit_kernel(const double2 *__restrict__ pts, const int64_t *__restrict__ starts,
             const bool simple = __all_sync(full, !valid || (kept && pj - pa == 1));
             if (simple) {
                 // every valid lane is kept with one piece: output pj is x itself
-                if (valid) {
-                    o[pj] = x;
-                    if (layer && pj >= 1)
-                        dda_splat<int32_t>(pa2.x, pa2.y, x.x, x.y, pj == 1 ? 0 : 1, w, layer, nv,
-                                           nu, status);
-                }
+                if (valid) o[pj] = x;
+                if (splat)
+                    bin_or_splat<int32_t>(valid && pj >= 1, pa2.x, pa2.y, x.x, x.y,
+                                          pj == 1 ? 0 : 1, w, grp, hist, plane, nv, nu, status,
+                                          tiles);
             } else {
                 // key: output index of the nearest kept point at or below this lane
                 const int key = kept ? pj : pa;
@@ -207,17 +211,19 @@ emit_kernel(const double2 *__restrict__ pts, const int64_t *__restrict__ starts,
                     const double oay = __shfl_sync(full, pa2.y, owner);
                     const int opj = __shfl_sync(full, pj, owner);
                     const int opa = __shfl_sync(full, pa, owner);
-                    if (m <= last_pos) {
+                    const bool here = m <= last_pos;
+                    double2 q = make_double2(0.0, 0.0), q0 = q;
+                    if (here) {
                         const int pieces = opj - opa, k = m - opa;
                         const double2 ox2 = make_double2(ox, oy), oa2 = make_double2(oax, oay);
-                        const double2 q = interp_piece(oa2, ox2, k, pieces);
+                        q = interp_piece(oa2, ox2, k, pieces);
+                        q0 = interp_piece(oa2, ox2, k - 1, pieces);
                         o[m] = q;
-                        if (layer && m >= 1) {
-                            const double2 q0 = interp_piece(oa2, ox2, k - 1, pieces);
-                            dda_splat<int32_t>(q0.x, q0.y, q.x, q.y, m == 1 ? 0 : 1, w, layer,
-                                               nv, nu, status);
-                        }
                     }
+                    if (splat)
+                        bin_or_splat<int32_t>(here && m >= 1, q0.x, q0.y, q.x, q.y,
+                                              m == 1 ? 0 : 1, w, grp, hist, plane, nv, nu, status,
+                                              tiles);
                 }
             }
             a.x = __shfl_sync(full, x.x, lk);
@@ -276,7 +282,7 @@ int hb_to_world(const double *pts, const int64_t *starts, int64_t n_edges, doubl
 
 int hb_splat(const double *pts, const int64_t *starts, int64_t n_edges, int64_t n_pts,
              const int32_t *group, const int32_t *weight, int32_t *counts, int nbins,
-             int nv, int nu, int32_t *status, void *stream) {
+             int nv, int nu, int32_t *status, const hb_tiles *tiles, void *stream) {
     if (n_edges < 0 || n_pts < 0 || nbins < 1 || nv < 1 || nu < 1 || nv > kMaxDim || nu > kMaxDim || !counts || !status ||
         (n_edges > 0 && (!pts || !starts || !group)))
         return set_error(HB_EINVAL, "hb_splat: bad arguments");
@@ -284,7 +290,7 @@ int hb_splat(const double *pts, const int64_t *starts, int64_t n_edges, int64_t 
     splat_kernel<int32_t><<<persistent_grid(splat_kernel<int32_t>, n_edges), kStreamBlock, 0,
                             as_stream(stream)>>>(
         reinterpret_cast<const double2 *>(pts), starts, n_edges, group, weight, counts,
-        (int64_t)nv * nu, nv, nu, status);
+        (int64_t)nv * nu, nv, nu, status, tiles ? *tiles : hb_tiles{}, tiles != nullptr);
     return check_launch("hb_splat");
 }
 
@@ -298,7 +304,7 @@ int hb_splat_f32(const double *pts, const int64_t *starts, int64_t n_edges, int6
     splat_kernel<float><<<persistent_grid(splat_kernel<float>, n_edges), kStreamBlock, 0,
                           as_stream(stream)>>>(
         reinterpret_cast<const double2 *>(pts), starts, n_edges, group, weight, hist,
-        (int64_t)nv * nu, nv, nu, status);
+        (int64_t)nv * nu, nv, nu, status, hb_tiles{}, 0);
     return check_launch("hb_splat_f32");
 }
 
@@ -345,7 +351,8 @@ int hb_scan_counts(const int64_t *counts, int64_t n_edges, int64_t *new_starts,
 int hb_resample_emit(const double *pts, const int64_t *starts, int64_t n_edges,
                      int64_t n_pts, const int32_t *pos, const int64_t *new_starts,
                      double *out, const int32_t *group, const int32_t *weight,
-                     int32_t *counts, int nv, int nu, int32_t *status, void *stream) {
+                     int32_t *counts, int nv, int nu, int32_t *status, const hb_tiles *tiles,
+                     void *stream) {
     if (n_edges < 0 || n_pts < 0 ||
         (n_edges > 0 && (!pts || !starts || !pos || !new_starts || !out)) ||
         (counts && (!group || !status || nv < 1 || nu < 1 || nv > kMaxDim || nu > kMaxDim)))
@@ -354,7 +361,7 @@ int hb_resample_emit(const double *pts, const int64_t *starts, int64_t n_edges,
     emit_kernel<<<persistent_grid(emit_kernel, n_edges), kStreamBlock, 0, as_stream(stream)>>>(
         reinterpret_cast<const double2 *>(pts), starts, n_edges, pos, new_starts,
         reinterpret_cast<double2 *>(out), group, weight, counts, (int64_t)nv * nu, nv, nu,
-        status);
+        status, tiles ? *tiles : hb_tiles{}, (counts && tiles) ? 1 : 0);
     return check_launch("hb_resample_emit");
 }
 

@@ -21,6 +21,7 @@ buffer). Metrics stay on the device until the run ends unless an
 
 from __future__ import annotations
 
+import ctypes
 import math
 from dataclasses import dataclass, field
 
@@ -172,6 +173,27 @@ class BundleEngine:
         self.smooth_ws = torch.empty(sws, dtype=torch.uint8, device=dev)
         scw = N.lib().hb_scan_workspace_bytes(max(E, 1))
         self.scan_ws = torch.empty(scw, dtype=torch.uint8, device=dev)
+        # tile-binned splatting (hb_splat.cu); segments are at most 1.5*delta
+        # long after resampling (and delta before), + rounding slack
+        self.tiles = None
+        if self.wkind != "float":
+            geo = N.HbTiles()
+            if N.lib().hb_tiles_geometry(B, self.nv, self.nu, 1.5 * self.delta + 2.0,
+                                         ctypes.byref(geo)) == 0:
+                nt = geo.ntiles
+                self.t_off = torch.zeros(nt + 1, dtype=torch.int64, device=dev)
+                self.t_cap = torch.zeros(nt, dtype=torch.int32, device=dev)
+                self.t_fill = torch.zeros(nt, dtype=torch.int32, device=dev)
+                self.t_work = torch.zeros(nt + 2, dtype=torch.int32, device=dev)
+                self.t_total = torch.zeros(1, dtype=torch.int64, device=dev)
+                self.t_rec = torch.empty(max(int(self.n_pts * 1.5), 4096), dtype=torch.int64,
+                                         device=dev)
+                geo.off, geo.cap = self.t_off.data_ptr(), self.t_cap.data_ptr()
+                geo.fill, geo.work = self.t_fill.data_ptr(), self.t_work.data_ptr()
+                geo.rec, geo.rec_capacity = self.t_rec.data_ptr(), self.t_rec.numel()
+                self.tiles = geo
+                self.tiles_census = N.HbTiles.from_buffer_copy(geo)
+                self.tiles_census.rec = None
         self.lap_passes = int(cfg.laplacian_passes)
         self._partials = torch.zeros(int(N.lib().hb_advect_partials()), dtype=torch.float64,
                                      device=dev)
@@ -221,10 +243,29 @@ class BundleEngine:
         b.record()
         self.trace.setdefault(name, []).append((a, b, self.iteration))
 
-    def _splat_args(self):
+    def _splat(self, s) -> None:
+        """Straight splat of the current points (iteration 0 / float weights);
+        with tiles it also takes the per-tile census for the next plan."""
+        E, B, nv, nu = self.n_edges, self.nbins, self.nv, self.nu
         if self.wkind == "float":
-            return "hb_splat_f32", ptr(self.wf32)
-        return "hb_splat", ptr(self.wint)
+            self._k("hb_splat_f32", ptr(self.pts), ptr(self.starts), E, self.n_pts,
+                    ptr(self.groups), ptr(self.wf32), ptr(self.hist), B, nv, nu,
+                    ptr(self.status), s)
+            return
+        census = None
+        if self.tiles is not None:
+            self.t_fill.zero_()
+            census = ctypes.byref(self.tiles_census)
+        self._k("hb_splat", ptr(self.pts), ptr(self.starts), E, self.n_pts, ptr(self.groups),
+                ptr(self.wint), ptr(self.hist), B, nv, nu, ptr(self.status), census, s)
+
+    def _ensure_records(self, n: int) -> None:
+        if n <= self.t_rec.numel():
+            return
+        self.t_rec = torch.empty(max(n, self.t_rec.numel() * 5 // 4), dtype=torch.int64,
+                                 device=self.dev)
+        self.tiles.rec = self.t_rec.data_ptr()
+        self.tiles.rec_capacity = self.t_rec.numel()
 
     def step(self) -> IterationRecord:
         """One bundling iteration (bundler.py:351-376) on the device."""
@@ -242,26 +283,30 @@ class BundleEngine:
             # resample (bundler.py:353-354): the counts/codes came out of the
             # previous iteration's fused advect pass; scan, size, then emit
             # fused with the splat (:355-356)
+            fused = self.wkind != "float"
+            tiles = None
+            if fused and self.tiles is not None:
+                self._k("hb_tiles_plan", ctypes.byref(self.tiles), ptr(self.t_total), s)
             self._k("hb_scan_counts", ptr(self.ecounts), E, ptr(self.starts_alt),
                     ptr(self.scan_ws), self.scan_ws.numel(), s)
             n_new = int(download(self.starts_alt[E:E + 1])[0]) if E else 0
             self._ensure_capacity(n_new)
-            fused = self.wkind != "float"
+            if fused and self.tiles is not None:
+                self._ensure_records(int(download(self.t_total)[0]))
+                tiles = ctypes.byref(self.tiles)
             self._k("hb_resample_emit", ptr(self.pts), ptr(self.starts), E, self.n_pts,
                     ptr(self.pos), ptr(self.starts_alt), ptr(self.alt), ptr(self.groups),
                     ptr(self.wint), ptr(self.hist) if fused else None, nv, nu,
-                    ptr(self.status), s)
+                    ptr(self.status), tiles, s)
+            if tiles is not None:
+                self._k("hb_tiles_flush", tiles, ptr(self.hist), nv, nu, s)
             self.pts, self.alt = self.alt, self.pts
             self.starts, self.starts_alt = self.starts_alt, self.starts
             self.n_pts = n_new
             if not fused:
-                name, w = self._splat_args()
-                self._k(name, ptr(self.pts), ptr(self.starts), E, self.n_pts,
-                        ptr(self.groups), w, ptr(self.hist), B, nv, nu, ptr(self.status), s)
+                self._splat(s)
         else:
-            name, w = self._splat_args()
-            self._k(name, ptr(self.pts), ptr(self.starts), E, self.n_pts, ptr(self.groups),
-                    w, ptr(self.hist), B, nv, nu, ptr(self.status), s)
+            self._splat(s)
         if self.reduce_hist is not None:
             self.reduce_hist(self.hist)
         is_int = self.wkind != "float"

@@ -43,7 +43,7 @@ def rasterize_segment(p0, p1) -> np.ndarray:
     hist = torch.zeros((1, nv, nu), dtype=torch.int32, device=dev)
     status = torch.zeros(1, dtype=torch.int32, device=dev)
     N.call("hb_splat", ptr(pts), ptr(starts), 1, 2, ptr(grp), None, ptr(hist), 1, nv, nu,
-           ptr(status), stream_ptr())
+           ptr(status), None, stream_ptr())
     v, u = np.nonzero(hist[0].cpu().numpy())
     cells = np.stack([u + lo[0], v + lo[1]], axis=1).astype(np.int64)
     d = c[1] - c[0]
@@ -103,7 +103,7 @@ def accumulate_edges(sampled: Sequence[SampledEdge], graph: Graph, matrix: np.nd
         hist = torch.zeros((nb, nv, nu), dtype=torch.int32, device=dev)
         w = None if plan.kind == "unit" else torch.from_numpy(plan.int_w).to(dev)
         N.call("hb_splat", ptr(dpts), ptr(dst), E, n, ptr(grp), ptr(w), ptr(hist), nb, nv, nu,
-               ptr(status), s)
+               ptr(status), None, s)
         N.call("hb_mix_layers", ptr(hist), None, ptr(mat), nb, nv, nu, ptr(out), s)
     return DensityField(transform, out.cpu().numpy())
 

@@ -75,7 +75,7 @@ def test_splat_counts_match_reference_kat():
     hist = torch.zeros((3, nv, nu), dtype=torch.int32, device="cuda")
     status = torch.zeros(1, dtype=torch.int32, device="cuda")
     N.call("hb_splat", ptr(dev(pts)), ptr(dev(starts)), len(starts) - 1, len(pts),
-           ptr(dev(groups.astype(np.int32))), None, ptr(hist), 3, nv, nu, ptr(status),
+           ptr(dev(groups.astype(np.int32))), None, ptr(hist), 3, nv, nu, ptr(status), None,
            stream_ptr())
     sync()
     assert np.array_equal(hist.cpu().numpy().astype(np.float32), k["raw"])
@@ -93,7 +93,7 @@ def test_mix_layers_repulsive_matrix_kat():
     out = torch.empty((3, nv, nu), dtype=torch.float32, device="cuda")
     s = stream_ptr()
     N.call("hb_splat", ptr(dev(pts)), ptr(dev(starts)), len(starts) - 1, len(pts),
-           ptr(dev(groups.astype(np.int32))), None, ptr(hist), 3, nv, nu, ptr(status), s)
+           ptr(dev(groups.astype(np.int32))), None, ptr(hist), 3, nv, nu, ptr(status), None, s)
     N.call("hb_mix_layers", ptr(hist), None, ptr(dev(k["mat"])), 3, nv, nu, ptr(out), s)
     sync()
     np.testing.assert_allclose(out.cpu().numpy(), k["raw_rep"], rtol=0, atol=1e-6)
@@ -122,7 +122,7 @@ def test_resample_matches_reference_kat(delta, key):
     m = int(ns[-1].item())
     out = torch.empty((m, 2), dtype=torch.float64, device="cuda")
     N.call("hb_resample_emit", ptr(dp), ptr(ds), E, n, ptr(pos), ptr(ns), ptr(out), None, None,
-           None, 1, 1, None, s)
+           None, 1, 1, None, None, s)
     sync()
     assert np.array_equal(ns.cpu().numpy(), k[key + "_starts"])
     assert np.array_equal(out.cpu().numpy(), k[key])
@@ -225,7 +225,7 @@ def test_resample_emit_splat_random_vs_oracle(seed):
     m = int(ns[-1].item())
     out = torch.empty((m, 2), dtype=torch.float64, device="cuda")
     N.call("hb_resample_emit", ptr(dp), ptr(ds), E, n, ptr(pos), ptr(ns), ptr(out),
-           ptr(dev(groups.astype(np.int32))), None, ptr(hist), nv, nu, ptr(status), s)
+           ptr(dev(groups.astype(np.int32))), None, ptr(hist), nv, nu, ptr(status), None, s)
     sync()
     assert np.array_equal(ns.cpu().numpy(), ref_starts)
     assert np.array_equal(out.cpu().numpy(), ref_pts)

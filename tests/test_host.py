@@ -119,7 +119,21 @@ def test_library_loads_and_exports_every_symbol():
 def test_library_rejects_bad_arguments_without_gpu():
     from paper_1504_02687_b200 import _native
     lib = _native.load_library()
-    assert lib.hb_splat(None, None, 5, 10, None, None, None, 1, 4, 4, None, None) == -1
+    assert lib.hb_splat(None, None, 5, 10, None, None, None, 1, 4, 4, None, None, None) == -1
     assert b"bad arguments" in lib.hb_last_error()
     assert lib.hb_advect_laplacian(None, None, None, 1, 1, None, None, 1, 8, 8, 1.0, 1e-8, 0.25,
                                    0, 0.5, 1, 1.0, None, None, None, None, None) == -1
+
+
+def test_tiles_geometry():
+    import ctypes
+    from paper_1504_02687_b200 import _native
+    lib = _native.load_library()
+    t = _native.HbTiles()
+    assert lib.hb_tiles_geometry(1, 1024, 1024, 1.5 * 4.64 + 2, ctypes.byref(t)) == 0
+    assert t.tile == 64 and t.halo == 10 and t.ntx == t.nty == 16 and t.ntiles == 256
+    # window (tile + 2 halo)^2 int32 must fit the 96 KB shared-memory budget
+    assert lib.hb_tiles_geometry(4, 2048, 2048, 1.5 * 33.0 + 2, ctypes.byref(t)) == 0
+    assert (t.tile + 2 * t.halo) ** 2 * 4 <= 96 * 1024 and t.ntiles == 4 * t.ntx * t.nty
+    assert lib.hb_tiles_geometry(1, 70000, 10, 3.0, ctypes.byref(t)) == -1
+    assert lib.hb_tiles_geometry(1, 100, 100, 200.0, ctypes.byref(t)) == -1

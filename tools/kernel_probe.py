@@ -66,7 +66,7 @@ def main():
             eng.hist.zero_()
         N.call("hb_resample_emit", ptr(eng.pts), ptr(eng.starts), E, n_old, ptr(eng.pos),
                ptr(eng.starts_alt), ptr(eng.alt), ptr(eng.groups), ptr(eng.wint),
-               ptr(eng.hist) if splat else None, nv, nu, ptr(eng.status), s)
+               ptr(eng.hist) if splat else None, nv, nu, ptr(eng.status), None, s)
 
     out["emit_splat_ms"] = timed(lambda: emit(True))
     out["emit_only_ms"] = timed(lambda: emit(False))
@@ -75,9 +75,44 @@ def main():
     def splat():
         eng.hist.zero_()
         N.call("hb_splat", ptr(eng.alt), ptr(eng.starts_alt), E, n_new, ptr(eng.groups),
-               ptr(eng.wint), ptr(eng.hist), Bn, nv, nu, ptr(eng.status), s)
+               ptr(eng.wint), ptr(eng.hist), Bn, nv, nu, ptr(eng.status), None, s)
 
     out["splat_only_ms"] = timed(splat)
+    if eng.tiles is not None:
+        import ctypes
+        tl = ctypes.byref(eng.tiles)
+        # demand of the real pass that produced this state's plan
+        N.call("hb_tiles_plan", tl, ptr(eng.t_total), s)
+        fill_prev = None
+
+        def emit_binned():
+            eng.hist.zero_()
+            eng.t_fill.zero_()
+            N.call("hb_resample_emit", ptr(eng.pts), ptr(eng.starts), E, n_old, ptr(eng.pos),
+                   ptr(eng.starts_alt), ptr(eng.alt), ptr(eng.groups), ptr(eng.wint),
+                   ptr(eng.hist), nv, nu, ptr(eng.status), tl, s)
+
+        eng._ensure_records(int(eng.t_total.item()))
+        tl = ctypes.byref(eng.tiles)
+        out["tiles"] = {"tile": eng.tiles.tile, "halo": eng.tiles.halo,
+                        "ntiles": eng.tiles.ntiles, "records_capacity": int(eng.t_total.item())}
+        out["emit_binned_ms"] = timed(emit_binned)
+        fill = eng.t_fill.clone()
+        cap = eng.t_cap.clone()
+        out["tiles"]["demand"] = int(fill.sum().item())
+        out["tiles"]["overflow"] = int((fill - cap).clamp_min(0).sum().item())
+        out["tiles"]["max_tile_demand"] = int(fill.max().item())
+        out["flush_ms"] = timed(lambda: N.call("hb_tiles_flush", tl, ptr(eng.hist), nv, nu, s))
+        # plan sized exactly from this pass's own demand: no overflow
+        N.call("hb_tiles_plan", tl, ptr(eng.t_total), s)
+        eng._ensure_records(int(eng.t_total.item()))
+        tl = ctypes.byref(eng.tiles)
+        out["emit_binned_planned_ms"] = timed(emit_binned)
+        fill = eng.t_fill.clone()
+        out["tiles"]["overflow_planned"] = int((fill - eng.t_cap).clamp_min(0).sum().item())
+        out["flush_planned_ms"] = timed(
+            lambda: N.call("hb_tiles_flush", tl, ptr(eng.hist), nv, nu, s))
+        del fill_prev
     hist = eng.hist.clone()
     out["hist_max"] = int(hist.max().item())
     out["hist_nonzero_frac"] = float((hist > 0).float().mean().item())

@@ -62,6 +62,14 @@ typedef struct hb_tiles {
     int32_t *work;       /* (ntiles+2) scratch: flush chunk prefix + counter */
     uint64_t *rec;       /* off[ntiles] records; NULL = census only */
     int64_t rec_capacity;
+    /* Segment-key mode (mode == 1): segments of bundled edges are mostly
+     * identical at the cell level, so instead of records every segment with
+     * k0 == 1 and cell delta within +-halo adds its weight to one counter
+     * keyed by (group, delta, start cell); hb_segtab_expand then rasterises
+     * each non-zero key once with its multiplicity.  tab holds
+     * nbins*(2*halo+1)^2*nv*nu uint32 counters, all zero between passes. */
+    int mode;            /* 0 = tile records, 1 = segment-key table */
+    uint32_t *tab;
 } hb_tiles;
 
 HB_API int hb_abi_version(void);
@@ -105,6 +113,15 @@ HB_API int hb_tiles_plan(const hb_tiles *t, int64_t *total, void *stream);
 /* Rasterise every binned record into counts (int32 (B,V,U)). */
 HB_API int hb_tiles_flush(const hb_tiles *t, int32_t *counts, int nv, int nu,
                           void *stream);
+
+/* Segment-key geometry: fills halo/nbins and mode = 1; returns the number of
+ * uint32 counters the caller must allocate (zeroed) in *entries. */
+HB_API int hb_segtab_geometry(int nbins, int nv, int nu, double max_seg_cells,
+                              hb_tiles *t, int64_t *entries);
+
+/* Rasterise every non-zero segment key into counts and reset it to zero. */
+HB_API int hb_segtab_expand(const hb_tiles *t, int32_t *counts, int nv, int nu,
+                            void *stream);
 
 /* _kernels.accumulate (_kernels.py:46-77) via raster._accumulate_packed
  * (raster.py:70-94), per-group form: counts[group[e]] += weight[e] on every

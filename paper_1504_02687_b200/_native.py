@@ -68,6 +68,8 @@ SIGNATURES = {
     "hb_tiles_geometry": (_I, [_I, _I, _I, _D, _P]),
     "hb_tiles_plan": (_I, [_P, _P, _P]),
     "hb_tiles_flush": (_I, [_P, _P, _I, _I, _P]),
+    "hb_segtab_geometry": (_I, [_I, _I, _I, _D, _P, _P]),
+    "hb_segtab_expand": (_I, [_P, _P, _I, _I, _P]),
     "hb_splat": (_I, [_P, _P, _I64, _I64, _P, _P, _P, _I, _I, _I, _P, _P, _P]),
     "hb_splat_f32": (_I, [_P, _P, _I64, _I64, _P, _P, _P, _I, _I, _I, _P, _P]),
     "hb_smooth_workspace_bytes": (_SZ, [_I, _I, _I]),
@@ -94,7 +96,8 @@ class HbTiles(ctypes.Structure):
                 ("nty", ctypes.c_int), ("nbins", ctypes.c_int), ("ntiles", ctypes.c_int),
                 ("off", ctypes.c_void_p), ("cap", ctypes.c_void_p), ("fill", ctypes.c_void_p),
                 ("work", ctypes.c_void_p), ("rec", ctypes.c_void_p),
-                ("rec_capacity", ctypes.c_int64)]
+                ("rec_capacity", ctypes.c_int64), ("mode", ctypes.c_int),
+                ("tab", ctypes.c_void_p)]
 
 
 _lib = None

@@ -278,6 +278,26 @@ __device__ __forceinline__ void bin_or_splat(bool has, double px0, double py0, d
     bool direct = has;
     int tile = -1;
     uint64_t rec = 0;
+    if (tl && tl->mode == 1) {  // segment-key table: one atomic per segment
+        if (has) {
+            const int x0 = cell_round(px0), y0 = cell_round(py0);
+            const int dx = cell_round(px1) - x0, dy = cell_round(py1) - y0;
+            const int H = tl->halo, iw = (int)w;
+            if (k0 == 1 && dx == 0 && dy == 0) {
+                direct = false;  // adds nothing (_kernels.py:67-71)
+            } else if (k0 == 1 && abs(dx) <= H && abs(dy) <= H && (T)iw == w && iw >= 1 &&
+                       (unsigned)x0 < (unsigned)nu && (unsigned)y0 < (unsigned)nv &&
+                       (unsigned)(x0 + dx) < (unsigned)nu && (unsigned)(y0 + dy) < (unsigned)nv) {
+                const int D = 2 * H + 1;
+                const int64_t dir = (int64_t)grp * D * D + (dy + H) * D + (dx + H);
+                atomicAdd(tl->tab + (dir * nv + y0) * nu + x0, (unsigned)iw);
+                direct = false;
+            }
+        }
+        if (direct)
+            dda_splat<T>(px0, py0, px1, py1, k0, w, hist + (int64_t)grp * plane, nv, nu, status);
+        return;
+    }
     if (has && tl) {
         const int x0 = cell_round(px0), y0 = cell_round(py0);
         const int dx = cell_round(px1) - x0, dy = cell_round(py1) - y0;

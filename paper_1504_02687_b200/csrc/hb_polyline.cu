@@ -131,7 +131,7 @@ __device__ __forceinline__ double2 interp_piece(double2 a, double2 x, int k, int
     return make_double2(dadd(a.x, dmul(t, dsub(x.x, a.x))), dadd(a.y, dmul(t, dsub(x.y, a.y))));
 }
 
-__global__ void __launch_bounds__(kStreamBlock)
+__global__ void __launch_bounds__(kStreamBlock, 3)
 emit_kernel(const double2 *__restrict__ pts, const int64_t *__restrict__ starts,
             int64_t n_edges, const int32_t *__restrict__ pos,
             const int64_t *__restrict__ new_starts, double2 *__restrict__ out,

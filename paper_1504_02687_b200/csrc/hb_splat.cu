@@ -211,3 +211,86 @@ int hb_tiles_flush(const hb_tiles *t, int32_t *counts, int nv, int nu, void *str
 }
 
 }  // extern "C"
+
+// ---------------------------------------------------------------------------
+// Segment-key table (mode 1).  tab[((g*D + dir)*nv + y0)*nu + x0] holds the
+// summed weight of every k0 == 1 segment of layer g that starts in cell
+// (x0, y0) with cell delta dir = (dy+H)*D + (dx+H).  The expansion reads the
+// table with 16-byte loads, rasterises each non-zero key once (weight x
+// path is exactly the sum of the individual paths: integer addition) and
+// resets it, so the table is zero again for the next pass.
+namespace hb {
+
+constexpr int kExpandBlock = 256;
+
+__global__ void __launch_bounds__(kExpandBlock)
+segtab_expand_kernel(const __grid_constant__ hb_tiles t, int32_t *__restrict__ counts, int nv,
+                     int nu, int64_t n4) {
+    const int H = t.halo, D = 2 * H + 1;
+    const int64_t plane = (int64_t)nv * nu;
+    uint4 *tab4 = reinterpret_cast<uint4 *>(t.tab);
+    for (int64_t q = (int64_t)blockIdx.x * kExpandBlock + threadIdx.x; q < n4;
+         q += (int64_t)gridDim.x * kExpandBlock) {
+        const uint4 v4 = tab4[q];
+        if ((v4.x | v4.y | v4.z | v4.w) == 0u) continue;
+        tab4[q] = make_uint4(0u, 0u, 0u, 0u);
+        const unsigned vals[4] = {v4.x, v4.y, v4.z, v4.w};
+#pragma unroll
+        for (int c = 0; c < 4; ++c) {
+            const unsigned val = vals[c];
+            if (!val) continue;
+            const int64_t idx = q * 4 + c;
+            const int64_t key = idx / plane;  // g*D*D + dir
+            const int64_t cell = idx - key * plane;
+            const int g = (int)(key / ((int64_t)D * D));
+            const int dir = (int)(key - (int64_t)g * D * D);
+            const int dy = dir / D - H, dx = dir % D - H;
+            const int y0 = (int)(cell / nu), x0 = (int)(cell - (int64_t)y0 * nu);
+            int32_t *layer = counts + (int64_t)g * plane;
+            dda_walk(x0, y0, x0 + dx, y0 + dy, 1, [&](int u, int v) {
+                atomicAdd(layer + (int64_t)v * nu + u, (int)val);
+            });
+        }
+    }
+}
+
+}  // namespace hb
+
+extern "C" {
+
+int hb_segtab_geometry(int nbins, int nv, int nu, double max_seg_cells, hb_tiles *t,
+                       int64_t *entries) {
+    if (!t || !entries || nbins < 1 || nv < 1 || nu < 1 || !(max_seg_cells >= 0))
+        return set_error(HB_EINVAL, "hb_segtab_geometry: bad arguments");
+    if (max_seg_cells > 60.0)
+        return set_error(HB_EINVAL, "hb_segtab_geometry: segments too long for a key table");
+    const int H = (int)ceil(max_seg_cells) + 1;
+    const int64_t D = 2 * H + 1;
+    t->mode = 1;
+    t->halo = H;
+    t->nbins = nbins;
+    *entries = (int64_t)nbins * D * D * nv * nu;
+    // whole uint4 loads in the expansion
+    *entries = (*entries + 3) / 4 * 4;
+    return HB_OK;
+}
+
+int hb_segtab_expand(const hb_tiles *t, int32_t *counts, int nv, int nu, void *stream) {
+    if (!t || t->mode != 1 || !t->tab || !counts || nv < 1 || nu < 1)
+        return set_error(HB_EINVAL, "hb_segtab_expand: bad arguments");
+    const int64_t D = 2 * t->halo + 1;
+    const int64_t n = (int64_t)t->nbins * D * D * nv * nu;
+    const int64_t n4 = (n + 3) / 4;
+    int per_sm = 0;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, segtab_expand_kernel,
+                                                      kExpandBlock, 0) != cudaSuccess ||
+        per_sm < 1)
+        per_sm = 1;
+    const int64_t want = (n4 + kExpandBlock - 1) / kExpandBlock;
+    const int64_t cap = (int64_t)device_sm_count() * per_sm * 4;
+    segtab_expand_kernel<<<(unsigned)(want < cap ? want : cap), kExpandBlock, 0,
+                           as_stream(stream)>>>(*t, counts, nv, nu, n4);
+    return check_launch("hb_segtab_expand");
+}
+
+}  // extern "C"

@@ -173,13 +173,25 @@ class BundleEngine:
         self.smooth_ws = torch.empty(sws, dtype=torch.uint8, device=dev)
         scw = N.lib().hb_scan_workspace_bytes(max(E, 1))
         self.scan_ws = torch.empty(scw, dtype=torch.uint8, device=dev)
-        # tile-binned splatting (hb_splat.cu); segments are at most 1.5*delta
-        # long after resampling (and delta before), + rounding slack
+        # Aggregated splatting (hb_splat.cu).  Resampled segments are at most
+        # 1.5*delta long (delta before the first resample), so their cell
+        # delta is at most floor(1.5*delta) + 1 per axis; longer ones simply
+        # take the direct path.  Preferred: the segment-key table (one atomic
+        # per segment, bundled duplicates collapse); else tile records.
         self.tiles = None
+        self.tile_mode = -1
         if self.wkind != "float":
             geo = N.HbTiles()
-            if N.lib().hb_tiles_geometry(B, self.nv, self.nu, 1.5 * self.delta + 2.0,
-                                         ctypes.byref(geo)) == 0:
+            ent = ctypes.c_int64(0)
+            budget = min(8 << 30, torch.cuda.mem_get_info(dev)[0] // 8)
+            if (N.lib().hb_segtab_geometry(B, self.nv, self.nu, 1.5 * self.delta,
+                                           ctypes.byref(geo), ctypes.byref(ent)) == 0
+                    and ent.value * 4 <= budget):
+                self.t_tab = torch.zeros(ent.value, dtype=torch.int32, device=dev)
+                geo.tab = self.t_tab.data_ptr()
+                self.tiles, self.tile_mode = geo, 1
+            elif N.lib().hb_tiles_geometry(B, self.nv, self.nu, 1.5 * self.delta + 2.0,
+                                           ctypes.byref(geo)) == 0:
                 nt = geo.ntiles
                 self.t_off = torch.zeros(nt + 1, dtype=torch.int64, device=dev)
                 self.t_cap = torch.zeros(nt, dtype=torch.int32, device=dev)
@@ -191,7 +203,8 @@ class BundleEngine:
                 geo.off, geo.cap = self.t_off.data_ptr(), self.t_cap.data_ptr()
                 geo.fill, geo.work = self.t_fill.data_ptr(), self.t_work.data_ptr()
                 geo.rec, geo.rec_capacity = self.t_rec.data_ptr(), self.t_rec.numel()
-                self.tiles = geo
+                geo.mode = 0
+                self.tiles, self.tile_mode = geo, 0
                 self.tiles_census = N.HbTiles.from_buffer_copy(geo)
                 self.tiles_census.rec = None
         self.lap_passes = int(cfg.laplacian_passes)
@@ -252,12 +265,16 @@ class BundleEngine:
                     ptr(self.groups), ptr(self.wf32), ptr(self.hist), B, nv, nu,
                     ptr(self.status), s)
             return
-        census = None
-        if self.tiles is not None:
+        sink = None
+        if self.tile_mode == 1:
+            sink = ctypes.byref(self.tiles)
+        elif self.tile_mode == 0:
             self.t_fill.zero_()
-            census = ctypes.byref(self.tiles_census)
+            sink = ctypes.byref(self.tiles_census)
         self._k("hb_splat", ptr(self.pts), ptr(self.starts), E, self.n_pts, ptr(self.groups),
-                ptr(self.wint), ptr(self.hist), B, nv, nu, ptr(self.status), census, s)
+                ptr(self.wint), ptr(self.hist), B, nv, nu, ptr(self.status), sink, s)
+        if self.tile_mode == 1:
+            self._k("hb_segtab_expand", sink, ptr(self.hist), nv, nu, s)
 
     def _ensure_records(self, n: int) -> None:
         if n <= self.t_rec.numel():
@@ -285,21 +302,24 @@ class BundleEngine:
             # fused with the splat (:355-356)
             fused = self.wkind != "float"
             tiles = None
-            if fused and self.tiles is not None:
+            if fused and self.tile_mode == 0:
                 self._k("hb_tiles_plan", ctypes.byref(self.tiles), ptr(self.t_total), s)
             self._k("hb_scan_counts", ptr(self.ecounts), E, ptr(self.starts_alt),
                     ptr(self.scan_ws), self.scan_ws.numel(), s)
             n_new = int(download(self.starts_alt[E:E + 1])[0]) if E else 0
             self._ensure_capacity(n_new)
-            if fused and self.tiles is not None:
+            if fused and self.tile_mode == 0:
                 self._ensure_records(int(download(self.t_total)[0]))
+            if fused and self.tiles is not None:
                 tiles = ctypes.byref(self.tiles)
             self._k("hb_resample_emit", ptr(self.pts), ptr(self.starts), E, self.n_pts,
                     ptr(self.pos), ptr(self.starts_alt), ptr(self.alt), ptr(self.groups),
                     ptr(self.wint), ptr(self.hist) if fused else None, nv, nu,
                     ptr(self.status), tiles, s)
-            if tiles is not None:
+            if self.tile_mode == 0 and tiles is not None:
                 self._k("hb_tiles_flush", tiles, ptr(self.hist), nv, nu, s)
+            elif self.tile_mode == 1 and tiles is not None:
+                self._k("hb_segtab_expand", tiles, ptr(self.hist), nv, nu, s)
             self.pts, self.alt = self.alt, self.pts
             self.starts, self.starts_alt = self.starts_alt, self.starts
             self.n_pts = n_new

@@ -112,6 +112,25 @@ def main():
         out["tiles"]["overflow_planned"] = int((fill - eng.t_cap).clamp_min(0).sum().item())
         out["flush_planned_ms"] = timed(
             lambda: N.call("hb_tiles_flush", tl, ptr(eng.hist), nv, nu, s))
+        # record multiplicity: identical (start cell, delta, k0, w) rasterise identically
+        off = eng.t_off.cpu().numpy()
+        fillc = torch.minimum(eng.t_fill, eng.t_cap).cpu().numpy()
+        hot = int(fillc.argmax())
+        recs = eng.t_rec[int(off[hot]):int(off[hot]) + int(fillc[hot])]
+        out["tiles"]["hot_tile_records"] = int(recs.numel())
+        out["tiles"]["hot_tile_unique"] = int(torch.unique(recs).numel())
+        chunk = recs[: 16384]
+        out["tiles"]["hot_chunk_unique_of_16384"] = int(torch.unique(chunk).numel())
+        allr = torch.cat([eng.t_rec[int(off[t]):int(off[t]) + int(fillc[t])]
+                          for t in range(len(fillc)) if fillc[t] > 0])
+        out["tiles"]["all_unique"] = int(torch.unique(allr).numel())
+        # per 16384-record chunk uniqueness over all tiles (what a chunk-local dedupe sees)
+        tot_u = 0
+        for t in range(len(fillc)):
+            r = eng.t_rec[int(off[t]):int(off[t]) + int(fillc[t])]
+            for c0 in range(0, r.numel(), 16384):
+                tot_u += int(torch.unique(r[c0:c0 + 16384]).numel())
+        out["tiles"]["chunk_local_unique"] = tot_u
         del fill_prev
     hist = eng.hist.clone()
     out["hist_max"] = int(hist.max().item())

@@ -31,18 +31,28 @@ struct Adv {
     double disp;
 };
 
-// _kernels.py:163-199 for one interior point
+// _kernels.py:163-199 for one interior point.  (A warp-cooperative variant
+// that tests the remaining candidates of pending points on idle lanes was
+// measured slower on B200: the shuffles cost more than the divergence.)
 __device__ __forceinline__ Adv advect_one(const float *__restrict__ rho, int nv, int nu,
                                           double xhi, double yhi, double2 p, double h,
                                           double eps, double min_step, int fixed) {
     Adv r{p, false, 0.0};
     const double x = p.x, y = p.y;
     const double xlo = 1.0, ylo = 1.0;  // INTERIOR_MARGIN (_kernels.py:19)
-    double gx, gy, r0;
-    gradient_value_ref(rho, nv, nu, x, y, gx, gy, r0);
-    double gn = hypot_ref(gx, gy);
-    if (gn < eps) gn = eps;
-    const double dx = gx / gn, dy = gy / gn;
+    // G = 2*gradient exactly, so |G| = 2*gn and G/|G| == g/gn bit for bit;
+    // only the eps clamp (gn < eps <=> |G| < 2*eps) needs the scaled values
+    double Gx, Gy, r0;
+    gradient2_value_ref(rho, nv, nu, x, y, Gx, Gy, r0);
+    const double Gn = hypot_ref(Gx, Gy);
+    double dx, dy;
+    if (Gn < 2.0 * eps) {
+        dx = dmul(0.5, Gx) / eps;
+        dy = dmul(0.5, Gy) / eps;
+    } else {
+        dx = Gx / Gn;
+        dy = Gy / Gn;
+    }
     double m = h;
     while (fixed || m >= min_step) {
         const double nx = fmin_ref(fmax_ref(dadd(x, dmul(m, dx)), xlo), xhi);
@@ -158,10 +168,11 @@ polyline_pass_kernel(const PolylinePass p) {
                     }
                     const int b = __ffs(m) - 1;
                     if (act && lane < b) { kept = true; gk = geff; }
-                    if (b > start) {
-                        ka.x = __shfl_sync(full, f.x, b - 1);
-                        ka.y = __shfl_sync(full, f.y, b - 1);
-                    }
+                    // b and start are warp-uniform; shuffle unconditionally so
+                    // the compiler needs no collective fix-up code
+                    const double kx = __shfl_sync(full, f.x, b > 0 ? b - 1 : 0);
+                    const double ky = __shfl_sync(full, f.y, b > 0 ? b - 1 : 0);
+                    if (b > start) { ka.x = kx; ka.y = ky; }
                     start = b + 1;
                 }
                 int pieces = 0;
@@ -180,11 +191,10 @@ polyline_pass_kernel(const PolylinePass p) {
                 }
                 if (part) p.pos[s + j] = kept ? off + incl : -1;
                 const unsigned km = __ballot_sync(full, kept);
-                if (km) {
-                    const int lk = 31 - __clz(km);
-                    ka.x = __shfl_sync(full, f.x, lk);
-                    ka.y = __shfl_sync(full, f.y, lk);
-                }
+                const int lk = km ? 31 - __clz(km) : 0;
+                const double kx2 = __shfl_sync(full, f.x, lk);
+                const double ky2 = __shfl_sync(full, f.y, lk);
+                if (km) { ka.x = kx2; ka.y = ky2; }
                 off += __shfl_sync(full, incl, 31);
                 prevf.x = __shfl_sync(full, f.x, 31);
                 prevf.y = __shfl_sync(full, f.y, 31);

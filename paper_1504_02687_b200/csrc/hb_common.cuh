@@ -104,23 +104,29 @@ __device__ __forceinline__ double bilinear_ref(const float *__restrict__ rho, in
     return dadd(a, dmul(fy, dsub(b, a)));
 }
 
-// _kernels.py:101-114 _cell_gradient (general, clamped)
-__device__ __forceinline__ void cell_grad_ref(const float *__restrict__ rho, int nv, int nu,
-                                              int u, int v, double &gx, double &gy) {
+// _kernels.py:101-114 _cell_gradient (general, clamped), without its 0.5
+// factor (see gradient2_value_ref)
+__device__ __forceinline__ void cell_grad2_ref(const float *__restrict__ rho, int nv, int nu,
+                                               int u, int v, double &gx, double &gy) {
     u = clampi(u, 1, nu - 2);
     v = clampi(v, 1, nv - 2);
     const float *c = rho + v * nu + u;
-    gx = dmul(0.5, (double)__fsub_rn(ldf(c + 1), ldf(c - 1)));
-    gy = dmul(0.5, (double)__fsub_rn(ldf(c + nu), ldf(c - nu)));
+    gx = (double)__fsub_rn(ldf(c + 1), ldf(c - 1));
+    gy = (double)__fsub_rn(ldf(c + nu), ldf(c - nu));
 }
 
 // _kernels.py:117-141 gradient_xy and, from the same 4x4 stencil, the
 // bilinear value at (x, y) (both clamp u0/v0 to [0, dim-2] identically).
+// Returns G = 2 * gradient_xy EXACTLY: the reference's 0.5 * (rho[+1] -
+// rho[-1]) factors are power-of-two scalings, which commute with every IEEE
+// rounding in the interpolation (values stay far from over/underflow), so
+// they are applied once by the caller -- or never, where only the direction
+// G/|G| is used.
 // Interior fast path (u0 in [1, nu-3], v0 in [1, nv-3], i.e. no clamp can
 // fire): 12 loads off one base pointer.  Otherwise the general clamped path.
-__device__ __forceinline__ void gradient_value_ref(const float *__restrict__ rho, int nv, int nu,
-                                                   double x, double y, double &gx, double &gy,
-                                                   double &val) {
+__device__ __forceinline__ void gradient2_value_ref(const float *__restrict__ rho, int nv,
+                                                    int nu, double x, double y, double &Gx,
+                                                    double &Gy, double &val) {
     const int u0 = clampi(floor_i(x), 0, nu - 2);
     const int v0 = clampi(floor_i(y), 0, nv - 2);
     const double fx = dsub(x, (double)u0);
@@ -137,19 +143,19 @@ __device__ __forceinline__ void gradient_value_ref(const float *__restrict__ rho
         a10 = ldf(c + nu);
         a11 = ldf(c + nu + 1);
         const float t1 = ldf(c + 2 * nu), t2 = ldf(c + 2 * nu + 1);
-        g00x = dmul(0.5, (double)__fsub_rn(a01, r0));
-        g00y = dmul(0.5, (double)__fsub_rn(a10, m0));
-        g10x = dmul(0.5, (double)__fsub_rn(r3, a00));
-        g10y = dmul(0.5, (double)__fsub_rn(a11, m1));
-        g01x = dmul(0.5, (double)__fsub_rn(a11, s0));
-        g01y = dmul(0.5, (double)__fsub_rn(t1, a00));
-        g11x = dmul(0.5, (double)__fsub_rn(s3, a10));
-        g11y = dmul(0.5, (double)__fsub_rn(t2, a01));
+        g00x = (double)__fsub_rn(a01, r0);
+        g00y = (double)__fsub_rn(a10, m0);
+        g10x = (double)__fsub_rn(r3, a00);
+        g10y = (double)__fsub_rn(a11, m1);
+        g01x = (double)__fsub_rn(a11, s0);
+        g01y = (double)__fsub_rn(t1, a00);
+        g11x = (double)__fsub_rn(s3, a10);
+        g11y = (double)__fsub_rn(t2, a01);
     } else {
-        cell_grad_ref(rho, nv, nu, u0, v0, g00x, g00y);
-        cell_grad_ref(rho, nv, nu, u0 + 1, v0, g10x, g10y);
-        cell_grad_ref(rho, nv, nu, u0, v0 + 1, g01x, g01y);
-        cell_grad_ref(rho, nv, nu, u0 + 1, v0 + 1, g11x, g11y);
+        cell_grad2_ref(rho, nv, nu, u0, v0, g00x, g00y);
+        cell_grad2_ref(rho, nv, nu, u0 + 1, v0, g10x, g10y);
+        cell_grad2_ref(rho, nv, nu, u0, v0 + 1, g01x, g01y);
+        cell_grad2_ref(rho, nv, nu, u0 + 1, v0 + 1, g11x, g11y);
         const float *c = rho + v0 * nu + u0;
         a00 = ldf(c);
         a01 = ldf(c + 1);
@@ -160,17 +166,20 @@ __device__ __forceinline__ void gradient_value_ref(const float *__restrict__ rho
     const double bx = dadd(g01x, dmul(fx, dsub(g11x, g01x)));
     const double ay = dadd(g00y, dmul(fx, dsub(g10y, g00y)));
     const double by = dadd(g01y, dmul(fx, dsub(g11y, g01y)));
-    gx = dadd(ax, dmul(fy, dsub(bx, ax)));
-    gy = dadd(ay, dmul(fy, dsub(by, ay)));
+    Gx = dadd(ax, dmul(fy, dsub(bx, ax)));
+    Gy = dadd(ay, dmul(fy, dsub(by, ay)));
     const double a = lerp_f32diff(a00, a01, fx);
     const double b = lerp_f32diff(a10, a11, fx);
     val = dadd(a, dmul(fy, dsub(b, a)));
 }
 
+// gradient_xy itself (bundler.gradient_at)
 __device__ __forceinline__ void gradient_ref(const float *__restrict__ rho, int nv, int nu,
                                              double x, double y, double &gx, double &gy) {
-    double v;
-    gradient_value_ref(rho, nv, nu, x, y, gx, gy, v);
+    double v, Gx, Gy;
+    gradient2_value_ref(rho, nv, nu, x, y, Gx, Gy, v);
+    gx = dmul(0.5, Gx);
+    gy = dmul(0.5, Gy);
 }
 
 // ---- DDA rasterisation of one segment (_kernels.py:58-77) ------------------
@@ -288,6 +297,8 @@ __device__ __forceinline__ void bin_or_splat(bool has, double px0, double py0, d
             } else if (k0 == 1 && abs(dx) <= H && abs(dy) <= H && (T)iw == w && iw >= 1 &&
                        (unsigned)x0 < (unsigned)nu && (unsigned)y0 < (unsigned)nv &&
                        (unsigned)(x0 + dx) < (unsigned)nu && (unsigned)(y0 + dy) < (unsigned)nv) {
+                // delta-major key (a cell-major layout was measured slower: it
+                // packs a hot cell's atomics into a few L2 slices)
                 const int D = 2 * H + 1;
                 const int64_t dir = (int64_t)grp * D * D + (dy + H) * D + (dx + H);
                 atomicAdd(tl->tab + (dir * nv + y0) * nu + x0, (unsigned)iw);

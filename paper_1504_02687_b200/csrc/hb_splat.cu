@@ -213,7 +213,7 @@ int hb_tiles_flush(const hb_tiles *t, int32_t *counts, int nv, int nu, void *str
 }  // extern "C"
 
 // ---------------------------------------------------------------------------
-// Segment-key table (mode 1).  tab[((g*D + dir)*nv + y0)*nu + x0] holds the
+// Segment-key table (mode 1).  tab[((g*D*D + dir)*nv + y0)*nu + x0] holds the
 // summed weight of every k0 == 1 segment of layer g that starts in cell
 // (x0, y0) with cell delta dir = (dy+H)*D + (dx+H).  The expansion reads the
 // table with 16-byte loads, rasterises each non-zero key once (weight x

@@ -78,7 +78,26 @@ def main():
                ptr(eng.wint), ptr(eng.hist), Bn, nv, nu, ptr(eng.status), None, s)
 
     out["splat_only_ms"] = timed(splat)
-    if eng.tiles is not None:
+    if eng.tile_mode == 1:
+        import ctypes
+        tl = ctypes.byref(eng.tiles)
+
+        def emit_segtab():
+            eng.hist.zero_()
+            N.call("hb_resample_emit", ptr(eng.pts), ptr(eng.starts), E, n_old, ptr(eng.pos),
+                   ptr(eng.starts_alt), ptr(eng.alt), ptr(eng.groups), ptr(eng.wint),
+                   ptr(eng.hist), nv, nu, ptr(eng.status), tl, s)
+
+        def expand():
+            N.call("hb_segtab_expand", tl, ptr(eng.hist), nv, nu, s)
+
+        out["segtab"] = {"halo": eng.tiles.halo, "entries": int(eng.t_tab.numel())}
+        out["emit_segtab_ms"] = timed(lambda: (emit_segtab(), expand()), reps=1)
+        emit_segtab()
+        out["segtab"]["nonzero_keys"] = int((eng.t_tab != 0).sum().item())
+        out["expand_ms"] = timed(expand, reps=1)
+        out["expand_empty_ms"] = timed(expand)
+    if eng.tile_mode == 0:
         import ctypes
         tl = ctypes.byref(eng.tiles)
         # demand of the real pass that produced this state's plan

@@ -78,6 +78,23 @@ HB_API int hb_device_sm_count(void);
 /* Total kernels this library has launched in the process (evidence counter). */
 HB_API long long hb_launch_count(void);
 
+/* Per-edge preparation of _sample_packed (bundler.py:77-85) on the device:
+ * src/dst grid endpoints (p - origin) / cell of node_pos[sources[e]] and
+ * node_pos[targets[e]] (model.py:214-216), and the point counts
+ * max(ceil(|dst - src| / delta), 1) + 1 with numpy's norm
+ * sqrt(dx*dx + dy*dy).  Scan counts with hb_scan_counts for `starts`. */
+HB_API int hb_edge_prepare(const double *node_pos, const int64_t *sources,
+                           const int64_t *targets, int64_t n_edges, double origin_x,
+                           double origin_y, double cell, double delta, double *src,
+                           double *dst, int64_t *counts, void *stream);
+
+/* _materialize (bundler.py:152-163) with the endpoint pins gathered from the
+ * node positions on the device. */
+HB_API int hb_to_world_nodes(const double *pts, const int64_t *starts, int64_t n_edges,
+                             double origin_x, double origin_y, double cell,
+                             const double *node_pos, const int64_t *sources,
+                             const int64_t *targets, double *out, void *stream);
+
 /* _kernels.fill_samples (_kernels.py:22-43), called by _sample_packed
  * (bundler.py:77-89).  src/dst: (E,2) grid endpoints; starts from the host
  * count rule max(ceil(|d|/delta),1)+1; pts: (starts[E],2). */

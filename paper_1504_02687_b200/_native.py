@@ -62,6 +62,8 @@ SIGNATURES = {
     "hb_last_error": (ctypes.c_char_p, []),
     "hb_device_sm_count": (_I, []),
     "hb_launch_count": (ctypes.c_longlong, []),
+    "hb_edge_prepare": (_I, [_P, _P, _P, _I64, _D, _D, _D, _D, _P, _P, _P, _P]),
+    "hb_to_world_nodes": (_I, [_P, _P, _I64, _D, _D, _D, _P, _P, _P, _P, _P]),
     "hb_sample_fill": (_I, [_P, _P, _P, _I64, _P, _P]),
     "hb_offset": (_I, [_P, _P, _I64, _P, _P]),
     "hb_to_world": (_I, [_P, _P, _I64, _D, _D, _D, _P, _P, _P, _P]),

@@ -24,7 +24,8 @@ import torch
 
 from . import _native as N
 from . import dist as D
-from .engine import MIN_STEP, BundleEngine, download, ptr, stream_ptr, weight_plan
+from .engine import (MIN_STEP, BundleEngine, download, download_pinned, ptr, stream_ptr,
+                     upload, weight_plan)
 from .model import (BundleConfig, DensityField, Graph, GridTransform, SampledEdge,
                     interaction_matrix, make_transform)
 
@@ -134,10 +135,37 @@ def prepare_engine(graph: Graph, config: BundleConfig | None = None, *, bins=Non
 
 def _setup(graph, cfg, bins_arr, matrix, fixed_step, group, capacity_factor):
     transform = make_transform(graph.positions, cfg.grid_size, cfg.padding_cells)
+    rank, world = D.rank_world(group)
+    reduce_hist = (lambda h: D.all_reduce_sum(h, group)) if world > 1 else None
+    common = dict(fixed_step=fixed_step, reduce_hist=reduce_hist,
+                  capacity_factor=capacity_factor)
+    if world == 1 and cfg.directed_offset_fraction == 0:
+        # per-edge preparation on the device: the host uploads node positions
+        # and endpoint indices once, the kernel computes the grid endpoints and
+        # the reference's point counts, CUB scans them into `starts`
+        dev = torch.device("cuda")
+        node_pos = upload(graph.positions, dev)
+        srcs = upload(graph.sources, dev)
+        tgts = upload(graph.targets, dev)
+        E = graph.n_edges
+        src = torch.empty((E, 2), dtype=torch.float64, device=dev)
+        dst = torch.empty((E, 2), dtype=torch.float64, device=dev)
+        counts = torch.empty(max(E, 1), dtype=torch.int64, device=dev)
+        starts = torch.empty(E + 1, dtype=torch.int64, device=dev)
+        ws = torch.empty(int(N.lib().hb_scan_workspace_bytes(max(E, 1))), dtype=torch.uint8,
+                         device=dev)
+        s = stream_ptr()
+        N.call("hb_edge_prepare", ptr(node_pos), ptr(srcs), ptr(tgts), E,
+               float(transform.origin[0]), float(transform.origin[1]),
+               float(transform.cell_size), float(cfg.delta), ptr(src), ptr(dst), ptr(counts), s)
+        N.call("hb_scan_counts", ptr(counts), E, ptr(starts), ptr(ws), ws.numel(), s)
+        eng = BundleEngine(src, dst, bins_arr, weight_plan(graph.weights), matrix,
+                           transform.shape, cfg, starts=starts, **common)
+        eng.node_arrays = (node_pos, srcs, tgts)
+        return eng, transform, 0, E
     pos = graph.positions
     src_all = transform.world_to_grid(pos[graph.sources])
     dst_all = transform.world_to_grid(pos[graph.targets])
-    rank, world = D.rank_world(group)
     lo, hi = 0, graph.n_edges
     if world > 1:
         from .engine import sample_counts
@@ -149,11 +177,9 @@ def _setup(graph, cfg, bins_arr, matrix, fixed_step, group, capacity_factor):
     if cfg.directed_offset_fraction > 0:
         od = _offset_vectors(src, dst, cfg.directed_offset_fraction
                              * max(transform.width, transform.height))
-    reduce_hist = (lambda h: D.all_reduce_sum(h, group)) if world > 1 else None
     eng = BundleEngine(src, dst, bins_arr[lo:hi], weight_plan(graph.weights[lo:hi]),
-                       matrix, transform.shape, cfg, fixed_step=fixed_step,
-                       offset_disp=od, reduce_hist=reduce_hist,
-                       capacity_factor=capacity_factor)
+                       matrix, transform.shape, cfg, offset_disp=od, **common)
+    eng.node_arrays = None
     return eng, transform, lo, hi
 
 
@@ -205,12 +231,15 @@ def bundle(graph: Graph, config: BundleConfig | None = None, *,
     cfg, bins_arr, matrix = _resolve(graph, config, bins, matrix)
     run = _run_engine(graph, cfg, bins_arr, matrix, _fixed_step, on_iteration, group)
     eng, tr = run.engine, run.transform
-    pos = graph.positions
-    src_w = pos[graph.sources[run.edge_lo:run.edge_hi]]
-    dst_w = pos[graph.targets[run.edge_lo:run.edge_hi]]
-    world_dev = eng.world_points(tr.origin, tr.cell_size, src_w, dst_w)
+    if eng.node_arrays is not None:
+        world_dev = eng.world_points_nodes(tr.origin, tr.cell_size, *eng.node_arrays)
+    else:
+        pos = graph.positions
+        src_w = pos[graph.sources[run.edge_lo:run.edge_hi]]
+        dst_w = pos[graph.targets[run.edge_lo:run.edge_hi]]
+        world_dev = eng.world_points(tr.origin, tr.cell_size, src_w, dst_w)
     if D.rank_world(group)[1] == 1:
-        world, starts = download(world_dev), download(eng.starts)
+        world, starts = download_pinned(world_dev), download(eng.starts)
     else:
         world, starts = D.gather_polylines(world_dev, eng.starts, group)
     field = DensityField(tr, download(eng.field))

@@ -77,6 +77,52 @@ __global__ void to_world_kernel(const double2 *__restrict__ pts,
     }
 }
 
+// bundler.py:77-85 per edge: grid endpoints (p - origin) / cell and the
+// point count max(ceil(|d| / delta), 1) + 1, |d| = sqrt(dx*dx + dy*dy) as
+// np.linalg.norm computes it for a 2-vector.
+__global__ void edge_prepare_kernel(const double2 *__restrict__ node_pos,
+                                    const int64_t *__restrict__ sources,
+                                    const int64_t *__restrict__ targets, int64_t n_edges,
+                                    double ox, double oy, double cell, double delta,
+                                    double2 *__restrict__ src, double2 *__restrict__ dst,
+                                    int64_t *__restrict__ counts) {
+    const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (e >= n_edges) return;
+    const double2 a = node_pos[sources[e]], b = node_pos[targets[e]];
+    const double2 sa = make_double2(dsub(a.x, ox) / cell, dsub(a.y, oy) / cell);
+    const double2 sb = make_double2(dsub(b.x, ox) / cell, dsub(b.y, oy) / cell);
+    src[e] = sa;
+    dst[e] = sb;
+    const double seg = hypot_ref(dsub(sb.x, sa.x), dsub(sb.y, sa.y));
+    const double c = ceil(seg / delta);
+    counts[e] = (c < 1.0 ? (int64_t)1 : (int64_t)c) + 1;
+}
+
+__global__ void to_world_nodes_kernel(const double2 *__restrict__ pts,
+                                      const int64_t *__restrict__ starts, int64_t n_edges,
+                                      double ox, double oy, double cell,
+                                      const double2 *__restrict__ node_pos,
+                                      const int64_t *__restrict__ sources,
+                                      const int64_t *__restrict__ targets,
+                                      double2 *__restrict__ out) {
+    const int64_t e = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) / kWarp;
+    const int lane = threadIdx.x & 31;
+    if (e >= n_edges) return;
+    const int64_t s = starts[e], t = starts[e + 1] - 1;
+    for (int64_t j = s + lane; j <= t; j += kWarp) {
+        double2 w;
+        if (j == s) {
+            w = node_pos[sources[e]];
+        } else if (j == t) {
+            w = node_pos[targets[e]];
+        } else {
+            const double2 p = pts[j];
+            w = make_double2(dadd(dmul(p.x, cell), ox), dadd(dmul(p.y, cell), oy));
+        }
+        out[j] = w;
+    }
+}
+
 // ---------------------------------------------------------------------------
 // accumulate (_kernels.py:46-77), warp per edge: lane j rasterises segment
 // (j-1, j); its start point comes from the lane below (or the carry).
@@ -278,6 +324,35 @@ int hb_to_world(const double *pts, const int64_t *starts, int64_t n_edges, doubl
         reinterpret_cast<const double2 *>(src_world), reinterpret_cast<const double2 *>(dst_world),
         reinterpret_cast<double2 *>(out));
     return check_launch("hb_to_world");
+}
+
+int hb_edge_prepare(const double *node_pos, const int64_t *sources, const int64_t *targets,
+                    int64_t n_edges, double origin_x, double origin_y, double cell, double delta,
+                    double *src, double *dst, int64_t *counts, void *stream) {
+    if (n_edges < 0 || !(cell > 0) || !(delta > 0) ||
+        (n_edges > 0 && (!node_pos || !sources || !targets || !src || !dst || !counts)))
+        return set_error(HB_EINVAL, "hb_edge_prepare: bad arguments");
+    if (n_edges == 0) return HB_OK;
+    edge_prepare_kernel<<<(unsigned)((n_edges + 255) / 256), 256, 0, as_stream(stream)>>>(
+        reinterpret_cast<const double2 *>(node_pos), sources, targets, n_edges, origin_x,
+        origin_y, cell, delta, reinterpret_cast<double2 *>(src), reinterpret_cast<double2 *>(dst),
+        counts);
+    return check_launch("hb_edge_prepare");
+}
+
+int hb_to_world_nodes(const double *pts, const int64_t *starts, int64_t n_edges, double origin_x,
+                      double origin_y, double cell, const double *node_pos,
+                      const int64_t *sources, const int64_t *targets, double *out,
+                      void *stream) {
+    if (n_edges < 0 ||
+        (n_edges > 0 && (!pts || !starts || !out || !node_pos || !sources || !targets)))
+        return set_error(HB_EINVAL, "hb_to_world_nodes: bad arguments");
+    if (n_edges == 0) return HB_OK;
+    to_world_nodes_kernel<<<warp_blocks(n_edges, 256), 256, 0, as_stream(stream)>>>(
+        reinterpret_cast<const double2 *>(pts), starts, n_edges, origin_x, origin_y, cell,
+        reinterpret_cast<const double2 *>(node_pos), sources, targets,
+        reinterpret_cast<double2 *>(out));
+    return check_launch("hb_to_world_nodes");
 }
 
 int hb_splat(const double *pts, const int64_t *starts, int64_t n_edges, int64_t n_pts,

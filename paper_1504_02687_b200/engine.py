@@ -79,6 +79,21 @@ def download(t: torch.Tensor) -> np.ndarray:
     return t.cpu().numpy()
 
 
+def download_pinned(t: torch.Tensor) -> np.ndarray:
+    """Device -> host into page-locked memory, returned as a numpy view.
+
+    Copying a multi-GB result into fresh pageable memory is dominated by
+    first-touch page faults (~2 s for config 4's 4.3 GB of polylines); a
+    pinned destination takes the DMA path (~60 GB/s), and torch's pinned
+    host allocator caches the block when the caller drops the result, so
+    repeated bundle() calls reuse it instead of calling cudaHostAlloc.
+    """
+    IO_BYTES["d2h"] += t.numel() * t.element_size()
+    host = torch.empty(t.shape, dtype=t.dtype, pin_memory=True)
+    host.copy_(t)
+    return host.numpy()
+
+
 def stream_ptr() -> int:
     return torch.cuda.current_stream().cuda_stream
 
@@ -127,7 +142,8 @@ class BundleEngine:
                  weights: WeightPlan, matrix: np.ndarray, shape: tuple[int, int],
                  cfg: BundleConfig, *, fixed_step: bool = False,
                  offset_disp: np.ndarray | None = None, device=None,
-                 reduce_hist=None, capacity_factor: float = 2.0):
+                 reduce_hist=None, capacity_factor: float = 2.0,
+                 starts: torch.Tensor | None = None):
         N.lib()  # fail loudly if the native library is missing
         if not torch.cuda.is_available():
             raise N.NativeError("paper_1504_02687_b200 needs a CUDA device (sm_100a); "
@@ -147,15 +163,20 @@ class BundleEngine:
         E, B = self.n_edges, self.nbins
         dev = self.dev
 
-        counts = sample_counts(src, dst, self.delta)
-        starts = np.zeros(E + 1, dtype=np.int64)
-        np.cumsum(counts, out=starts[1:])
-        self.n_pts = int(starts[-1])
+        on_device = isinstance(src, torch.Tensor)
+        if on_device:
+            # src/dst/starts were prepared on the device (hb_edge_prepare)
+            self.n_pts = int(download(starts[E:E + 1])[0]) if E else 0
+        else:
+            counts = sample_counts(src, dst, self.delta)
+            starts_h = np.zeros(E + 1, dtype=np.int64)
+            np.cumsum(counts, out=starts_h[1:])
+            self.n_pts = int(starts_h[-1])
         self.cap = max(int(self.n_pts * capacity_factor), 1024)
         self.pts = torch.empty((self.cap, 2), dtype=torch.float64, device=dev)
         self.alt = torch.empty((self.cap, 2), dtype=torch.float64, device=dev)
         self.pos = torch.empty(self.cap, dtype=torch.int32, device=dev)
-        self.starts = upload(starts, dev)
+        self.starts = starts if on_device else upload(starts_h, dev)
         self.starts_alt = torch.empty_like(self.starts)
         self.ecounts = torch.empty(max(E, 1), dtype=torch.int64, device=dev)
         self.groups = upload(np.asarray(groups, dtype=np.int32), dev)
@@ -221,8 +242,8 @@ class BundleEngine:
         self.trace: dict | None = None
 
         s = stream_ptr()
-        srcd = upload(np.asarray(src, dtype=np.float64), dev)
-        dstd = upload(np.asarray(dst, dtype=np.float64), dev)
+        srcd = src if on_device else upload(np.asarray(src, dtype=np.float64), dev)
+        dstd = dst if on_device else upload(np.asarray(dst, dtype=np.float64), dev)
         N.call("hb_sample_fill", ptr(srcd), ptr(dstd), ptr(self.starts), E,
                ptr(self.pts), s)
         if offset_disp is not None:
@@ -400,6 +421,15 @@ class BundleEngine:
     # ------------------------------------------------------------------
     def packed_points(self) -> tuple[torch.Tensor, torch.Tensor]:
         return self.pts[: self.n_pts], self.starts
+
+    def world_points_nodes(self, origin, cell, node_pos: torch.Tensor, sources: torch.Tensor,
+                           targets: torch.Tensor) -> torch.Tensor:
+        """grid -> world with the endpoint pins gathered on the device."""
+        out = torch.empty((self.n_pts, 2), dtype=torch.float64, device=self.dev)
+        N.call("hb_to_world_nodes", ptr(self.pts), ptr(self.starts), self.n_edges,
+               float(origin[0]), float(origin[1]), float(cell), ptr(node_pos), ptr(sources),
+               ptr(targets), ptr(out), stream_ptr())
+        return out
 
     def world_points(self, origin, cell, src_world=None, dst_world=None) -> torch.Tensor:
         out = torch.empty((self.n_pts, 2), dtype=torch.float64, device=self.dev)

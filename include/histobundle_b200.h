@@ -192,6 +192,13 @@ HB_API int hb_integral_image(const float *in, int nbins, int nv, int nu, double 
 HB_API int hb_used_cells(const float *rho, const float *layer_peak, int nbins, int nv,
                   int nu, double rel, unsigned long long *count, void *stream);
 
+/* Packed advection field out[l][v][u] = (rho, dX, dY, 0) float4 (16-byte
+ * aligned, B*V*U*4 floats): dX/dY are _cell_gradient's float32 differences
+ * (_kernels.py:101-114) at the clamped cell.  Optional input of
+ * hb_advect_laplacian. */
+HB_API int hb_grad_field(const float *rho, int nbins, int nv, int nu, float *out,
+                         void *stream);
+
 /* Size (doubles) of the disp_partials buffer hb_advect_laplacian fills. */
 HB_API int64_t hb_advect_partials(void);
 
@@ -202,13 +209,15 @@ HB_API int64_t hb_advect_partials(void);
  *   counts/pos = resample_count(pts_out, delta)   (when counts != NULL;
  *   same outputs as hb_resample_count).
  * h < 0 skips advection (Laplacian only, bundler.laplacian_smooth).
+ * grad_field (nullable) is hb_grad_field(rho): same results, fewer gathers.
  * pts_out may alias pts_in.  edge_layer: (E) int32 layer of each edge (its
  * bin).  moved: u64 accumulator (added to).  disp_partials:
  * hb_advect_partials() doubles (zeroed and filled here), summed by
  * hb_reduce_f64 in fixed order. */
 HB_API int hb_advect_laplacian(const double *pts_in, double *pts_out,
                         const int64_t *starts, int64_t n_edges, int64_t n_pts,
-                        const int32_t *edge_layer, const float *rho, int nbins,
+                        const int32_t *edge_layer, const float *rho,
+                        const float *grad_field, int nbins,
                         int nv, int nu, double h, double eps, double min_step,
                         int fixed_step, double lap_factor, int lap_passes,
                         double delta, int64_t *counts, int32_t *pos,

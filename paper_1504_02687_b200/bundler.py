@@ -336,7 +336,7 @@ def advect_point(p, field: DensityField, layer: int, h: float, epsilon: float = 
     layer0 = torch.zeros(1, dtype=torch.int32, device=pts.device)
     moved = torch.zeros(1, dtype=torch.int64, device=pts.device)
     part = torch.zeros(int(N.lib().hb_advect_partials()), dtype=torch.float64, device=pts.device)
-    N.call("hb_advect_laplacian", ptr(pts), ptr(out), ptr(starts), 1, 3, ptr(layer0), ptr(rho),
+    N.call("hb_advect_laplacian", ptr(pts), ptr(out), ptr(starts), 1, 3, ptr(layer0), ptr(rho), None,
            1, nv, nu, float(h), float(epsilon), float(min_step), int(bool(fixed_step)), 0.5, 0,
            1.0, None, None, ptr(moved), ptr(part), stream_ptr())
     return out.cpu().numpy()[1].copy()
@@ -351,7 +351,7 @@ def laplacian_smooth(polyline: SampledEdge, factor: float = 0.5, passes: int = 1
     moved = torch.zeros(1, dtype=torch.int64, device=pts.device)
     part = torch.zeros(int(N.lib().hb_advect_partials()), dtype=torch.float64, device=pts.device)
     if passes > 0:  # in place; h < 0: Laplacian sweeps only
-        N.call("hb_advect_laplacian", ptr(pts), ptr(pts), ptr(starts), 1, n, None, None, 1, 3, 3,
+        N.call("hb_advect_laplacian", ptr(pts), ptr(pts), ptr(starts), 1, n, None, None, None, 1, 3, 3,
                -1.0, 1e-8, MIN_STEP, 0, float(factor), int(passes), 1.0, None, None, ptr(moved),
                ptr(part), stream_ptr())
     polyline.points[...] = pts.cpu().numpy()

@@ -34,7 +34,8 @@ struct Adv {
 // _kernels.py:163-199 for one interior point.  (A warp-cooperative variant
 // that tests the remaining candidates of pending points on idle lanes was
 // measured slower on B200: the shuffles cost more than the divergence.)
-__device__ __forceinline__ Adv advect_one(const float *__restrict__ rho, int nv, int nu,
+__device__ __forceinline__ Adv advect_one(const float *__restrict__ rho,
+                                          const float4 *__restrict__ gf, int nv, int nu,
                                           double xhi, double yhi, double2 p, double h,
                                           double eps, double min_step, int fixed) {
     Adv r{p, false, 0.0};
@@ -43,7 +44,10 @@ __device__ __forceinline__ Adv advect_one(const float *__restrict__ rho, int nv,
     // G = 2*gradient exactly, so |G| = 2*gn and G/|G| == g/gn bit for bit;
     // only the eps clamp (gn < eps <=> |G| < 2*eps) needs the scaled values
     double Gx, Gy, r0;
-    gradient2_value_ref(rho, nv, nu, x, y, Gx, Gy, r0);
+    if (gf)
+        gradient2_value_gf(gf, nv, nu, x, y, Gx, Gy, r0);
+    else
+        gradient2_value_ref(rho, nv, nu, x, y, Gx, Gy, r0);
     const double Gn = hypot_ref(Gx, Gy);
     double dx, dy;
     if (Gn < 2.0 * eps) {
@@ -70,12 +74,16 @@ __device__ __forceinline__ Adv advect_one(const float *__restrict__ rho, int nv,
     return r;
 }
 
-__global__ void __launch_bounds__(kStreamBlock, 3)
+// One instantiation per stage combination, so each launch carries only the
+// registers its stages need (a fused advect+count build measured slower than
+// advect and count as two launches: the count's state cut occupancy).
+template <bool ADV, bool LAP, bool COUNT>
+__global__ void __launch_bounds__(kStreamBlock, (ADV && COUNT) ? 3 : 4)
 polyline_pass_kernel(const PolylinePass p) {
     const unsigned full = 0xffffffffu;
     const int lane = threadIdx.x & 31;
-    const bool do_adv = p.h >= 0.0;
-    const bool do_count = p.counts != nullptr;
+    constexpr bool do_adv = ADV;
+    constexpr bool do_count = COUNT;
     const double lo = 0.5 * p.delta, hi = 1.5 * p.delta;  // _kernels.py:211-212
     const double lo2 = do_count ? sqrt_lt_bound(lo) : 0.0;
     const double hi2 = do_count ? sqrt_gt_bound(hi) : 0.0;
@@ -97,7 +105,9 @@ polyline_pass_kernel(const PolylinePass p) {
         const int n = (int)(t_nx - s);
         if (e + nwarps < p.n_edges) { s_nx = p.starts[e + nwarps]; t_nx = p.starts[e + nwarps + 1]; }
         const double2 *pin = p.pin + s;
-        const float *rho = do_adv ? p.rho + (int64_t)p.edge_layer[e] * p.plane : nullptr;
+        const int64_t lbase = do_adv ? (int64_t)p.edge_layer[e] * p.plane : 0;
+        const float *rho = do_adv ? p.rho + lbase : nullptr;
+        const float4 *gf = (do_adv && p.gf) ? p.gf + lbase : nullptr;
 
         double2 cur = make_double2(0.0, 0.0);   // A(chunk c), lane = local index - c0
         double2 left = make_double2(0.0, 0.0);  // A(c0 - 1)
@@ -113,7 +123,7 @@ polyline_pass_kernel(const PolylinePass p) {
             if (jn + kWarp < n) raw = pin[jn + kWarp];
             if (jn < n) {
                 if (do_adv && jn > 0 && jn < n - 1) {
-                    const Adv a = advect_one(rho, p.nv, p.nu, xhi, yhi, nxt, p.h, p.eps,
+                    const Adv a = advect_one(rho, gf, p.nv, p.nu, xhi, yhi, nxt, p.h, p.eps,
                                              p.min_step, p.fixed);
                     my_moved += a.moved;
                     if (a.moved) my_disp = dadd(my_disp, a.disp);
@@ -132,7 +142,7 @@ polyline_pass_kernel(const PolylinePass p) {
             const int j = c0 + lane;
             const bool valid = j < n;
             double2 f = cur;
-            if (p.lap) {
+            if (LAP) {
                 double lx = __shfl_up_sync(full, cur.x, 1), ly = __shfl_up_sync(full, cur.y, 1);
                 double rx = __shfl_down_sync(full, cur.x, 1), ry = __shfl_down_sync(full, cur.y, 1);
                 const double n0x = __shfl_sync(full, nxt.x, 0), n0y = __shfl_sync(full, nxt.y, 0);
@@ -151,7 +161,9 @@ polyline_pass_kernel(const PolylinePass p) {
                 double qx = __shfl_up_sync(full, f.x, 1), qy = __shfl_up_sync(full, f.y, 1);
                 if (lane == 0) { qx = prevf.x; qy = prevf.y; }
                 const bool part = valid && j > 0;  // local point 0 is always kept at 0
-                // squared gaps; g < lo <=> g2 < lo2 exactly (see sqrt_lt_bound)
+                // squared gaps; g < lo <=> g2 < lo2 exactly (see sqrt_lt_bound).
+                // (A bit-parallel resolution of isolated merges was measured
+                // slower: in bundles merges come in long chains.)
                 const double gs = part ? dist2_ref(f.x, f.y, qx, qy) : 0.0;
                 const bool last = (j == n - 1);
                 bool kept = false;
@@ -232,14 +244,30 @@ polyline_pass_kernel(const PolylinePass p) {
     }
 }
 
-int launch_polyline_pass(const PolylinePass &p, cudaStream_t st, const char *what) {
-    if (p.n_edges == 0) return HB_OK;
-    const unsigned grid = persistent_grid(polyline_pass_kernel, p.n_edges);
+template <bool ADV, bool LAP, bool COUNT>
+static int launch_variant(const PolylinePass &p, cudaStream_t st, const char *what) {
+    const unsigned grid = persistent_grid(polyline_pass_kernel<ADV, LAP, COUNT>, p.n_edges);
     if (p.partials &&
         cudaMemsetAsync(p.partials, 0, sizeof(double) * kMaxStreamBlocks, st) != cudaSuccess)
         return check_launch(what, 0);
-    polyline_pass_kernel<<<grid, kStreamBlock, 0, st>>>(p);
+    polyline_pass_kernel<ADV, LAP, COUNT><<<grid, kStreamBlock, 0, st>>>(p);
     return check_launch(what);
+}
+
+int launch_polyline_pass(const PolylinePass &p, cudaStream_t st, const char *what) {
+    if (p.n_edges == 0) return HB_OK;
+    const bool adv = p.h >= 0.0, lap = p.lap != 0, cnt = p.counts != nullptr;
+    const int v = (adv ? 4 : 0) | (lap ? 2 : 0) | (cnt ? 1 : 0);
+    switch (v) {
+        case 0: return launch_variant<false, false, false>(p, st, what);
+        case 1: return launch_variant<false, false, true>(p, st, what);
+        case 2: return launch_variant<false, true, false>(p, st, what);
+        case 3: return launch_variant<false, true, true>(p, st, what);
+        case 4: return launch_variant<true, false, false>(p, st, what);
+        case 5: return launch_variant<true, false, true>(p, st, what);
+        case 6: return launch_variant<true, true, false>(p, st, what);
+        default: return launch_variant<true, true, true>(p, st, what);
+    }
 }
 
 // one block, fixed summation order
@@ -283,7 +311,8 @@ int64_t hb_advect_partials(void) { return kMaxStreamBlocks; }
 
 int hb_advect_laplacian(const double *pts_in, double *pts_out, const int64_t *starts,
                         int64_t n_edges, int64_t n_pts, const int32_t *edge_layer,
-                        const float *rho, int nbins, int nv, int nu, double h, double eps,
+                        const float *rho, const float *grad_field, int nbins, int nv, int nu,
+                        double h, double eps,
                         double min_step, int fixed_step, double lap_factor, int lap_passes,
                         double delta, int64_t *counts, int32_t *pos,
                         unsigned long long *moved, double *disp_partials, void *stream) {
@@ -302,6 +331,7 @@ int hb_advect_laplacian(const double *pts_in, double *pts_out, const int64_t *st
     p.n_edges = n_edges;
     p.edge_layer = edge_layer;
     p.rho = rho;
+    p.gf = reinterpret_cast<const float4 *>(grad_field);
     p.plane = (int64_t)nv * nu;
     p.nv = nv;
     p.nu = nu;

@@ -157,6 +157,27 @@ __global__ void mix_pass_kernel(const T *__restrict__ groups, const float *__res
     }
 }
 
+// Packed advection field: (rho, dX, dY, 0) per cell with the float32
+// central differences of _cell_gradient (_kernels.py:101-114) at the clamped
+// cell, so the advection reads one 16-byte value per stencil corner.
+__global__ void grad_field_kernel(const float *__restrict__ rho, int nv, int nu,
+                                  float4 *__restrict__ out) {
+    const int u = blockIdx.x * blockDim.x + threadIdx.x;
+    const int v = blockIdx.y;
+    const int l = blockIdx.z;
+    if (u >= nu) return;
+    const int64_t plane = (int64_t)nv * nu;
+    const float *r = rho + l * plane;
+    const int uc = min(max(u, 1), nu - 2), vc = min(max(v, 1), nv - 2);
+    const float *c = r + (int64_t)vc * nu + uc;
+    float dx = 0.0f, dy = 0.0f;
+    if (nu >= 3 && nv >= 3) {
+        dx = __fsub_rn(c[1], c[-1]);
+        dy = __fsub_rn(c[nu], c[-nu]);
+    }
+    out[l * plane + (int64_t)v * nu + u] = make_float4(r[(int64_t)v * nu + u], dx, dy, 0.0f);
+}
+
 // used_cell_count (bundler.py:292-305): rho > float32(rel * peak_l) when
 // peak_l > 0 (NEP 50 makes the comparison float32).
 __global__ void used_cells_kernel(const float *__restrict__ rho, const float *__restrict__ peak,
@@ -268,6 +289,15 @@ int hb_integral_image(const float *in, int nbins, int nv, int nu, double *table,
     const unsigned rb = (unsigned)((rows + 32 * kRowWarps - 1) / (32 * kRowWarps));
     row_scan_kernel<<<rb, kRowWarps * 32, 0, st>>>(table, rows, nu);
     return check_launch("hb_integral_image", 2);
+}
+
+int hb_grad_field(const float *rho, int nbins, int nv, int nu, float *out, void *stream) {
+    if (!rho || !out || nbins < 1 || nv < 3 || nu < 3 || nv > kMaxDim || nu > kMaxDim)
+        return set_error(HB_EINVAL, "hb_grad_field: bad arguments");
+    dim3 g((nu + 255) / 256, nv, nbins);
+    grad_field_kernel<<<g, 256, 0, as_stream(stream)>>>(rho, nv, nu,
+                                                       reinterpret_cast<float4 *>(out));
+    return check_launch("hb_grad_field");
 }
 
 int hb_used_cells(const float *rho, const float *layer_peak, int nbins, int nv, int nu,

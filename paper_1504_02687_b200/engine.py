@@ -10,8 +10,9 @@ stream:
   i = 0: hb_splat
   [world > 1: all-reduce of the int32 counts over NCCL]
   hb_smooth (mix + 3 exact box passes + layer peaks)
-  hb_advect_laplacian: advect + Laplacian + the NEXT iteration's resample
-         count in one streaming pass (+ per-block metric partials)
+  hb_grad_field (packed rho/dX/dY), hb_advect_laplacian: advect + Laplacian
+         in one streaming pass (+ per-block metric partials), then
+         hb_resample_count for the NEXT iteration's resample
   hb_reduce_f64, hb_used_cells
 
 Host reads per iteration: the new point total (needed to size the emit
@@ -188,6 +189,12 @@ class BundleEngine:
         hdtype = torch.float32 if self.wkind == "float" else torch.int32
         self.hist = torch.empty((B, self.nv, self.nu), dtype=hdtype, device=dev)
         self.field = torch.empty((B, self.nv, self.nu), dtype=torch.float32, device=dev)
+        # packed (rho, dX, dY) advection field (hb_grad_field), 16 B per cell
+        self.gfield = torch.empty((B, self.nv, self.nu, 4), dtype=torch.float32, device=dev)
+        # resample count as its own launch after the advect pass (measured
+        # faster than fusing it: the fused build's register footprint halves
+        # the advect's occupancy)
+        self.split_count = True
         self.peak = torch.empty(B, dtype=torch.float32, device=dev)
         self.status = torch.zeros(1, dtype=torch.int32, device=dev)
         sws = N.lib().hb_smooth_workspace_bytes(B, self.nv, self.nu)
@@ -356,14 +363,19 @@ class BundleEngine:
                 self.radii.data_ptr(), int(self.radii.numel()), ptr(self.field),
                 ptr(self.smooth_ws), self.smooth_ws.numel(), ptr(self.peak), s)
         h_i = cfg.lambda_ ** i * cfg.h_max  # bundler.py:360, Python float power
-        # advect -> Laplacian -> next iteration's resample count, in place
+        # advect -> Laplacian (-> next iteration's resample count), in place
         last = i == self.iters - 1
+        self._k("hb_grad_field", ptr(self.field), B, nv, nu, ptr(self.gfield), s)
+        fuse = not last and not self.split_count
         self._k("hb_advect_laplacian", ptr(self.pts), ptr(self.pts), ptr(self.starts), E,
-                self.n_pts, ptr(self.groups), ptr(self.field), B, nv, nu, float(h_i),
-                float(cfg.epsilon), MIN_STEP, int(self.fixed_step),
+                self.n_pts, ptr(self.groups), ptr(self.field), ptr(self.gfield), B, nv, nu,
+                float(h_i), float(cfg.epsilon), MIN_STEP, int(self.fixed_step),
                 float(cfg.laplacian_factor), self.lap_passes, self.delta,
-                None if last else ptr(self.ecounts), None if last else ptr(self.pos),
+                ptr(self.ecounts) if fuse else None, ptr(self.pos) if fuse else None,
                 self.m_moved.data_ptr() + 8 * i, ptr(self._partials), s)
+        if not last and self.split_count:
+            self._k("hb_resample_count", ptr(self.pts), ptr(self.starts), E, self.delta,
+                    ptr(self.ecounts), ptr(self.pos), s)
         self._k("hb_reduce_f64", ptr(self._partials), self._partials.numel(),
                 self.m_disp.data_ptr() + 8 * i, s)
         self._k("hb_used_cells", ptr(self.field), ptr(self.peak), B, nv, nu, 0.01,

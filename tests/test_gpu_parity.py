@@ -141,7 +141,7 @@ def test_advect_matches_reference_kat(fixed):
     h = 3.0 if fixed else 6.0
     s = stream_ptr()
     N.call("hb_advect_laplacian", ptr(dev(pts)), ptr(out), ptr(dev(starts)), E, n,
-           ptr(dev(groups.astype(np.int32))), ptr(dev(rho)), nb, nv, nu, h, 1e-8, 0.25,
+           ptr(dev(groups.astype(np.int32))), ptr(dev(rho)), None, nb, nv, nu, h, 1e-8, 0.25,
            int(fixed), 0.5, 0, 1.0, None, None, ptr(moved), ptr(part), s)
     N.call("hb_reduce_f64", ptr(part), part.numel(), ptr(disp), s)
     sync()
@@ -162,7 +162,7 @@ def test_laplacian_matches_reference_kat(factor, passes, key):
     rho = torch.zeros((1, 3, 3), dtype=torch.float32, device="cuda")
     grp = torch.zeros(E, dtype=torch.int32, device="cuda")
     N.call("hb_advect_laplacian", ptr(dev(pts)), ptr(out), ptr(dev(starts)), E, n, ptr(grp),
-           ptr(rho), 1, 3, 3, -1.0, 1e-8, 0.25, 0, factor, passes, 1.0, None, None, ptr(moved),
+           ptr(rho), None, 1, 3, 3, -1.0, 1e-8, 0.25, 0, factor, passes, 1.0, None, None, ptr(moved),
            ptr(part), stream_ptr())
     sync()
     assert np.array_equal(out.cpu().numpy(), k[key])
@@ -251,7 +251,7 @@ def test_advect_laplacian_random_vs_oracle():
     counts = torch.empty(E, dtype=torch.int64, device="cuda")
     pos = torch.empty(n, dtype=torch.int32, device="cuda")
     N.call("hb_advect_laplacian", ptr(dev(pts)), ptr(out), ptr(dev(starts)), E, n,
-           ptr(dev(groups.astype(np.int32))), ptr(dev(rho)), 2, nv, nu, 9.0, 1e-8, 0.25, 0, 0.5,
+           ptr(dev(groups.astype(np.int32))), ptr(dev(rho)), None, 2, nv, nu, 9.0, 1e-8, 0.25, 0, 0.5,
            2, delta, ptr(counts), ptr(pos), ptr(dmoved), ptr(part), stream_ptr())
     sync()
     assert np.array_equal(out.cpu().numpy(), ref)

@@ -121,7 +121,7 @@ def test_library_rejects_bad_arguments_without_gpu():
     lib = _native.load_library()
     assert lib.hb_splat(None, None, 5, 10, None, None, None, 1, 4, 4, None, None, None) == -1
     assert b"bad arguments" in lib.hb_last_error()
-    assert lib.hb_advect_laplacian(None, None, None, 1, 1, None, None, 1, 8, 8, 1.0, 1e-8, 0.25,
+    assert lib.hb_advect_laplacian(None, None, None, 1, 1, None, None, None, 1, 8, 8, 1.0, 1e-8, 0.25,
                                    0, 0.5, 1, 1.0, None, None, None, None, None) == -1
 
 

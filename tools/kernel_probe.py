@@ -163,9 +163,15 @@ def main():
     h = cfg.lambda_ ** args.iters * cfg.h_max
     work = torch.empty_like(eng.alt)
 
+    gfield = torch.empty((Bn, nv, nu, 4), dtype=torch.float32, device="cuda")
+    N.call("hb_grad_field", ptr(eng.field), Bn, nv, nu, ptr(gfield), s)
+    out["grad_field_ms"] = timed(lambda: N.call("hb_grad_field", ptr(eng.field), Bn, nv, nu,
+                                                ptr(gfield), s))
+    use_gf = [None]
+
     def adv(h_, lap, count):
         N.call("hb_advect_laplacian", ptr(eng.alt), ptr(work), ptr(eng.starts_alt), E, n_new,
-               ptr(eng.groups), ptr(eng.field), Bn, nv, nu, float(h_), float(cfg.epsilon),
+               ptr(eng.groups), ptr(eng.field), use_gf[0], Bn, nv, nu, float(h_), float(cfg.epsilon),
                MIN_STEP, 0, float(cfg.laplacian_factor), lap, float(cfg.delta),
                ptr(eng.ecounts) if count else None, ptr(eng.pos) if count else None,
                eng.m_moved.data_ptr(), ptr(eng._partials), s)
@@ -175,6 +181,10 @@ def main():
     out["adv_only_ms"] = timed(lambda: adv(h, 0, False))
     out["lap_only_ms"] = timed(lambda: adv(-1.0, 1, False))
     out["count_only_ms"] = timed(lambda: adv(-1.0, 0, True))
+    use_gf[0] = ptr(gfield)
+    out["gf_adv_lap_count_ms"] = timed(lambda: adv(h, 1, True))
+    out["gf_adv_lap_ms"] = timed(lambda: adv(h, 1, False))
+    out["gf_adv_only_ms"] = timed(lambda: adv(h, 0, False))
     out["copy_pts_ms"] = timed(lambda: work[:n_new].copy_(eng.alt[:n_new]))
     print(json.dumps(out))
 

@@ -170,6 +170,8 @@ polyline_pass_kernel(const PolylinePass p) {
                 double gk = 0.0;
                 int start = (c0 == 0) ? 1 : 0;
                 while (start < kWarp) {
+                    // speculate: every lane's predecessor is kept (lane
+                    // `start` measures against the anchor `ka`)
                     double geff = gs;
                     if (lane == start && part) geff = dist2_ref(f.x, f.y, ka.x, ka.y);
                     const bool act = part && lane >= start;
@@ -178,14 +180,25 @@ polyline_pass_kernel(const PolylinePass p) {
                         if (act) { kept = true; gk = geff; }
                         break;
                     }
-                    const int b = __ffs(m) - 1;
+                    const int b = __ffs(m) - 1;  // first merged lane
                     if (act && lane < b) { kept = true; gk = geff; }
                     // b and start are warp-uniform; shuffle unconditionally so
                     // the compiler needs no collective fix-up code
                     const double kx = __shfl_sync(full, f.x, b > 0 ? b - 1 : 0);
                     const double ky = __shfl_sync(full, f.y, b > 0 ? b - 1 : 0);
                     if (b > start) { ka.x = kx; ka.y = ky; }
-                    start = b + 1;
+                    // resolve the whole merge chain at once: every later lane
+                    // measures against the same anchor; the first one at
+                    // >= lo (or the polyline's last point) is kept
+                    const double ga = (part && lane > b) ? dist2_ref(f.x, f.y, ka.x, ka.y) : 0.0;
+                    const unsigned mc =
+                        __ballot_sync(full, part && lane > b && (last || !(ga < lo2)));
+                    if (mc == 0) break;  // chain runs past this chunk; anchor carries
+                    const int c = __ffs(mc) - 1;
+                    if (lane == c) { kept = true; gk = ga; }
+                    ka.x = __shfl_sync(full, f.x, c);
+                    ka.y = __shfl_sync(full, f.y, c);
+                    start = c + 1;
                 }
                 int pieces = 0;
                 if (kept) {

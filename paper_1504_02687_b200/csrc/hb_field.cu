@@ -32,6 +32,11 @@ __device__ __forceinline__ float mixed_value(const T *__restrict__ g, const floa
     return __double2float_rn(acc);
 }
 
+// Column folds: the values of a batch of kColBatch rows are loaded (and
+// mixed) first, independent of the running sum, so every thread keeps
+// kColBatch loads in flight; only the float64 adds are sequential.
+constexpr int kColBatch = 16;
+
 template <typename T>
 __global__ void __launch_bounds__(kColBlock)
 col_scan_mix_kernel(const T *__restrict__ groups, const float *__restrict__ mat, int nb, int nv,
@@ -40,12 +45,22 @@ col_scan_mix_kernel(const T *__restrict__ groups, const float *__restrict__ mat,
     const int l = blockIdx.y;
     if (u >= nu) return;
     const int64_t plane = (int64_t)nv * nu;
+    double *dst = table + l * plane + u;
     double c = 0.0;
-    for (int v = 0; v < nv; ++v) {
-        const int64_t off = (int64_t)v * nu + u;
-        const double hv = (double)mixed_value<T>(groups, mat, nb, l, plane, off);
-        c = (v == 0) ? hv : dadd(c, hv);
-        table[l * plane + off] = c;
+    for (int v0 = 0; v0 < nv; v0 += kColBatch) {
+        double hv[kColBatch];
+#pragma unroll
+        for (int k = 0; k < kColBatch; ++k)
+            hv[k] = (v0 + k < nv)
+                        ? (double)mixed_value<T>(groups, mat, nb, l, plane, (int64_t)(v0 + k) * nu + u)
+                        : 0.0;
+#pragma unroll
+        for (int k = 0; k < kColBatch; ++k) {
+            if (v0 + k < nv) {
+                c = (v0 + k == 0) ? hv[k] : dadd(c, hv[k]);
+                dst[(int64_t)(v0 + k) * nu] = c;
+            }
+        }
     }
 }
 
@@ -59,44 +74,86 @@ col_scan_f32_kernel(const float *__restrict__ in, int nv, int nu,
     const float *src = in + l * plane + u;
     double *dst = table + l * plane + u;
     double c = 0.0;
-#pragma unroll 4
-    for (int v = 0; v < nv; ++v) {
-        const double x = (double)__ldg(src + (int64_t)v * nu);
-        c = (v == 0) ? x : dadd(c, x);
-        dst[(int64_t)v * nu] = c;
+    float nxt[kColBatch];
+#pragma unroll
+    for (int k = 0; k < kColBatch; ++k) nxt[k] = k < nv ? __ldg(src + (int64_t)k * nu) : 0.0f;
+    for (int v0 = 0; v0 < nv; v0 += kColBatch) {
+        float cur[kColBatch];
+#pragma unroll
+        for (int k = 0; k < kColBatch; ++k) cur[k] = nxt[k];
+        // prefetch the next batch before the dependent adds of this one
+#pragma unroll
+        for (int k = 0; k < kColBatch; ++k) {
+            const int v = v0 + kColBatch + k;
+            nxt[k] = v < nv ? __ldg(src + (int64_t)v * nu) : 0.0f;
+        }
+#pragma unroll
+        for (int k = 0; k < kColBatch; ++k) {
+            if (v0 + k < nv) {
+                const double x = (double)cur[k];
+                c = (v0 + k == 0) ? x : dadd(c, x);
+                dst[(int64_t)(v0 + k) * nu] = c;
+            }
+        }
     }
 }
 
 // Row fold in place.  Rows are flattened over (layer, v).  A warp owns 32
-// rows; for each 32-column tile it loads coalesced into shared memory, each
-// lane folds its own row left to right, and the tile is stored back.
-constexpr int kRowWarps = 4;
+// rows and walks them in 32x32 tiles: tile t+1 is copied into shared memory
+// with cp.async while each lane folds its own row of tile t left to right,
+// then tile t is stored back coalesced.
+constexpr int kRowWarps = 2;
+
+__device__ __forceinline__ void cp_async8(void *smem, const void *gmem) {
+    const unsigned sa = (unsigned)__cvta_generic_to_shared(smem);
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(sa), "l"(gmem));
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() {
+    asm volatile("cp.async.wait_group %0;\n" ::"n"(N));
+}
 
 __global__ void __launch_bounds__(kRowWarps * 32)
 row_scan_kernel(double *__restrict__ table, int64_t n_rows, int nu) {
-    __shared__ double tile[kRowWarps][32][33];
+    __shared__ double tile[kRowWarps][2][32][33];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int64_t r0 = ((int64_t)blockIdx.x * kRowWarps + warp) * 32;
     if (r0 >= n_rows) return;
     const int nr = (int)(n_rows - r0 < 32 ? n_rows - r0 : 32);
-    double (*t)[33] = tile[warp];
-    double carry = 0.0;
-    for (int c0 = 0; c0 < nu; c0 += 32) {
+    const int ntiles = (nu + 31) / 32;
+    auto issue = [&](int t) {
+        const int c0 = t * 32;
         const int nc = nu - c0 < 32 ? nu - c0 : 32;
-        for (int i = 0; i < nr; ++i)
-            if (lane < nc) t[i][lane] = table[(r0 + i) * nu + c0 + lane];
+        if (lane < nc)
+            for (int i = 0; i < nr; ++i)
+                cp_async8(&tile[warp][t & 1][i][lane], table + (r0 + i) * nu + c0 + lane);
+        cp_async_commit();
+    };
+    issue(0);
+    double carry = 0.0;
+    for (int t = 0; t < ntiles; ++t) {
+        if (t + 1 < ntiles) {
+            issue(t + 1);
+            cp_async_wait<1>();
+        } else {
+            cp_async_wait<0>();
+        }
         __syncwarp();
+        double (*tt)[33] = tile[warp][t & 1];
+        const int c0 = t * 32;
+        const int nc = nu - c0 < 32 ? nu - c0 : 32;
         if (lane < nr) {
             double c = carry;
             for (int k = 0; k < nc; ++k) {
-                c = (c0 + k == 0) ? t[lane][k] : dadd(c, t[lane][k]);
-                t[lane][k] = c;
+                c = (c0 + k == 0) ? tt[lane][k] : dadd(c, tt[lane][k]);
+                tt[lane][k] = c;
             }
             carry = c;
         }
         __syncwarp();
-        for (int i = 0; i < nr; ++i)
-            if (lane < nc) table[(r0 + i) * nu + c0 + lane] = t[i][lane];
+        if (lane < nc)
+            for (int i = 0; i < nr; ++i) table[(r0 + i) * nu + c0 + lane] = tt[i][lane];
         __syncwarp();
     }
 }

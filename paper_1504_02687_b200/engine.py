@@ -293,16 +293,15 @@ class BundleEngine:
                     ptr(self.groups), ptr(self.wf32), ptr(self.hist), B, nv, nu,
                     ptr(self.status), s)
             return
+        # Straight initial polylines have no duplicate segments, so the key
+        # table would only add its expansion: splat directly (tile mode still
+        # takes its census for the first binned pass).
         sink = None
-        if self.tile_mode == 1:
-            sink = ctypes.byref(self.tiles)
-        elif self.tile_mode == 0:
+        if self.tile_mode == 0:
             self.t_fill.zero_()
             sink = ctypes.byref(self.tiles_census)
         self._k("hb_splat", ptr(self.pts), ptr(self.starts), E, self.n_pts, ptr(self.groups),
                 ptr(self.wint), ptr(self.hist), B, nv, nu, ptr(self.status), sink, s)
-        if self.tile_mode == 1:
-            self._k("hb_segtab_expand", sink, ptr(self.hist), nv, nu, s)
 
     def _ensure_records(self, n: int) -> None:
         if n <= self.t_rec.numel():

@@ -298,22 +298,29 @@ int hb_smooth(const int32_t *counts, const float *hist, const float *matrix, int
                                                           plane, dst, pk);
         } else {
             dim3 gc((nu + kColBlock - 1) / kColBlock, nbins);
-            if (mix_first && counts)
-                col_scan_mix_kernel<int32_t><<<gc, kColBlock, 0, st>>>(counts, matrix, nbins,
-                                                                       nv, nu, table);
-            else if (mix_first)
-                col_scan_mix_kernel<float><<<gc, kColBlock, 0, st>>>(hist, matrix, nbins, nv,
-                                                                     nu, table);
-            else
-                col_scan_f32_kernel<<<gc, kColBlock, 0, st>>>(first ? hist : src, nv, nu,
-                                                              table);
+            const float *fin = first ? hist : src;
+            if (mix_first) {
+                // H = float32(M * G) as its own elementwise pass into the stage
+                // buffer (a fused mix in the sequential column fold was measured
+                // 10x slower); the fold below consumes it before any pass
+                // output can overwrite the stage buffer
+                dim3 g((unsigned)((plane + 255) / 256), nbins);
+                if (counts)
+                    mix_pass_kernel<int32_t><<<g, 256, 0, st>>>(counts, matrix, nbins, plane,
+                                                                stage, nullptr);
+                else
+                    mix_pass_kernel<float><<<g, 256, 0, st>>>(hist, matrix, nbins, plane, stage,
+                                                              nullptr);
+                fin = stage;
+            }
+            col_scan_f32_kernel<<<gc, kColBlock, 0, st>>>(fin, nv, nu, table);
             const int64_t rows = (int64_t)nbins * nv;
             const unsigned rb = (unsigned)((rows + 32 * kRowWarps - 1) / (32 * kRowWarps));
             row_scan_kernel<<<rb, kRowWarps * 32, 0, st>>>(table, rows, nu);
             dim3 gb((nu + kBoxBlock - 1) / kBoxBlock, nv, nbins);
             box_kernel<<<gb, kBoxBlock, 0, st>>>(table, nv, nu, r, dst, pk);
         }
-        int rc = check_launch("hb_smooth", r == 0 ? 1 : 3);
+        int rc = check_launch("hb_smooth", r == 0 ? 1 : (mix_first ? 4 : 3));
         if (rc) return rc;
         src = dst;
     }

@@ -366,7 +366,9 @@ def main():
                        "delta": cfg.delta, "sigma": cfg.sigma, "lambda": cfg.lambda_,
                        "parallelism": f"edge-shard x{world}" + (" + nccl int32 allreduce"
                                                                  if world > 1 else ""),
-                       "l2": "inputs > L2 (point arrays >> 126 MB), no flush"},
+                       "l2": "inputs > L2 (point arrays >> 126 MB), no flush",
+                       "splat": {1: "segment-key table", 0: "tile records", -1: "direct"}[eng.tile_mode],
+                       "segment_key_ratio": [round(x, 4) for x in eng.key_ratio]},
             "roofline": roof, "cpu_baseline": cpu, "clocks": clk, "e2e": e2e,
             "gpu_launches": launches,
         }

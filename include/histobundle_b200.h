@@ -136,9 +136,10 @@ HB_API int hb_tiles_flush(const hb_tiles *t, int32_t *counts, int nv, int nu,
 HB_API int hb_segtab_geometry(int nbins, int nv, int nu, double max_seg_cells,
                               hb_tiles *t, int64_t *entries);
 
-/* Rasterise every non-zero segment key into counts and reset it to zero. */
+/* Rasterise every non-zero segment key into counts and reset it to zero;
+ * adds the number of non-zero keys to *nonzero (nullable). */
 HB_API int hb_segtab_expand(const hb_tiles *t, int32_t *counts, int nv, int nu,
-                            void *stream);
+                            unsigned long long *nonzero, void *stream);
 
 /* _kernels.accumulate (_kernels.py:46-77) via raster._accumulate_packed
  * (raster.py:70-94), per-group form: counts[group[e]] += weight[e] on every

@@ -71,7 +71,7 @@ SIGNATURES = {
     "hb_tiles_plan": (_I, [_P, _P, _P]),
     "hb_tiles_flush": (_I, [_P, _P, _I, _I, _P]),
     "hb_segtab_geometry": (_I, [_I, _I, _I, _D, _P, _P]),
-    "hb_segtab_expand": (_I, [_P, _P, _I, _I, _P]),
+    "hb_segtab_expand": (_I, [_P, _P, _I, _I, _P, _P]),
     "hb_splat": (_I, [_P, _P, _I64, _I64, _P, _P, _P, _I, _I, _I, _P, _P, _P]),
     "hb_splat_f32": (_I, [_P, _P, _I64, _I64, _P, _P, _P, _I, _I, _I, _P, _P]),
     "hb_smooth_workspace_bytes": (_SZ, [_I, _I, _I]),

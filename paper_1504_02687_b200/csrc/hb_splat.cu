@@ -225,8 +225,9 @@ constexpr int kExpandBlock = 256;
 
 __global__ void __launch_bounds__(kExpandBlock)
 segtab_expand_kernel(const __grid_constant__ hb_tiles t, int32_t *__restrict__ counts, int nv,
-                     int nu, int64_t n4) {
+                     int nu, int64_t n4, unsigned long long *__restrict__ nonzero) {
     const int H = t.halo, D = 2 * H + 1;
+    unsigned keys = 0;
     const int64_t plane = (int64_t)nv * nu;
     uint4 *tab4 = reinterpret_cast<uint4 *>(t.tab);
     for (int64_t q = (int64_t)blockIdx.x * kExpandBlock + threadIdx.x; q < n4;
@@ -239,6 +240,7 @@ segtab_expand_kernel(const __grid_constant__ hb_tiles t, int32_t *__restrict__ c
         for (int c = 0; c < 4; ++c) {
             const unsigned val = vals[c];
             if (!val) continue;
+            ++keys;
             const int64_t idx = q * 4 + c;
             const int64_t key = idx / plane;  // g*D*D + dir
             const int64_t cell = idx - key * plane;
@@ -251,6 +253,10 @@ segtab_expand_kernel(const __grid_constant__ hb_tiles t, int32_t *__restrict__ c
                 atomicAdd(layer + (int64_t)v * nu + u, (int)val);
             });
         }
+    }
+    if (nonzero) {
+        for (int o = 16; o; o >>= 1) keys += __shfl_down_sync(0xffffffffu, keys, o);
+        if ((threadIdx.x & 31) == 0 && keys) atomicAdd(nonzero, (unsigned long long)keys);
     }
 }
 
@@ -275,7 +281,8 @@ int hb_segtab_geometry(int nbins, int nv, int nu, double max_seg_cells, hb_tiles
     return HB_OK;
 }
 
-int hb_segtab_expand(const hb_tiles *t, int32_t *counts, int nv, int nu, void *stream) {
+int hb_segtab_expand(const hb_tiles *t, int32_t *counts, int nv, int nu,
+                     unsigned long long *nonzero, void *stream) {
     if (!t || t->mode != 1 || !t->tab || !counts || nv < 1 || nu < 1)
         return set_error(HB_EINVAL, "hb_segtab_expand: bad arguments");
     const int64_t D = 2 * t->halo + 1;
@@ -289,7 +296,7 @@ int hb_segtab_expand(const hb_tiles *t, int32_t *counts, int nv, int nu, void *s
     const int64_t want = (n4 + kExpandBlock - 1) / kExpandBlock;
     const int64_t cap = (int64_t)device_sm_count() * per_sm * 4;
     segtab_expand_kernel<<<(unsigned)(want < cap ? want : cap), kExpandBlock, 0,
-                           as_stream(stream)>>>(*t, counts, nv, nu, n4);
+                           as_stream(stream)>>>(*t, counts, nv, nu, n4, nonzero);
     return check_launch("hb_segtab_expand");
 }
 

@@ -216,6 +216,7 @@ class BundleEngine:
                                            ctypes.byref(geo), ctypes.byref(ent)) == 0
                     and ent.value * 4 <= budget):
                 self.t_tab = torch.zeros(ent.value, dtype=torch.int32, device=dev)
+                self.t_keys = torch.zeros(1, dtype=torch.int64, device=dev)
                 geo.tab = self.t_tab.data_ptr()
                 self.tiles, self.tile_mode = geo, 1
             elif N.lib().hb_tiles_geometry(B, self.nv, self.nu, 1.5 * self.delta + 2.0,
@@ -257,6 +258,9 @@ class BundleEngine:
             od = upload(offset_disp, dev)
             N.call("hb_offset", ptr(self.pts), ptr(self.starts), E, ptr(od), s)
         self.iteration = 0
+        self._tab_on = True       # segment-key table in use for the next emit
+        self._tab_segments = 0    # segments the last table pass saw
+        self.key_ratio: list[float] = []
 
     # ------------------------------------------------------------------
     def _ensure_capacity(self, n: int) -> None:
@@ -337,8 +341,21 @@ class BundleEngine:
             self._ensure_capacity(n_new)
             if fused and self.tile_mode == 0:
                 self._ensure_records(int(download(self.t_total)[0]))
-            if fused and self.tiles is not None:
+            if fused and self.tile_mode == 1 and self._tab_on:
+                # keys the last table pass produced vs segments it saw: the
+                # table only pays off once bundles make segments repeat
+                prev = int(download(self.t_keys)[0])
+                if self._tab_segments:
+                    self.key_ratio.append(prev / self._tab_segments)
+                    self._tab_on = prev <= 0.5 * self._tab_segments
+                self.t_keys.zero_()
+            elif fused and self.tile_mode == 1:
+                self._tab_on = True  # re-probe after one direct iteration
+                self._tab_segments = 0
+            use_tab = fused and self.tiles is not None and (self.tile_mode == 0 or self._tab_on)
+            if use_tab:
                 tiles = ctypes.byref(self.tiles)
+                self._tab_segments = n_new - E
             self._k("hb_resample_emit", ptr(self.pts), ptr(self.starts), E, self.n_pts,
                     ptr(self.pos), ptr(self.starts_alt), ptr(self.alt), ptr(self.groups),
                     ptr(self.wint), ptr(self.hist) if fused else None, nv, nu,
@@ -346,7 +363,7 @@ class BundleEngine:
             if self.tile_mode == 0 and tiles is not None:
                 self._k("hb_tiles_flush", tiles, ptr(self.hist), nv, nu, s)
             elif self.tile_mode == 1 and tiles is not None:
-                self._k("hb_segtab_expand", tiles, ptr(self.hist), nv, nu, s)
+                self._k("hb_segtab_expand", tiles, ptr(self.hist), nv, nu, ptr(self.t_keys), s)
             self.pts, self.alt = self.alt, self.pts
             self.starts, self.starts_alt = self.starts_alt, self.starts
             self.n_pts = n_new
@@ -400,6 +417,7 @@ class BundleEngine:
         self.starts.copy_(starts0)
         self.n_pts = n0
         self.iteration = 0
+        self._tab_on, self._tab_segments, self.key_ratio = True, 0, []
         self.records = []
         self._ev = []
         self.m_moved.zero_()

@@ -89,7 +89,7 @@ def main():
                    ptr(eng.hist), nv, nu, ptr(eng.status), tl, s)
 
         def expand():
-            N.call("hb_segtab_expand", tl, ptr(eng.hist), nv, nu, s)
+            N.call("hb_segtab_expand", tl, ptr(eng.hist), nv, nu, None, s)
 
         out["segtab"] = {"halo": eng.tiles.halo, "entries": int(eng.t_tab.numel())}
         out["emit_segtab_ms"] = timed(lambda: (emit_segtab(), expand()), reps=1)

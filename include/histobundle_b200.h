@@ -193,10 +193,11 @@ HB_API int hb_integral_image(const float *in, int nbins, int nv, int nu, double 
 HB_API int hb_used_cells(const float *rho, const float *layer_peak, int nbins, int nv,
                   int nu, double rel, unsigned long long *count, void *stream);
 
-/* Packed advection field out[l][v][u] = (rho, dX, dY, 0) float4 (16-byte
- * aligned, B*V*U*4 floats): dX/dY are _cell_gradient's float32 differences
- * (_kernels.py:101-114) at the clamped cell.  Optional input of
- * hb_advect_laplacian. */
+/* Quad advection field, 3 planes of B*V*U float4 (12 floats per cell,
+ * 16-byte aligned): Q = rho at the cell's 2x2 corners, GX/GY = the float32
+ * central differences of _cell_gradient (_kernels.py:101-114) at those
+ * corners.  Optional input of hb_advect_laplacian (same results, 4 vector
+ * loads per point instead of ~9 scattered ones). */
 HB_API int hb_grad_field(const float *rho, int nbins, int nv, int nu, float *out,
                          void *stream);
 

@@ -34,8 +34,8 @@ struct Adv {
 // _kernels.py:163-199 for one interior point.  (A warp-cooperative variant
 // that tests the remaining candidates of pending points on idle lanes was
 // measured slower on B200: the shuffles cost more than the divergence.)
-__device__ __forceinline__ Adv advect_one(const float *__restrict__ rho,
-                                          const float4 *__restrict__ gf, int nv, int nu,
+__device__ __forceinline__ Adv advect_one(const float *__restrict__ rho, const QuadField &qf,
+                                          bool quad, int nv, int nu,
                                           double xhi, double yhi, double2 p, double h,
                                           double eps, double min_step, int fixed) {
     Adv r{p, false, 0.0};
@@ -44,8 +44,8 @@ __device__ __forceinline__ Adv advect_one(const float *__restrict__ rho,
     // G = 2*gradient exactly, so |G| = 2*gn and G/|G| == g/gn bit for bit;
     // only the eps clamp (gn < eps <=> |G| < 2*eps) needs the scaled values
     double Gx, Gy, r0;
-    if (gf)
-        gradient2_value_gf(gf, nv, nu, x, y, Gx, Gy, r0);
+    if (quad)
+        gradient2_value_quad(qf, nv, nu, x, y, Gx, Gy, r0);
     else
         gradient2_value_ref(rho, nv, nu, x, y, Gx, Gy, r0);
     const double Gn = hypot_ref(Gx, Gy);
@@ -61,7 +61,8 @@ __device__ __forceinline__ Adv advect_one(const float *__restrict__ rho,
     while (fixed || m >= min_step) {
         const double nx = fmin_ref(fmax_ref(dadd(x, dmul(m, dx)), xlo), xhi);
         const double ny = fmin_ref(fmax_ref(dadd(y, dmul(m, dy)), ylo), yhi);
-        if (fixed || bilinear_ref(rho, nv, nu, nx, ny) >= r0) {
+        if (fixed ||
+            (quad ? bilinear_quad(qf.q, nv, nu, nx, ny) : bilinear_ref(rho, nv, nu, nx, ny)) >= r0) {
             r.p = make_double2(nx, ny);
             if (nx != x || ny != y) {
                 r.moved = true;
@@ -107,7 +108,10 @@ polyline_pass_kernel(const PolylinePass p) {
         const double2 *pin = p.pin + s;
         const int64_t lbase = do_adv ? (int64_t)p.edge_layer[e] * p.plane : 0;
         const float *rho = do_adv ? p.rho + lbase : nullptr;
-        const float4 *gf = (do_adv && p.gf) ? p.gf + lbase : nullptr;
+        const bool quad = do_adv && p.gf != nullptr;
+        const int64_t cells = (int64_t)p.plane * p.nbins_field;
+        QuadField qf{nullptr, nullptr, nullptr};
+        if (quad) qf = QuadField{p.gf + lbase, p.gf + cells + lbase, p.gf + 2 * cells + lbase};
 
         double2 cur = make_double2(0.0, 0.0);   // A(chunk c), lane = local index - c0
         double2 left = make_double2(0.0, 0.0);  // A(c0 - 1)
@@ -123,8 +127,8 @@ polyline_pass_kernel(const PolylinePass p) {
             if (jn + kWarp < n) raw = pin[jn + kWarp];
             if (jn < n) {
                 if (do_adv && jn > 0 && jn < n - 1) {
-                    const Adv a = advect_one(rho, gf, p.nv, p.nu, xhi, yhi, nxt, p.h, p.eps,
-                                             p.min_step, p.fixed);
+                    const Adv a = advect_one(rho, qf, quad, p.nv, p.nu, xhi, yhi, nxt, p.h,
+                                             p.eps, p.min_step, p.fixed);
                     my_moved += a.moved;
                     if (a.moved) my_disp = dadd(my_disp, a.disp);
                     nxt = a.p;
@@ -345,6 +349,7 @@ int hb_advect_laplacian(const double *pts_in, double *pts_out, const int64_t *st
     p.edge_layer = edge_layer;
     p.rho = rho;
     p.gf = reinterpret_cast<const float4 *>(grad_field);
+    p.nbins_field = nbins;
     p.plane = (int64_t)nv * nu;
     p.nv = nv;
     p.nu = nu;

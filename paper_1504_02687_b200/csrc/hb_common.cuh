@@ -173,28 +173,43 @@ __device__ __forceinline__ void gradient2_value_ref(const float *__restrict__ rh
     val = dadd(a, dmul(fy, dsub(b, a)));
 }
 
-// Same result from the packed per-cell field gf[v][u] = (rho, dX, dY, 0) with
-// dX = rho[v'][u'+1] - rho[v'][u'-1], dY = rho[v'+1][u'] - rho[v'-1][u'] at
-// the clamped (u', v') of _cell_gradient (float32 differences, exactly the
-// reference's): four 16-byte loads instead of twelve scattered 4-byte ones.
-__device__ __forceinline__ void gradient2_value_gf(const float4 *__restrict__ gf, int nv, int nu,
-                                                   double x, double y, double &Gx, double &Gy,
-                                                   double &val) {
+// Same results from the quad field (hb_grad_field): q = rho at the 2x2
+// corners of cell (u0, v0), qx/qy = the corners' float32 differences.
+struct QuadField {
+    const float4 *q, *gx, *gy;
+};
+
+__device__ __forceinline__ void gradient2_value_quad(const QuadField &f, int nv, int nu, double x,
+                                                     double y, double &Gx, double &Gy,
+                                                     double &val) {
     const int u0 = clampi(floor_i(x), 0, nu - 2);
     const int v0 = clampi(floor_i(y), 0, nv - 2);
     const double fx = dsub(x, (double)u0);
     const double fy = dsub(y, (double)v0);
-    const float4 *g = gf + v0 * nu + u0;
-    const float4 c00 = __ldg(g), c10 = __ldg(g + 1), c01 = __ldg(g + nu), c11 = __ldg(g + nu + 1);
-    const double ax = dadd((double)c00.y, dmul(fx, dsub((double)c10.y, (double)c00.y)));
-    const double bx = dadd((double)c01.y, dmul(fx, dsub((double)c11.y, (double)c01.y)));
-    const double ay = dadd((double)c00.z, dmul(fx, dsub((double)c10.z, (double)c00.z)));
-    const double by = dadd((double)c01.z, dmul(fx, dsub((double)c11.z, (double)c01.z)));
+    const int o = v0 * nu + u0;
+    const float4 q = __ldg(f.q + o), dx = __ldg(f.gx + o), dy = __ldg(f.gy + o);
+    // corners: .x (u0,v0)  .y (u0+1,v0)  .z (u0,v0+1)  .w (u0+1,v0+1)
+    const double ax = dadd((double)dx.x, dmul(fx, dsub((double)dx.y, (double)dx.x)));
+    const double bx = dadd((double)dx.z, dmul(fx, dsub((double)dx.w, (double)dx.z)));
+    const double ay = dadd((double)dy.x, dmul(fx, dsub((double)dy.y, (double)dy.x)));
+    const double by = dadd((double)dy.z, dmul(fx, dsub((double)dy.w, (double)dy.z)));
     Gx = dadd(ax, dmul(fy, dsub(bx, ax)));
     Gy = dadd(ay, dmul(fy, dsub(by, ay)));
-    const double a = lerp_f32diff(c00.x, c10.x, fx);
-    const double b = lerp_f32diff(c01.x, c11.x, fx);
+    const double a = lerp_f32diff(q.x, q.y, fx);
+    const double b = lerp_f32diff(q.z, q.w, fx);
     val = dadd(a, dmul(fy, dsub(b, a)));
+}
+
+__device__ __forceinline__ double bilinear_quad(const float4 *__restrict__ q, int nv, int nu,
+                                                double x, double y) {
+    const int u0 = clampi(floor_i(x), 0, nu - 2);
+    const int v0 = clampi(floor_i(y), 0, nv - 2);
+    const double fx = dsub(x, (double)u0);
+    const double fy = dsub(y, (double)v0);
+    const float4 c = __ldg(q + v0 * nu + u0);
+    const double a = lerp_f32diff(c.x, c.y, fx);
+    const double b = lerp_f32diff(c.z, c.w, fx);
+    return dadd(a, dmul(fy, dsub(b, a)));
 }
 
 // gradient_xy itself (bundler.gradient_at)
@@ -402,7 +417,8 @@ struct PolylinePass {
     int64_t n_edges = 0;
     const int32_t *edge_layer = nullptr;
     const float *rho = nullptr;
-    const float4 *gf = nullptr;  // packed (rho, dX, dY) field, optional
+    const float4 *gf = nullptr;  // quad field (hb_grad_field), optional
+    int nbins_field = 1;         // layers of the quad field (plane stride)
     int64_t plane = 0;
     int nv = 0, nu = 0;
     double h = -1.0, eps = 1e-8, min_step = 0.25;

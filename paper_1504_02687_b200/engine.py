@@ -189,8 +189,11 @@ class BundleEngine:
         hdtype = torch.float32 if self.wkind == "float" else torch.int32
         self.hist = torch.empty((B, self.nv, self.nu), dtype=hdtype, device=dev)
         self.field = torch.empty((B, self.nv, self.nu), dtype=torch.float32, device=dev)
-        # packed (rho, dX, dY) advection field (hb_grad_field), 16 B per cell
-        self.gfield = torch.empty((B, self.nv, self.nu, 4), dtype=torch.float32, device=dev)
+        # quad advection field (hb_grad_field), 48 B per cell: used while it
+        # stays L2-resident, otherwise the advection gathers from rho itself
+        quad_bytes = 48 * B * self.nv * self.nu
+        self.gfield = (torch.empty((3, B, self.nv, self.nu, 4), dtype=torch.float32, device=dev)
+                       if quad_bytes <= (100 << 20) else None)
         # resample count as its own launch after the advect pass (measured
         # faster than fusing it: the fused build's register footprint halves
         # the advect's occupancy)
@@ -381,7 +384,8 @@ class BundleEngine:
         h_i = cfg.lambda_ ** i * cfg.h_max  # bundler.py:360, Python float power
         # advect -> Laplacian (-> next iteration's resample count), in place
         last = i == self.iters - 1
-        self._k("hb_grad_field", ptr(self.field), B, nv, nu, ptr(self.gfield), s)
+        if self.gfield is not None:
+            self._k("hb_grad_field", ptr(self.field), B, nv, nu, ptr(self.gfield), s)
         fuse = not last and not self.split_count
         self._k("hb_advect_laplacian", ptr(self.pts), ptr(self.pts), ptr(self.starts), E,
                 self.n_pts, ptr(self.groups), ptr(self.field), ptr(self.gfield), B, nv, nu,

@@ -48,7 +48,13 @@ def shard_edges(point_counts: np.ndarray, world: int) -> list[tuple[int, int]]:
 
 
 def all_reduce_sum(t: torch.Tensor, group=None) -> torch.Tensor:
-    """In-place sum over ranks (NCCL int32 all-reduce on GPUs)."""
+    """In-place sum over ranks (NCCL int32 all-reduce on GPUs; device tensors
+    are staged through the host for a gloo group)."""
+    if t.is_cuda and dist.get_backend(group) != "nccl":
+        h = t.cpu()
+        dist.all_reduce(h, op=dist.ReduceOp.SUM, group=group)
+        t.copy_(h)
+        return t
     dist.all_reduce(t, op=dist.ReduceOp.SUM, group=group)
     return t
 

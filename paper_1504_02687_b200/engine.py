@@ -320,15 +320,25 @@ class BundleEngine:
 
     def step(self) -> IterationRecord:
         """One bundling iteration (bundler.py:351-376) on the device."""
+        self.step_splat()
+        if self.reduce_hist is not None:
+            self.reduce_hist(self.hist)
+        return self.step_field()
+
+    def step_splat(self) -> None:
+        """First half of an iteration: resample + histogram of this shard.
+
+        Between the two halves ``self.hist`` holds this shard's int32 group
+        counts; a multi-GPU run sums it over ranks (``reduce_hist``), and a
+        single-GPU shard emulation may sum several engines' histograms here."""
         i = self.iteration
         if i >= self.iters:
             raise RuntimeError("all iterations done")
-        cfg = self.cfg
         s = stream_ptr()
         E, B, nv, nu = self.n_edges, self.nbins, self.nv, self.nu
         ev0 = torch.cuda.Event(enable_timing=True)
-        ev1 = torch.cuda.Event(enable_timing=True)
         ev0.record()
+        self._ev_open = ev0
         self.hist.zero_()
         if i > 0:
             # resample (bundler.py:353-354): the counts/codes came out of the
@@ -374,8 +384,16 @@ class BundleEngine:
                 self._splat(s)
         else:
             self._splat(s)
-        if self.reduce_hist is not None:
-            self.reduce_hist(self.hist)
+
+    def step_field(self) -> IterationRecord:
+        """Second half: smoothing of the (global) histogram, advection,
+        Laplacian, next resample count, metrics."""
+        i = self.iteration
+        cfg = self.cfg
+        s = stream_ptr()
+        E, B, nv, nu = self.n_edges, self.nbins, self.nv, self.nu
+        ev0 = self._ev_open
+        ev1 = torch.cuda.Event(enable_timing=True)
         is_int = self.wkind != "float"
         self._k("hb_smooth", ptr(self.hist) if is_int else None,
                 None if is_int else ptr(self.hist), ptr(self.mat_dev), B, nv, nu,

@@ -251,27 +251,38 @@ def main():
     from paper_1504_02687_b200.engine import IO_BYTES
     from paper_1504_02687_b200.workloads import workload
 
-    torch.cuda.set_device(local)
+    # HB_BENCH_ONE_DEVICE=1 / HB_DIST_BACKEND=gloo: test-only switches that
+    # let the multi-rank code path run with every rank on cuda:0 (NCCL
+    # refuses two ranks on one GPU).  Bench numbers always use NCCL.
+    device_index = 0 if os.environ.get("HB_BENCH_ONE_DEVICE") == "1" else local
+    torch.cuda.set_device(device_index)
     group = None
     if world > 1:
         os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        backend = os.environ.get("HB_DIST_BACKEND", "nccl")
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", device_index))
+        else:
+            dist.init_process_group(backend)
 
     def barrier():
         if world > 1:
             dist.barrier()
 
+    def coll_device():
+        return "cuda" if dist.get_backend() == "nccl" else "cpu"
+
     def max_over_ranks(x: float) -> float:
         if world == 1:
             return x
-        t = torch.tensor([x], dtype=torch.float64, device="cuda")
+        t = torch.tensor([x], dtype=torch.float64, device=coll_device())
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         return float(t.item())
 
     def sum_over_ranks(x: int) -> int:
         if world == 1:
             return x
-        t = torch.tensor([x], dtype=torch.int64, device="cuda")
+        t = torch.tensor([x], dtype=torch.int64, device=coll_device())
         dist.all_reduce(t)
         return int(t.item())
 

@@ -34,23 +34,25 @@ class NativeError(RuntimeError):
     pass
 
 
-def build(verbose: bool = False) -> str:
-    """Compile csrc/*.cu into _lib/libhb_b200.so (cross-compiles without a GPU)."""
-    os.makedirs(LIB_DIR, exist_ok=True)
+def build(verbose: bool = False, out: str = LIB_PATH, defines: tuple = ()) -> str:
+    """Compile csrc/*.cu into _lib/libhb_b200.so (cross-compiles without a GPU).
+    ``out``/``defines`` build tuning variants for tools/ (``-DNAME=V``)."""
+    lib_dir = os.path.dirname(out)
+    os.makedirs(lib_dir, exist_ok=True)
     nvcc = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
     objs = []
     for src in SOURCES:
-        obj = os.path.join(LIB_DIR, src.replace(".cu", ".o"))
-        cmd = [nvcc, *NVCC_FLAGS, "-I", INCLUDE, "-c", os.path.join(CSRC, src), "-o", obj]
+        obj = os.path.join(lib_dir, src.replace(".cu", ".o"))
+        cmd = [nvcc, *NVCC_FLAGS, *defines, "-I", INCLUDE, "-c", os.path.join(CSRC, src), "-o", obj]
         if verbose:
             print(" ".join(cmd))
         subprocess.run(cmd, check=True)
         objs.append(obj)
-    tmp = LIB_PATH + ".tmp"
+    tmp = out + ".tmp"
     subprocess.run([nvcc, "-gencode", "arch=compute_100a,code=sm_100a", "-shared",
                     "--cudart=static", "-o", tmp, *objs], check=True)
-    os.replace(tmp, LIB_PATH)
-    return LIB_PATH
+    os.replace(tmp, out)
+    return out
 
 
 _P, _I64, _I, _D, _SZ = (ctypes.c_void_p, ctypes.c_int64, ctypes.c_int,
@@ -106,8 +108,10 @@ class HbTiles(ctypes.Structure):
 _lib = None
 
 
-def load_library(path: str = LIB_PATH):
-    """dlopen the library and bind every declared symbol (no device needed)."""
+def load_library(path: str | None = None):
+    """dlopen the library and bind every declared symbol (no device needed).
+    ``HB_B200_LIB`` points tools at a tuning variant built by ``build(out=...)``."""
+    path = path or os.environ.get("HB_B200_LIB") or LIB_PATH
     global _lib
     if _lib is not None:
         return _lib

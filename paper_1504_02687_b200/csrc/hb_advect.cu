@@ -33,14 +33,18 @@ struct Adv {
 
 // _kernels.py:163-199 for one interior point.  (A warp-cooperative variant
 // that tests the remaining candidates of pending points on idle lanes was
-// measured slower on B200: the shuffles cost more than the divergence.)
+// measured slower on B200: the shuffles cost more than the divergence; so
+// was gathering two or three step candidates at once -- the kernel is
+// issue-bound, not latency-bound.)
+template <bool quad>
 __device__ __forceinline__ Adv advect_one(const float *__restrict__ rho, const QuadField &qf,
-                                          bool quad, int nv, int nu,
+                                          int nv, int nu,
                                           double xhi, double yhi, double2 p, double h,
                                           double eps, double min_step, int fixed) {
     Adv r{p, false, 0.0};
     const double x = p.x, y = p.y;
     const double xlo = 1.0, ylo = 1.0;  // INTERIOR_MARGIN (_kernels.py:19)
+    const bool inner_grid = nu >= 3 && nv >= 3;
     // G = 2*gradient exactly, so |G| = 2*gn and G/|G| == g/gn bit for bit;
     // only the eps clamp (gn < eps <=> |G| < 2*eps) needs the scaled values
     double Gx, Gy, r0;
@@ -59,10 +63,14 @@ __device__ __forceinline__ Adv advect_one(const float *__restrict__ rho, const Q
     }
     double m = h;
     while (fixed || m >= min_step) {
-        const double nx = fmin_ref(fmax_ref(dadd(x, dmul(m, dx)), xlo), xhi);
-        const double ny = fmin_ref(fmax_ref(dadd(y, dmul(m, dy)), ylo), yhi);
+        const double nx = clamp_ref(dadd(x, dmul(m, dx)), xlo, xhi);
+        const double ny = clamp_ref(dadd(y, dmul(m, dy)), ylo, yhi);
+        // xhi = nu-2, yhi = nv-2: with nu, nv >= 3 the candidate's cell needs
+        // no further clamp (inner_grid is warp-uniform)
         if (fixed ||
-            (quad ? bilinear_quad(qf.q, nv, nu, nx, ny) : bilinear_ref(rho, nv, nu, nx, ny)) >= r0) {
+            (quad ? (inner_grid ? bilinear_quad<true>(qf.q, nv, nu, nx, ny)
+                                : bilinear_quad(qf.q, nv, nu, nx, ny))
+                  : bilinear_ref(rho, nv, nu, nx, ny)) >= r0) {
             r.p = make_double2(nx, ny);
             if (nx != x || ny != y) {
                 r.moved = true;
@@ -75,11 +83,15 @@ __device__ __forceinline__ Adv advect_one(const float *__restrict__ rho, const Q
     return r;
 }
 
-// One instantiation per stage combination, so each launch carries only the
-// registers its stages need (a fused advect+count build measured slower than
-// advect and count as two launches: the count's state cut occupancy).
-template <bool ADV, bool LAP, bool COUNT>
-__global__ void __launch_bounds__(kStreamBlock, (ADV && COUNT) ? 3 : 4)
+#ifndef HB_ADV_MINB
+#define HB_ADV_MINB 4
+#endif
+#ifndef HB_CNT_MINB
+#define HB_CNT_MINB 4
+#endif
+
+template <bool ADV, bool LAP, bool COUNT, bool QUAD>
+__global__ void __launch_bounds__(kStreamBlock, (ADV && COUNT) ? 3 : (ADV ? HB_ADV_MINB : (COUNT ? HB_CNT_MINB : 4)))
 polyline_pass_kernel(const PolylinePass p) {
     const unsigned full = 0xffffffffu;
     const int lane = threadIdx.x & 31;
@@ -94,6 +106,7 @@ polyline_pass_kernel(const PolylinePass p) {
     const int64_t nwarps = (int64_t)gridDim.x * (kStreamBlock / 32);
     unsigned my_moved = 0;
     double my_disp = 0.0;
+    __shared__ double2 s_row[COUNT ? kStreamBlock : 1];
 
     int64_t e = ((int64_t)blockIdx.x * kStreamBlock + threadIdx.x) / 32;
     // the next edge's bounds are fetched one edge ahead and every chunk's raw
@@ -108,7 +121,7 @@ polyline_pass_kernel(const PolylinePass p) {
         const double2 *pin = p.pin + s;
         const int64_t lbase = do_adv ? (int64_t)p.edge_layer[e] * p.plane : 0;
         const float *rho = do_adv ? p.rho + lbase : nullptr;
-        const bool quad = do_adv && p.gf != nullptr;
+        constexpr bool quad = ADV && QUAD;
         const int64_t cells = (int64_t)p.plane * p.nbins_field;
         QuadField qf{nullptr, nullptr, nullptr};
         if (quad) qf = QuadField{p.gf + lbase, p.gf + cells + lbase, p.gf + 2 * cells + lbase};
@@ -127,7 +140,7 @@ polyline_pass_kernel(const PolylinePass p) {
             if (jn + kWarp < n) raw = pin[jn + kWarp];
             if (jn < n) {
                 if (do_adv && jn > 0 && jn < n - 1) {
-                    const Adv a = advect_one(rho, qf, quad, p.nv, p.nu, xhi, yhi, nxt, p.h,
+                    const Adv a = advect_one<quad>(rho, qf, p.nv, p.nu, xhi, yhi, nxt, p.h,
                                              p.eps, p.min_step, p.fixed);
                     my_moved += a.moved;
                     if (a.moved) my_disp = dadd(my_disp, a.disp);
@@ -146,7 +159,7 @@ polyline_pass_kernel(const PolylinePass p) {
             const int j = c0 + lane;
             const bool valid = j < n;
             double2 f = cur;
-            if (LAP) {
+            if constexpr (LAP) {
                 double lx = __shfl_up_sync(full, cur.x, 1), ly = __shfl_up_sync(full, cur.y, 1);
                 double rx = __shfl_down_sync(full, cur.x, 1), ry = __shfl_down_sync(full, cur.y, 1);
                 const double n0x = __shfl_sync(full, nxt.x, 0), n0y = __shfl_sync(full, nxt.y, 0);
@@ -158,26 +171,35 @@ polyline_pass_kernel(const PolylinePass p) {
                     f = make_double2(dadd(cur.x, dmul(p.factor, dsub(mx, cur.x))),
                                      dadd(cur.y, dmul(p.factor, dsub(my, cur.y))));
                 }
+                left.x = __shfl_sync(full, cur.x, 31);
+                left.y = __shfl_sync(full, cur.y, 31);
             }
             if (p.pout && valid) p.pout[s + j] = f;
 
-            if (do_count) {
-                double qx = __shfl_up_sync(full, f.x, 1), qy = __shfl_up_sync(full, f.y, 1);
-                if (lane == 0) { qx = prevf.x; qy = prevf.y; }
+            if constexpr (COUNT) {
+                // the chunk's final points in a per-warp shared row: every
+                // anchor broadcast below is one LDS.128 instead of 4 SHFL
+                double2 *row = s_row + (threadIdx.x & ~31);
+                __syncwarp();
+                row[lane] = f;
+                __syncwarp();
+                const double2 q = lane ? row[lane - 1] : prevf;  // predecessor
                 const bool part = valid && j > 0;  // local point 0 is always kept at 0
                 // squared gaps; g < lo <=> g2 < lo2 exactly (see sqrt_lt_bound).
                 // (A bit-parallel resolution of isolated merges was measured
                 // slower: in bundles merges come in long chains.)
-                const double gs = part ? dist2_ref(f.x, f.y, qx, qy) : 0.0;
+                const double gs = part ? dist2_ref(f.x, f.y, q.x, q.y) : 0.0;
                 const bool last = (j == n - 1);
                 bool kept = false;
                 double gk = 0.0;
                 int start = (c0 == 0) ? 1 : 0;
+                // Round 1: lane `start` measures against the carried anchor
+                // `ka`.  Later rounds start right after a kept lane c, so
+                // ka == f[start-1] and the speculative gap gs is already the
+                // true one (same operands, same rounding).
+                double geff = (lane == start && part) ? dist2_ref(f.x, f.y, ka.x, ka.y) : gs;
                 while (start < kWarp) {
-                    // speculate: every lane's predecessor is kept (lane
-                    // `start` measures against the anchor `ka`)
-                    double geff = gs;
-                    if (lane == start && part) geff = dist2_ref(f.x, f.y, ka.x, ka.y);
+                    // speculate: every lane's predecessor is kept
                     const bool act = part && lane >= start;
                     const unsigned m = __ballot_sync(full, act && !last && geff < lo2);
                     if (m == 0) {
@@ -186,11 +208,7 @@ polyline_pass_kernel(const PolylinePass p) {
                     }
                     const int b = __ffs(m) - 1;  // first merged lane
                     if (act && lane < b) { kept = true; gk = geff; }
-                    // b and start are warp-uniform; shuffle unconditionally so
-                    // the compiler needs no collective fix-up code
-                    const double kx = __shfl_sync(full, f.x, b > 0 ? b - 1 : 0);
-                    const double ky = __shfl_sync(full, f.y, b > 0 ? b - 1 : 0);
-                    if (b > start) { ka.x = kx; ka.y = ky; }
+                    if (b > start) ka = row[b - 1];
                     // resolve the whole merge chain at once: every later lane
                     // measures against the same anchor; the first one at
                     // >= lo (or the polyline's last point) is kept
@@ -200,36 +218,37 @@ polyline_pass_kernel(const PolylinePass p) {
                     if (mc == 0) break;  // chain runs past this chunk; anchor carries
                     const int c = __ffs(mc) - 1;
                     if (lane == c) { kept = true; gk = ga; }
-                    ka.x = __shfl_sync(full, f.x, c);
-                    ka.y = __shfl_sync(full, f.y, c);
+                    ka = row[c];
                     start = c + 1;
+                    geff = gs;
                 }
-                int pieces = 0;
-                if (kept) {
-                    // while (g > hi) { g *= 0.5; pieces *= 2; }  on squared gaps:
-                    // g * 2^-k > hi  <=>  g2 > 4^k * hi2 (exact power-of-two scaling)
-                    double t = hi2;
-                    pieces = 1;
-                    while (gk > t) { t = dmul(t, 4.0); pieces *= 2; }
-                }
-                int incl = pieces;
+                // while (g > hi) { g *= 0.5; pieces *= 2; }  on squared gaps:
+                // g * 2^-k > hi  <=>  g2 > 4^k * hi2 (exact power-of-two scaling)
+                int pieces = kept ? 1 : 0;
+                const unsigned km = __ballot_sync(full, kept);
+                int incl, total;
+                if (!__any_sync(full, kept && gk > hi2)) {
+                    // every kept point is one piece: the prefix sum is a popcount
+                    incl = __popc(km & (0xffffffffu >> (31 - lane)));
+                    total = __popc(km);
+                } else {
+                    if (kept) {
+                        double t = hi2;
+                        while (gk > t) { t = dmul(t, 4.0); pieces *= 2; }
+                    }
+                    incl = pieces;
 #pragma unroll
-                for (int d = 1; d < kWarp; d <<= 1) {
-                    const int t = __shfl_up_sync(full, incl, d);
-                    if (lane >= d) incl += t;
+                    for (int d = 1; d < kWarp; d <<= 1) {
+                        const int t = __shfl_up_sync(full, incl, d);
+                        if (lane >= d) incl += t;
+                    }
+                    total = __shfl_sync(full, incl, 31);
                 }
                 if (part) p.pos[s + j] = kept ? off + incl : -1;
-                const unsigned km = __ballot_sync(full, kept);
-                const int lk = km ? 31 - __clz(km) : 0;
-                const double kx2 = __shfl_sync(full, f.x, lk);
-                const double ky2 = __shfl_sync(full, f.y, lk);
-                if (km) { ka.x = kx2; ka.y = ky2; }
-                off += __shfl_sync(full, incl, 31);
-                prevf.x = __shfl_sync(full, f.x, 31);
-                prevf.y = __shfl_sync(full, f.y, 31);
+                if (km) ka = row[31 - __clz(km)];
+                off += total;
+                prevf = row[31];
             }
-            left.x = __shfl_sync(full, cur.x, 31);
-            left.y = __shfl_sync(full, cur.y, 31);
             cur = nxt;
         }
         if (do_count && lane == 0) p.counts[e] = (int64_t)off + 1;
@@ -263,11 +282,19 @@ polyline_pass_kernel(const PolylinePass p) {
 
 template <bool ADV, bool LAP, bool COUNT>
 static int launch_variant(const PolylinePass &p, cudaStream_t st, const char *what) {
-    const unsigned grid = persistent_grid(polyline_pass_kernel<ADV, LAP, COUNT>, p.n_edges);
     if (p.partials &&
         cudaMemsetAsync(p.partials, 0, sizeof(double) * kMaxStreamBlocks, st) != cudaSuccess)
         return check_launch(what, 0);
-    polyline_pass_kernel<ADV, LAP, COUNT><<<grid, kStreamBlock, 0, st>>>(p);
+    if constexpr (ADV) {
+        if (p.gf != nullptr) {  // quad advection field (hb_grad_field)
+            const unsigned grid =
+                persistent_grid(polyline_pass_kernel<ADV, LAP, COUNT, true>, p.n_edges);
+            polyline_pass_kernel<ADV, LAP, COUNT, true><<<grid, kStreamBlock, 0, st>>>(p);
+            return check_launch(what);
+        }
+    }
+    const unsigned grid = persistent_grid(polyline_pass_kernel<ADV, LAP, COUNT, false>, p.n_edges);
+    polyline_pass_kernel<ADV, LAP, COUNT, false><<<grid, kStreamBlock, 0, st>>>(p);
     return check_launch(what);
 }
 

@@ -47,10 +47,13 @@ __device__ __forceinline__ double hypot_ref(double ax, double ay) {
     return sqrt(dadd(dmul(ax, ax), dmul(ay, ay)));
 }
 
-// numba min/max.  Operands here are never NaN and the clamp bounds are >= 1,
-// so the hardware min/max (DMNMX) returns exactly what `a < b ? a : b` does.
-__device__ __forceinline__ double fmin_ref(double a, double b) { return fmin(a, b); }
-__device__ __forceinline__ double fmax_ref(double a, double b) { return fmax(a, b); }
+// numba min(max(v, lo), hi) (_kernels.py:180-181).  v is never NaN and
+// lo >= 1 > 0, so no signed zero can tie: the compare-select below returns
+// the same double bit for bit, and compiles to 2 DSETP + 4 SEL where
+// fmin/fmax carry NaN fix-ups (~12 instructions).
+__device__ __forceinline__ double clamp_ref(double v, double lo, double hi) {
+    return v < lo ? lo : (v > hi ? hi : v);
+}
 
 // Exact sqrt-free comparisons.  sqrt() is correctly rounded and monotone, so
 //   sqrt(d) <  lo  <=>  d <  sqrt_lt_bound(lo)   (smallest d with sqrt(d) >= lo)
@@ -200,10 +203,13 @@ __device__ __forceinline__ void gradient2_value_quad(const QuadField &f, int nv,
     val = dadd(a, dmul(fy, dsub(b, a)));
 }
 
+// `inner`: the caller guarantees 1 <= x <= nu-2 and 1 <= y <= nv-2 (a
+// clamped advection candidate), so floor() already lies in the clamp range.
+template <bool inner = false>
 __device__ __forceinline__ double bilinear_quad(const float4 *__restrict__ q, int nv, int nu,
                                                 double x, double y) {
-    const int u0 = clampi(floor_i(x), 0, nu - 2);
-    const int v0 = clampi(floor_i(y), 0, nv - 2);
+    const int u0 = inner ? floor_i(x) : clampi(floor_i(x), 0, nu - 2);
+    const int v0 = inner ? floor_i(y) : clampi(floor_i(y), 0, nv - 2);
     const double fx = dsub(x, (double)u0);
     const double fy = dsub(y, (double)v0);
     const float4 c = __ldg(q + v0 * nu + u0);

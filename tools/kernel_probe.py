@@ -53,13 +53,20 @@ def main():
     s = stream_ptr()
     E, Bn, nv, nu = eng.n_edges, eng.nbins, eng.nv, eng.nu
     # state: eng.pts holds final points of iteration iters-1, ecounts/pos valid
+    # the real count input: final (advected + smoothed) points of iteration iters-1
+    cnt_tmp = torch.empty_like(eng.ecounts)
+    pos_tmp = torch.empty_like(eng.pos)
+    out_count = timed(lambda: N.call(
+        "hb_resample_count", ptr(eng.pts), ptr(eng.starts), E, float(w.config.delta),
+        ptr(cnt_tmp), ptr(pos_tmp), s))
+    del cnt_tmp, pos_tmp
     N.call("hb_scan_counts", ptr(eng.ecounts), E, ptr(eng.starts_alt), ptr(eng.scan_ws),
            eng.scan_ws.numel(), s)
     n_new = int(eng.starts_alt[E].item())
     eng._ensure_capacity(n_new)
     n_old = eng.n_pts
     out = {"config": w.name, "iteration_state": args.iters, "n_old": n_old, "n_new": n_new,
-           "edges": E}
+           "edges": E, "count_final_ms": out_count}
 
     def emit(splat: bool):
         if splat:

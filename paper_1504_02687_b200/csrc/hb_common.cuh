@@ -344,9 +344,12 @@ __device__ __forceinline__ void bin_or_splat(bool has, double px0, double py0, d
                        (unsigned)(x0 + dx) < (unsigned)nu && (unsigned)(y0 + dy) < (unsigned)nv) {
                 // delta-major key (a cell-major layout was measured slower: it
                 // packs a hot cell's atomics into a few L2 slices)
-                const int D = 2 * H + 1;
-                const int64_t dir = (int64_t)grp * D * D + (dy + H) * D + (dx + H);
-                atomicAdd(tl->tab + (dir * nv + y0) * nu + x0, (unsigned)iw);
+                // (hb_segtab_geometry keeps the table below 2^31 entries,
+                // so the index fits 32-bit arithmetic)
+                const unsigned D = 2 * H + 1;
+                const unsigned dir = (unsigned)grp * D * D + (unsigned)((dy + H) * D + (dx + H));
+                atomicAdd(tl->tab + ((dir * (unsigned)nv + (unsigned)y0) * (unsigned)nu + (unsigned)x0),
+                          (unsigned)iw);
                 direct = false;
             }
         }

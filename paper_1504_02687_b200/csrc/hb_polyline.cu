@@ -171,9 +171,10 @@ splat_kernel(const double2 *__restrict__ pts, const int64_t *__restrict__ starts
 __device__ __forceinline__ double2 interp_piece(double2 a, double2 x, int k, int pieces) {
     if (k == pieces) return x;
     if (k == 0) return a;
-    // t = k / pieces (_kernels.py:264); pieces is a power of two, so the
-    // quotient is exact and equals k times the exact reciprocal
-    const double t = dmul((double)k, __drcp_rn((double)pieces));
+    // t = k / pieces (_kernels.py:264); pieces = 2^s is a power of two, so
+    // the quotient is exact and equals k * 2^-s (built from the exponent)
+    const int sh = __ffs(pieces) - 1;
+    const double t = dmul((double)k, __longlong_as_double((long long)(1023 - sh) << 52));
     return make_double2(dadd(a.x, dmul(t, dsub(x.x, a.x))), dadd(a.y, dmul(t, dsub(x.y, a.y))));
 }
 

@@ -278,6 +278,8 @@ int hb_segtab_geometry(int nbins, int nv, int nu, double max_seg_cells, hb_tiles
     *entries = (int64_t)nbins * D * D * nv * nu;
     // whole uint4 loads in the expansion
     *entries = (*entries + 3) / 4 * 4;
+    if (*entries >= ((int64_t)1 << 31))  // keys are 32-bit indices (bin_or_splat)
+        return set_error(HB_EINVAL, "hb_segtab_geometry: key table above 2^31 entries");
     return HB_OK;
 }
 

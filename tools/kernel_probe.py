@@ -59,14 +59,38 @@ def main():
     out_count = timed(lambda: N.call(
         "hb_resample_count", ptr(eng.pts), ptr(eng.starts), E, float(w.config.delta),
         ptr(cnt_tmp), ptr(pos_tmp), s))
-    del cnt_tmp, pos_tmp
+    # resample shape of the real state: pieces per kept point, chunk classes
+    pos_i = pos_tmp[:eng.n_pts].long()
+    st = eng.starts[:E + 1].long()
+    kept = pos_i >= 0
+    kp = torch.nonzero(kept).squeeze(1)
+    pv = pos_i[kp]
+    edge_of = torch.searchsorted(st, kp, right=True) - 1
+    same = edge_of[1:] == edge_of[:-1]
+    pieces = (pv[1:] - pv[:-1])[same]
+    hist = torch.bincount(pieces.clamp_max(64)).cpu().tolist()
+    tot = max(1, int(pieces.numel()))
+    local = kp - st[edge_of]
+    chunk_id = edge_of * 4096 + local // 32  # (edge, chunk) key, edges < 2^31/4096 chunks ok
+    multi = torch.unique(chunk_id[1:][same & ((pv[1:] - pv[:-1]) != 1)])
+    allp = torch.arange(eng.n_pts, device=pos_i.device)
+    e_all = torch.searchsorted(st, allp, right=True) - 1
+    ck_all = e_all * 4096 + (allp - st[e_all]) // 32
+    dropped = torch.unique(ck_all[~kept])
+    merged_chunks = int(torch.unique(torch.cat([multi, dropped])).numel())
+    n_chunks = int(((st[1:] - st[:-1] + 31) // 32).sum().item())
+    del allp, e_all, ck_all
+    out_stats = {"pieces_hist_frac": {i: round(c / tot, 5) for i, c in enumerate(hist) if c},
+                 "kept_frac": float(kept.float().mean().item()),
+                 "complex_chunk_frac": merged_chunks / max(1, n_chunks)}
+    del cnt_tmp, pos_tmp, pos_i, kp, pv, edge_of, pieces, local, chunk_id
     N.call("hb_scan_counts", ptr(eng.ecounts), E, ptr(eng.starts_alt), ptr(eng.scan_ws),
            eng.scan_ws.numel(), s)
     n_new = int(eng.starts_alt[E].item())
     eng._ensure_capacity(n_new)
     n_old = eng.n_pts
     out = {"config": w.name, "iteration_state": args.iters, "n_old": n_old, "n_new": n_new,
-           "edges": E, "count_final_ms": out_count}
+           "edges": E, "count_final_ms": out_count, "resample_shape": out_stats}
 
     def emit(splat: bool):
         if splat:

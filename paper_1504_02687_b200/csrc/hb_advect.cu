@@ -68,8 +68,8 @@ __device__ __forceinline__ Adv advect_one(const float *__restrict__ rho, const Q
         // xhi = nu-2, yhi = nv-2: with nu, nv >= 3 the candidate's cell needs
         // no further clamp (inner_grid is warp-uniform)
         if (fixed ||
-            (quad ? (inner_grid ? bilinear_quad<true>(qf.q, nv, nu, nx, ny)
-                                : bilinear_quad(qf.q, nv, nu, nx, ny))
+            (quad ? (inner_grid ? bilinear_quad<true>(qf.q, qf.base, nv, nu, nx, ny)
+                                : bilinear_quad(qf.q, qf.base, nv, nu, nx, ny))
                   : bilinear_ref(rho, nv, nu, nx, ny)) >= r0) {
             r.p = make_double2(nx, ny);
             if (nx != x || ny != y) {
@@ -100,9 +100,8 @@ polyline_pass_kernel(const PolylinePass p) {
     const double lo = 0.5 * p.delta, hi = 1.5 * p.delta;  // _kernels.py:211-212
     const double lo2 = do_count ? sqrt_lt_bound(lo) : 0.0;
     const double hi2 = do_count ? sqrt_gt_bound(hi) : 0.0;
-    // xhi = nu - 1 - INTERIOR_MARGIN (_kernels.py:158-159)
-    const double xhi = dsub(dsub((double)p.nu, 1.0), 1.0);
-    const double yhi = dsub(dsub((double)p.nv, 1.0), 1.0);
+    // xhi = nu - 1 - INTERIOR_MARGIN (_kernels.py:158-159), set by the host
+    const double xhi = p.xhi, yhi = p.yhi;
     const int64_t nwarps = (int64_t)gridDim.x * (kStreamBlock / 32);
     unsigned my_moved = 0;
     double my_disp = 0.0;
@@ -123,8 +122,8 @@ polyline_pass_kernel(const PolylinePass p) {
         const float *rho = do_adv ? p.rho + lbase : nullptr;
         constexpr bool quad = ADV && QUAD;
         const int64_t cells = (int64_t)p.plane * p.nbins_field;
-        QuadField qf{nullptr, nullptr, nullptr};
-        if (quad) qf = QuadField{p.gf + lbase, p.gf + cells + lbase, p.gf + 2 * cells + lbase};
+        QuadField qf{nullptr, nullptr, nullptr, 0u};
+        if (quad) qf = QuadField{p.gf, p.gf + cells, p.gf + 2 * cells, (unsigned)lbase};
 
         double2 cur = make_double2(0.0, 0.0);   // A(chunk c), lane = local index - c0
         double2 left = make_double2(0.0, 0.0);  // A(c0 - 1)
@@ -366,6 +365,8 @@ int hb_advect_laplacian(const double *pts_in, double *pts_out, const int64_t *st
         (counts && (!pos || !(delta > 0))) ||
         (n_pts > 0 && (!pts_in || !pts_out || !starts)))
         return set_error(HB_EINVAL, "hb_advect_laplacian: bad arguments");
+    if (adv && grad_field && (int64_t)nbins * nv * nu >= ((int64_t)1 << 31))
+        return set_error(HB_EINVAL, "hb_advect_laplacian: quad field above 2^31 cells");
     if (n_pts == 0 || n_edges == 0) return HB_OK;
     cudaStream_t st = as_stream(stream);
     PolylinePass p{};
@@ -380,6 +381,8 @@ int hb_advect_laplacian(const double *pts_in, double *pts_out, const int64_t *st
     p.plane = (int64_t)nv * nu;
     p.nv = nv;
     p.nu = nu;
+    p.xhi = (double)(nu - 2);  // == (nu - 1.0) - 1.0 exactly
+    p.yhi = (double)(nv - 2);
     p.h = adv ? h : -1.0;
     p.eps = eps;
     p.min_step = min_step;

@@ -178,8 +178,12 @@ __device__ __forceinline__ void gradient2_value_ref(const float *__restrict__ rh
 
 // Same results from the quad field (hb_grad_field): q = rho at the 2x2
 // corners of cell (u0, v0), qx/qy = the corners' float32 differences.
+// q/gx/gy point at the WHOLE field (all layers); `base` is the layer's first
+// cell.  Offsets are 32-bit (hb_advect_laplacian checks layers*V*U < 2^31),
+// which keeps the per-sample address math to a few integer ops.
 struct QuadField {
     const float4 *q, *gx, *gy;
+    unsigned base;
 };
 
 __device__ __forceinline__ void gradient2_value_quad(const QuadField &f, int nv, int nu, double x,
@@ -189,7 +193,7 @@ __device__ __forceinline__ void gradient2_value_quad(const QuadField &f, int nv,
     const int v0 = clampi(floor_i(y), 0, nv - 2);
     const double fx = dsub(x, (double)u0);
     const double fy = dsub(y, (double)v0);
-    const int o = v0 * nu + u0;
+    const unsigned o = f.base + (unsigned)(v0 * nu + u0);
     const float4 q = __ldg(f.q + o), dx = __ldg(f.gx + o), dy = __ldg(f.gy + o);
     // corners: .x (u0,v0)  .y (u0+1,v0)  .z (u0,v0+1)  .w (u0+1,v0+1)
     const double ax = dadd((double)dx.x, dmul(fx, dsub((double)dx.y, (double)dx.x)));
@@ -206,13 +210,13 @@ __device__ __forceinline__ void gradient2_value_quad(const QuadField &f, int nv,
 // `inner`: the caller guarantees 1 <= x <= nu-2 and 1 <= y <= nv-2 (a
 // clamped advection candidate), so floor() already lies in the clamp range.
 template <bool inner = false>
-__device__ __forceinline__ double bilinear_quad(const float4 *__restrict__ q, int nv, int nu,
-                                                double x, double y) {
+__device__ __forceinline__ double bilinear_quad(const float4 *__restrict__ q, unsigned base,
+                                                int nv, int nu, double x, double y) {
     const int u0 = inner ? floor_i(x) : clampi(floor_i(x), 0, nu - 2);
     const int v0 = inner ? floor_i(y) : clampi(floor_i(y), 0, nv - 2);
     const double fx = dsub(x, (double)u0);
     const double fy = dsub(y, (double)v0);
-    const float4 c = __ldg(q + v0 * nu + u0);
+    const float4 c = __ldg(q + (base + (unsigned)(v0 * nu + u0)));
     const double a = lerp_f32diff(c.x, c.y, fx);
     const double b = lerp_f32diff(c.z, c.w, fx);
     return dadd(a, dmul(fy, dsub(b, a)));
@@ -430,6 +434,7 @@ struct PolylinePass {
     int nbins_field = 1;         // layers of the quad field (plane stride)
     int64_t plane = 0;
     int nv = 0, nu = 0;
+    double xhi = 0.0, yhi = 0.0;  // nu - 1 - INTERIOR_MARGIN, nv - 1 - ... (exact)
     double h = -1.0, eps = 1e-8, min_step = 0.25;
     int fixed = 0;
     double factor = 0.5;

@@ -178,6 +178,16 @@ __device__ __forceinline__ double2 interp_piece(double2 a, double2 x, int k, int
     return make_double2(dadd(a.x, dmul(t, dsub(x.x, a.x))), dadd(a.y, dmul(t, dsub(x.y, a.y))));
 }
 
+// Streaming point traffic is marked evict-first so the segment-key table's
+// lines (hit by ~1 atomic per segment) stay resident in L2.
+#ifndef HB_NO_STREAM_HINTS
+#define HB_LD_STREAM(p) __ldcs(p)
+#define HB_ST_STREAM(p, v) __stcs((p), (v))
+#else
+#define HB_LD_STREAM(p) (*(p))
+#define HB_ST_STREAM(p, v) (*(p) = (v))
+#endif
+
 __global__ void __launch_bounds__(kStreamBlock, 3)
 emit_kernel(const double2 *__restrict__ pts, const int64_t *__restrict__ starts,
             int64_t n_edges, const int32_t *__restrict__ pos,
@@ -206,8 +216,8 @@ emit_kernel(const double2 *__restrict__ pts, const int64_t *__restrict__ starts,
         // carry: last kept point so far and its output index (none yet)
         double2 a = make_double2(0.0, 0.0);
         int apos = -1;
-        int pj_nx = lane < n ? pos[s + lane] : -1;
-        double2 x_nx = lane < n ? pts[s + lane] : make_double2(0.0, 0.0);
+        int pj_nx = lane < n ? HB_LD_STREAM(pos + s + lane) : -1;
+        double2 x_nx = lane < n ? HB_LD_STREAM(pts + s + lane) : make_double2(0.0, 0.0);
         for (int c0 = 0; c0 < n; c0 += kWarp) {
             // local point 0 has pos 0: it is output 0 and the first `a`
             const int j = c0 + lane;
@@ -215,8 +225,8 @@ emit_kernel(const double2 *__restrict__ pts, const int64_t *__restrict__ starts,
             const int pj = pj_nx;
             const double2 x = x_nx;
             if (j + kWarp < n) {
-                pj_nx = pos[s + j + kWarp];
-                x_nx = pts[s + j + kWarp];
+                pj_nx = HB_LD_STREAM(pos + s + j + kWarp);
+                x_nx = HB_LD_STREAM(pts + s + j + kWarp);
             } else {
                 pj_nx = -1;  // past the end of the edge
             }
@@ -236,7 +246,7 @@ emit_kernel(const double2 *__restrict__ pts, const int64_t *__restrict__ starts,
             const bool simple = __all_sync(full, !valid || (kept && pj - pa == 1));
             if (simple) {
                 // every valid lane is kept with one piece: output pj is x itself
-                if (valid) o[pj] = x;
+                if (valid) HB_ST_STREAM(o + pj, x);
                 if (splat)
                     bin_or_splat<int32_t>(valid && pj >= 1, pa2.x, pa2.y, x.x, x.y,
                                           pj == 1 ? 0 : 1, w, grp, hist, plane, nv, nu, status,
@@ -265,7 +275,7 @@ emit_kernel(const double2 *__restrict__ pts, const int64_t *__restrict__ starts,
                         const double2 ox2 = make_double2(ox, oy), oa2 = make_double2(oax, oay);
                         q = interp_piece(oa2, ox2, k, pieces);
                         q0 = interp_piece(oa2, ox2, k - 1, pieces);
-                        o[m] = q;
+                        HB_ST_STREAM(o + m, q);
                     }
                     if (splat)
                         bin_or_splat<int32_t>(here && m >= 1, q0.x, q0.y, q.x, q.y,

@@ -122,7 +122,9 @@ class ClockSampler:
 
 def algorithmic_bytes(name: str, n_prev: int, n_cur: int, n_edges: int, cells: int,
                       passes: int, nbins: int) -> int:
-    if name == "hb_advect_laplacian":
+    if name == "hb_advect_points":      # advect: read + write every point
+        return 32 * n_cur + 8 * n_edges + 4 * cells
+    if name == "hb_advect_laplacian":   # Laplacian (+ fused next resample count)
         return 32 * n_cur + 16 * n_edges + 4 * cells
     if name == "hb_resample_emit":      # resample emit + fused splat
         return 16 * n_prev + 16 * n_cur + 40 * n_edges + 4 * cells

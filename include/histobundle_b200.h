@@ -204,6 +204,22 @@ HB_API int hb_grad_field(const float *rho, int nbins, int nv, int nu, float *out
 /* Size (doubles) of the disp_partials buffer hb_advect_laplacian fills. */
 HB_API int64_t hb_advect_partials(void);
 
+/* _kernels.advect (_kernels.py:144-200) alone, in place: every interior
+ * point of every polyline (endpoints are found from starts) moves to the
+ * first step candidate m = h, h/2, ... >= min_step whose bilinear density is
+ * >= its own (fixed_step: m = h, always taken).  Points are processed as one
+ * flat stream (bit-identical positions to the per-edge form; see
+ * hb_advect_flat.cu).  grad_field: nullable hb_grad_field(rho).  Requires
+ * nv, nu >= 3 and nbins*nv*nu < 2^31.  moved: u64 accumulator (added to);
+ * disp_partials: hb_advect_partials() doubles (zeroed and filled here),
+ * summed by hb_reduce_f64.  Follow with hb_advect_laplacian(h < 0) for the
+ * Laplacian (and the fused resample count). */
+HB_API int hb_advect_points(double *pts, const int64_t *starts, int64_t n_edges,
+                            int64_t n_pts, const int32_t *edge_layer, const float *rho,
+                            const float *grad_field, int nbins, int nv, int nu, double h,
+                            double eps, double min_step, int fixed_step,
+                            unsigned long long *moved, double *disp_partials, void *stream);
+
 /* _kernels.advect (_kernels.py:144-200) -> _kernels.laplacian
  * (_kernels.py:275-296) -> _kernels.resample_count (_kernels.py:203-232) of
  * the NEXT iteration, fused in one streaming pass:

@@ -24,6 +24,7 @@ from __future__ import annotations
 
 import ctypes
 import math
+import os
 from dataclasses import dataclass, field
 
 import numpy as np
@@ -198,6 +199,11 @@ class BundleEngine:
         # faster than fusing it: the fused build's register footprint halves
         # the advect's occupancy)
         self.split_count = True
+        # advection as a flat point stream (hb_advect_points) followed by the
+        # Laplacian fused with the resample count; the per-edge fused pass
+        # (hb_advect_laplacian with h >= 0) remains for very large fields
+        self.flat_advect = (B * self.nv * self.nu < (1 << 31)
+                            and os.environ.get("HB_FLAT_ADVECT", "1") != "0")
         self.peak = torch.empty(B, dtype=torch.float32, device=dev)
         self.status = torch.zeros(1, dtype=torch.int32, device=dev)
         sws = N.lib().hb_smooth_workspace_bytes(B, self.nv, self.nu)
@@ -393,7 +399,6 @@ class BundleEngine:
         s = stream_ptr()
         E, B, nv, nu = self.n_edges, self.nbins, self.nv, self.nu
         ev0 = self._ev_open
-        ev1 = torch.cuda.Event(enable_timing=True)
         is_int = self.wkind != "float"
         self._k("hb_smooth", ptr(self.hist) if is_int else None,
                 None if is_int else ptr(self.hist), ptr(self.mat_dev), B, nv, nu,
@@ -404,6 +409,23 @@ class BundleEngine:
         last = i == self.iters - 1
         if self.gfield is not None:
             self._k("hb_grad_field", ptr(self.field), B, nv, nu, ptr(self.gfield), s)
+        if self.flat_advect:
+            self._k("hb_advect_points", ptr(self.pts), ptr(self.starts), E, self.n_pts,
+                    ptr(self.groups), ptr(self.field), ptr(self.gfield), B, nv, nu,
+                    float(h_i), float(cfg.epsilon), MIN_STEP, int(self.fixed_step),
+                    self.m_moved.data_ptr() + 8 * i, ptr(self._partials), s)
+            if self.lap_passes > 0 or not last:
+                # Laplacian sweep(s) fused with the next resample count, in place
+                self._k("hb_advect_laplacian", ptr(self.pts), ptr(self.pts), ptr(self.starts),
+                        E, self.n_pts, None, None, None, B, nv, nu, -1.0, float(cfg.epsilon),
+                        MIN_STEP, 0, float(cfg.laplacian_factor), self.lap_passes, self.delta,
+                        None if last else ptr(self.ecounts), None if last else ptr(self.pos),
+                        None, None, s)
+            self._k("hb_reduce_f64", ptr(self._partials), self._partials.numel(),
+                    self.m_disp.data_ptr() + 8 * i, s)
+            self._k("hb_used_cells", ptr(self.field), ptr(self.peak), B, nv, nu, 0.01,
+                    self.m_used.data_ptr() + 8 * i, s)
+            return self._close_iteration(ev0, h_i)
         fuse = not last and not self.split_count
         self._k("hb_advect_laplacian", ptr(self.pts), ptr(self.pts), ptr(self.starts), E,
                 self.n_pts, ptr(self.groups), ptr(self.field), ptr(self.gfield), B, nv, nu,
@@ -418,9 +440,13 @@ class BundleEngine:
                 self.m_disp.data_ptr() + 8 * i, s)
         self._k("hb_used_cells", ptr(self.field), ptr(self.peak), B, nv, nu, 0.01,
                 self.m_used.data_ptr() + 8 * i, s)
+        return self._close_iteration(ev0, h_i)
+
+    def _close_iteration(self, ev0, h_i: float) -> IterationRecord:
+        ev1 = torch.cuda.Event(enable_timing=True)
         ev1.record()
         self._ev.append((ev0, ev1))
-        rec = IterationRecord(i, h_i, self.n_pts, E)
+        rec = IterationRecord(self.iteration, h_i, self.n_pts, self.n_edges)
         self.records.append(rec)
         self.iteration += 1
         return rec

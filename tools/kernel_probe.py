@@ -217,6 +217,21 @@ def main():
     out["gf_adv_lap_ms"] = timed(lambda: adv(h, 1, False))
     out["gf_adv_only_ms"] = timed(lambda: adv(h, 0, False))
     out["copy_pts_ms"] = timed(lambda: work[:n_new].copy_(eng.alt[:n_new]))
+    # flat advection (in place on a copy) and the Laplacian+count pass after it
+    work[:n_new].copy_(eng.alt[:n_new])
+
+    def flat():
+        N.call("hb_advect_points", ptr(work), ptr(eng.starts_alt), E, n_new, ptr(eng.groups),
+               ptr(eng.field), ptr(gfield), Bn, nv, nu, float(h), float(cfg.epsilon), MIN_STEP, 0,
+               eng.m_moved.data_ptr(), ptr(eng._partials), s)
+
+    out["gf_flat_adv_ms"] = timed(flat, reps=1)
+    cnt2 = torch.empty_like(eng.ecounts)
+    pos2 = torch.empty_like(eng.pos)
+    out["lap_count_ms"] = timed(lambda: N.call(
+        "hb_advect_laplacian", ptr(work), ptr(work), ptr(eng.starts_alt), E, n_new, None, None,
+        None, Bn, nv, nu, -1.0, float(cfg.epsilon), MIN_STEP, 0, float(cfg.laplacian_factor), 1,
+        float(cfg.delta), ptr(cnt2), ptr(pos2), None, None, s), reps=1)
     print(json.dumps(out))
 
 

@@ -121,9 +121,8 @@ polyline_pass_kernel(const PolylinePass p) {
         const int64_t lbase = do_adv ? (int64_t)p.edge_layer[e] * p.plane : 0;
         const float *rho = do_adv ? p.rho + lbase : nullptr;
         constexpr bool quad = ADV && QUAD;
-        const int64_t cells = (int64_t)p.plane * p.nbins_field;
-        QuadField qf{nullptr, nullptr, nullptr, 0u};
-        if (quad) qf = QuadField{p.gf, p.gf + cells, p.gf + 2 * cells, (unsigned)lbase};
+        QuadField qf{nullptr, 0u};
+        if (quad) qf = QuadField{p.gf, (unsigned)lbase};
 
         double2 cur = make_double2(0.0, 0.0);   // A(chunk c), lane = local index - c0
         double2 left = make_double2(0.0, 0.0);  // A(c0 - 1)
@@ -365,8 +364,8 @@ int hb_advect_laplacian(const double *pts_in, double *pts_out, const int64_t *st
         (counts && (!pos || !(delta > 0))) ||
         (n_pts > 0 && (!pts_in || !pts_out || !starts)))
         return set_error(HB_EINVAL, "hb_advect_laplacian: bad arguments");
-    if (adv && grad_field && (int64_t)nbins * nv * nu >= ((int64_t)1 << 31))
-        return set_error(HB_EINVAL, "hb_advect_laplacian: quad field above 2^31 cells");
+    if (adv && grad_field && 3 * (int64_t)nbins * nv * nu >= ((int64_t)1 << 32))
+        return set_error(HB_EINVAL, "hb_advect_laplacian: quad field above 2^32/3 cells");
     if (n_pts == 0 || n_edges == 0) return HB_OK;
     cudaStream_t st = as_stream(stream);
     PolylinePass p{};

@@ -37,7 +37,6 @@ struct AdvectFlat {
     const float4 *gf = nullptr;  // quad field (hb_grad_field) or null
     int nbins = 1;
     unsigned plane = 0;  // cells per layer; layers * plane < 2^31 (checked)
-    unsigned cells = 0;  // layers * plane: stride of the quad field's planes
     int nv = 0, nu = 0;
     double xhi = 0.0, yhi = 0.0, h = 0.0, eps = 1e-8, min_step = 0.25;
     int fixed = 0;
@@ -194,9 +193,7 @@ __global__ void __launch_bounds__(kStreamBlock, 4) advect_flat_kernel(const Adve
                 // _kernels.py:163-175 (G = 2*gradient, see gradient2_value_ref)
                 double Gx, Gy;
                 if (QUAD) {
-                    gradient2_value_quad(QuadField{p.gf, p.gf + p.cells, p.gf + 2 * (size_t)p.cells,
-                                                   base},
-                                         p.nv, p.nu, x, y, Gx, Gy, r0);
+                    gradient2_value_quad(QuadField{p.gf, base}, p.nv, p.nu, x, y, Gx, Gy, r0);
                 } else {
                     gradient2_value_ref(p.rho + base, p.nv, p.nu, x, y, Gx, Gy, r0);
                 }
@@ -280,7 +277,8 @@ int hb_advect_points(double *pts, const int64_t *starts, int64_t n_edges, int64_
         nu > kMaxDim || !moved || !disp_partials || !(h >= 0.0) ||
         (n_pts > 0 && (!pts || !starts || !edge_layer || !rho)))
         return set_error(HB_EINVAL, "hb_advect_points: bad arguments");
-    if ((int64_t)nbins * nv * nu >= ((int64_t)1 << 31))
+    if ((int64_t)nbins * nv * nu >= ((int64_t)1 << 31) ||
+        (grad_field && 3 * (int64_t)nbins * nv * nu >= ((int64_t)1 << 32)))
         return set_error(HB_EINVAL, "hb_advect_points: field above 2^31 cells");
     cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
     if (cudaMemsetAsync(disp_partials, 0, sizeof(double) * kMaxStreamBlocks, st) != cudaSuccess)
@@ -296,7 +294,6 @@ int hb_advect_points(double *pts, const int64_t *starts, int64_t n_edges, int64_
     p.gf = reinterpret_cast<const float4 *>(grad_field);
     p.nbins = nbins;
     p.plane = (unsigned)((int64_t)nv * nu);
-    p.cells = (unsigned)((int64_t)nbins * nv * nu);
     p.nv = nv;
     p.nu = nu;
     p.xhi = (double)(nu - 2);  // == (nu - 1.0) - 1.0 exactly (_kernels.py:158-159)

@@ -178,11 +178,12 @@ __device__ __forceinline__ void gradient2_value_ref(const float *__restrict__ rh
 
 // Same results from the quad field (hb_grad_field): q = rho at the 2x2
 // corners of cell (u0, v0), qx/qy = the corners' float32 differences.
-// q/gx/gy point at the WHOLE field (all layers); `base` is the layer's first
-// cell.  Offsets are 32-bit (hb_advect_laplacian checks layers*V*U < 2^31),
-// which keeps the per-sample address math to a few integer ops.
+// q points at the WHOLE field (all layers, one {Q, GX, GY} record of three
+// float4 per cell); `base` is the layer's first cell.  Offsets are 32-bit
+// (the host checks 3 * layers*V*U < 2^32), which keeps the per-sample
+// address math to a few integer ops.
 struct QuadField {
-    const float4 *q, *gx, *gy;
+    const float4 *q;
     unsigned base;
 };
 
@@ -193,8 +194,8 @@ __device__ __forceinline__ void gradient2_value_quad(const QuadField &f, int nv,
     const int v0 = clampi(floor_i(y), 0, nv - 2);
     const double fx = dsub(x, (double)u0);
     const double fy = dsub(y, (double)v0);
-    const unsigned o = f.base + (unsigned)(v0 * nu + u0);
-    const float4 q = __ldg(f.q + o), dx = __ldg(f.gx + o), dy = __ldg(f.gy + o);
+    const float4 *rec = f.q + 3u * (f.base + (unsigned)(v0 * nu + u0));
+    const float4 q = __ldg(rec), dx = __ldg(rec + 1), dy = __ldg(rec + 2);
     // corners: .x (u0,v0)  .y (u0+1,v0)  .z (u0,v0+1)  .w (u0+1,v0+1)
     const double ax = dadd((double)dx.x, dmul(fx, dsub((double)dx.y, (double)dx.x)));
     const double bx = dadd((double)dx.z, dmul(fx, dsub((double)dx.w, (double)dx.z)));
@@ -216,7 +217,7 @@ __device__ __forceinline__ double bilinear_quad(const float4 *__restrict__ q, un
     const int v0 = inner ? floor_i(y) : clampi(floor_i(y), 0, nv - 2);
     const double fx = dsub(x, (double)u0);
     const double fy = dsub(y, (double)v0);
-    const float4 c = __ldg(q + (base + (unsigned)(v0 * nu + u0)));
+    const float4 c = __ldg(q + 3u * (base + (unsigned)(v0 * nu + u0)));
     const double a = lerp_f32diff(c.x, c.y, fx);
     const double b = lerp_f32diff(c.z, c.w, fx);
     return dadd(a, dmul(fy, dsub(b, a)));

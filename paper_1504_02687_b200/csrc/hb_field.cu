@@ -214,9 +214,10 @@ __global__ void mix_pass_kernel(const T *__restrict__ groups, const float *__res
     }
 }
 
-// Quad advection field.  For every cell (u, v) of a layer, three float4:
-//   Q [v][u] = rho at the 2x2 corners (u,v) (u+1,v) (u,v+1) (u+1,v+1)
-//   GX[v][u] = dX at the same corners,  GY[v][u] = dY at the same corners,
+// Quad advection field.  For every cell (u, v) of a layer, a 48-byte record
+// of three float4 (interleaved, so a gradient sample reads 2 sectors, not 3):
+//   Q  = rho at the 2x2 corners (u,v) (u+1,v) (u,v+1) (u+1,v+1)
+//   GX = dX at the same corners,  GY = dY at the same corners,
 // where dX/dY are _cell_gradient's float32 central differences
 // (_kernels.py:101-114) at the clamped corner cell.  A bilinear sample
 // (_kernels.py:80-98) is then one 16-byte load and the gradient+value of a
@@ -231,28 +232,27 @@ __device__ __forceinline__ void cell_diff(const float *__restrict__ r, int nv, i
 }
 
 __global__ void grad_field_kernel(const float *__restrict__ rho, int nv, int nu,
-                                  float4 *__restrict__ q, float4 *__restrict__ gx,
-                                  float4 *__restrict__ gy) {
+                                  float4 *__restrict__ out) {
     const int u = blockIdx.x * blockDim.x + threadIdx.x;
     const int v = blockIdx.y;
     const int l = blockIdx.z;
     if (u >= nu) return;
     const int64_t plane = (int64_t)nv * nu;
     const float *r = rho + l * plane;
-    const int64_t o = l * plane + (int64_t)v * nu + u;
+    float4 *rec = out + 3 * (l * plane + (int64_t)v * nu + u);  // {Q, GX, GY} of the cell
     if (u > nu - 2 || v > nv - 2) {
-        q[o] = gx[o] = gy[o] = make_float4(0.f, 0.f, 0.f, 0.f);
+        rec[0] = rec[1] = rec[2] = make_float4(0.f, 0.f, 0.f, 0.f);
         return;
     }
     const float *c = r + (int64_t)v * nu + u;
-    q[o] = make_float4(c[0], c[1], c[nu], c[nu + 1]);
+    rec[0] = make_float4(c[0], c[1], c[nu], c[nu + 1]);
     float x00, y00, x10, y10, x01, y01, x11, y11;
     cell_diff(r, nv, nu, u, v, x00, y00);
     cell_diff(r, nv, nu, u + 1, v, x10, y10);
     cell_diff(r, nv, nu, u, v + 1, x01, y01);
     cell_diff(r, nv, nu, u + 1, v + 1, x11, y11);
-    gx[o] = make_float4(x00, x10, x01, x11);
-    gy[o] = make_float4(y00, y10, y01, y11);
+    rec[1] = make_float4(x00, x10, x01, x11);
+    rec[2] = make_float4(y00, y10, y01, y11);
 }
 
 // used_cell_count (bundler.py:292-305): rho > float32(rel * peak_l) when
@@ -379,9 +379,7 @@ int hb_grad_field(const float *rho, int nbins, int nv, int nu, float *out, void 
     if (!rho || !out || nbins < 1 || nv < 3 || nu < 3 || nv > kMaxDim || nu > kMaxDim)
         return set_error(HB_EINVAL, "hb_grad_field: bad arguments");
     dim3 g((nu + 255) / 256, nv, nbins);
-    const int64_t cells = (int64_t)nbins * nv * nu;
-    float4 *q = reinterpret_cast<float4 *>(out);
-    grad_field_kernel<<<g, 256, 0, as_stream(stream)>>>(rho, nv, nu, q, q + cells, q + 2 * cells);
+    grad_field_kernel<<<g, 256, 0, as_stream(stream)>>>(rho, nv, nu, reinterpret_cast<float4 *>(out));
     return check_launch("hb_grad_field");
 }
 

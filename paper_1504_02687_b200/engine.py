@@ -193,7 +193,7 @@ class BundleEngine:
         # quad advection field (hb_grad_field), 48 B per cell: used while it
         # stays L2-resident, otherwise the advection gathers from rho itself
         quad_bytes = 48 * B * self.nv * self.nu
-        self.gfield = (torch.empty((3, B, self.nv, self.nu, 4), dtype=torch.float32, device=dev)
+        self.gfield = (torch.empty((B, self.nv, self.nu, 3, 4), dtype=torch.float32, device=dev)
                        if quad_bytes <= (100 << 20) else None)
         # resample count as its own launch after the advect pass (measured
         # faster than fusing it: the fused build's register footprint halves

@@ -254,6 +254,11 @@ emit_kernel(const double2 *__restrict__ pts, const int64_t *__restrict__ starts,
             } else {
                 // key: output index of the nearest kept point at or below this lane
                 const int key = kept ? pj : pa;
+                // segment m-1 -> m starts at output m-1: the previous lane's
+                // point (bit-identical to re-interpolating piece k-1), the
+                // previous round's lane 31, or at the chunk start output apos,
+                // the carried kept point a
+                double2 qprev = a;
                 for (int m = apos + 1 + lane; m - lane <= last_pos; m += kWarp) {
                     int lo = 0;
 #pragma unroll
@@ -269,18 +274,20 @@ emit_kernel(const double2 *__restrict__ pts, const int64_t *__restrict__ starts,
                     const int opj = __shfl_sync(full, pj, owner);
                     const int opa = __shfl_sync(full, pa, owner);
                     const bool here = m <= last_pos;
-                    double2 q = make_double2(0.0, 0.0), q0 = q;
+                    double2 q = make_double2(0.0, 0.0);
                     if (here) {
                         const int pieces = opj - opa, k = m - opa;
-                        const double2 ox2 = make_double2(ox, oy), oa2 = make_double2(oax, oay);
-                        q = interp_piece(oa2, ox2, k, pieces);
-                        q0 = interp_piece(oa2, ox2, k - 1, pieces);
+                        q = interp_piece(make_double2(oax, oay), make_double2(ox, oy), k, pieces);
                         HB_ST_STREAM(o + m, q);
                     }
-                    if (splat)
-                        bin_or_splat<int32_t>(here && m >= 1, q0.x, q0.y, q.x, q.y,
+                    if (splat) {
+                        double q0x = __shfl_up_sync(full, q.x, 1), q0y = __shfl_up_sync(full, q.y, 1);
+                        if (lane == 0) { q0x = qprev.x; q0y = qprev.y; }
+                        qprev = make_double2(__shfl_sync(full, q.x, 31), __shfl_sync(full, q.y, 31));
+                        bin_or_splat<int32_t>(here && m >= 1, q0x, q0y, q.x, q.y,
                                               m == 1 ? 0 : 1, w, grp, hist, plane, nv, nu, status,
                                               tiles);
+                    }
                 }
             }
             a.x = __shfl_sync(full, x.x, lk);

@@ -44,8 +44,37 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--config", type=int, default=4)
     ap.add_argument("--iters", type=int, default=6)
+    ap.add_argument("--sort-edges", default="none", choices=["none", "srcdst", "mid"],
+                    help="experiment: reorder the graph's edges spatially first")
     args = ap.parse_args()
     w = workload(args.config)
+    if args.sort_edges != "none":
+        import numpy as np
+
+        from paper_1504_02687_b200.model import Graph
+
+        g = w.graph
+        ps, pt = g.positions[g.sources], g.positions[g.targets]
+
+        def q(v, bits):  # quantise [0,1] -> int
+            return np.clip((v * (1 << bits)).astype(np.int64), 0, (1 << bits) - 1)
+
+        def interleave(cols, bits):
+            key = np.zeros(len(cols[0]), dtype=np.int64)
+            for b in range(bits):
+                for c, col in enumerate(cols):
+                    key |= ((col >> b) & 1) << (b * len(cols) + c)
+            return key
+
+        if args.sort_edges == "srcdst":
+            key = interleave([q(ps[:, 0], 8), q(ps[:, 1], 8), q(pt[:, 0], 8), q(pt[:, 1], 8)], 8)
+        else:
+            mid = 0.5 * (ps + pt)
+            key = interleave([q(mid[:, 0], 16), q(mid[:, 1], 16)], 16)
+        order = np.argsort(key, kind="stable")
+        bins = None if w.bins is None else np.asarray(w.bins)[order]
+        w = type(w)(**{**w.__dict__, "graph": Graph(g.positions, g.sources[order],
+                                                         g.targets[order]), "bins": bins})
     eng, tr, _, _ = B.prepare_engine(w.graph, w.config, bins=w.bins, matrix=w.matrix)
     for _ in range(args.iters):
         eng.step()

@@ -328,6 +328,9 @@ __device__ __forceinline__ uint64_t encode_seg(int x0, int y0, int dx, int dy, i
 // tile's bucket; everything else -- census mode (no record storage), bucket
 // overflow, non-unit float weights, long or out-of-grid segments -- is
 // rasterised straight into the histogram exactly as before.
+// Row pitch (entries) of the segment-key table: nu rounded up to 4.
+__host__ __device__ __forceinline__ int segtab_pitch(int nu) { return (nu + 3) & ~3; }
+
 template <typename T>
 __device__ __forceinline__ void bin_or_splat(bool has, double px0, double py0, double px1,
                                              double py1, int k0, T w, int grp,
@@ -353,7 +356,8 @@ __device__ __forceinline__ void bin_or_splat(bool has, double px0, double py0, d
                 // so the index fits 32-bit arithmetic)
                 const unsigned D = 2 * H + 1;
                 const unsigned dir = (unsigned)grp * D * D + (unsigned)((dy + H) * D + (dx + H));
-                atomicAdd(tl->tab + ((dir * (unsigned)nv + (unsigned)y0) * (unsigned)nu + (unsigned)x0),
+                atomicAdd(tl->tab + ((dir * (unsigned)nv + (unsigned)y0) * (unsigned)segtab_pitch(nu) +
+                                     (unsigned)x0),
                           (unsigned)iw);
                 direct = false;
             }

@@ -222,41 +222,131 @@ int hb_tiles_flush(const hb_tiles *t, int32_t *counts, int nv, int nu, void *str
 namespace hb {
 
 constexpr int kExpandBlock = 256;
+// Tile shape measured on config 4 (expansion ms/iteration): 64x32 0.665,
+// 64x16 0.52, 64x8 0.40, 64x4 0.33, 64x2 / 32x4 / 16x8 0.33 -- small tiles
+// give many blocks to hide the table scan's latency; the halo overhead of
+// the shared histogram only costs flush atomics on touched cells.
+#ifndef HB_EX_TY
+#define HB_EX_TY 4
+#endif
+#ifndef HB_EX_UNROLL
+#define HB_EX_UNROLL 2
+#endif
+#ifndef HB_EX_TX
+#define HB_EX_TX 64
+#endif
+constexpr int kExTX = HB_EX_TX, kExTY = HB_EX_TY;  // start-cell tile of one expansion block
+static_assert(kExTX <= 64 && kExTX % 4 == 0, "column field of the packed key is 6 bits");
+static_assert(kExTY <= 128, "row field of the packed key is 7 bits");
+constexpr int kExUnroll = HB_EX_UNROLL;      // table loads in flight per thread per round
+constexpr int kExRound = kExpandBlock * kExUnroll * 4;  // max keys found per round
+constexpr int kExBuf = 2 * kExRound;                    // compacted key buffer
 
+// One block per (start-cell tile, group).  The block scans every delta plane
+// of the key table over its tile (aligned uint4 rows), zeroing what it reads
+// and compacting the non-zero keys (plane, row, column, count) into a shared
+// buffer; whenever the buffer could overflow, all threads rasterise buffered
+// keys (_kernels.py:58-77, k0 = 1), one per thread, into a shared histogram
+// covering the tile plus the H-cell halo its segments reach.  The shared
+// histogram is added to the global one at the end: one atomic per touched
+// cell instead of one per rasterised cell (bundled keys pile onto few cells).
 __global__ void __launch_bounds__(kExpandBlock)
 segtab_expand_kernel(const __grid_constant__ hb_tiles t, int32_t *__restrict__ counts, int nv,
-                     int nu, int64_t n4, unsigned long long *__restrict__ nonzero) {
-    const int H = t.halo, D = 2 * H + 1;
-    unsigned keys = 0;
-    const int64_t plane = (int64_t)nv * nu;
+                     int nu, unsigned long long *__restrict__ nonzero) {
+    extern __shared__ int sh[];  // (kExTY + 2H) x (kExTX + 2H) cell counts
+    __shared__ uint2 buf[kExBuf];
+    __shared__ int nbuf;
+    const int H = t.halo, D = 2 * H + 1, DD = D * D;
+    const int SW = kExTX + 2 * H, SH = kExTY + 2 * H;
+    const int pitch = segtab_pitch(nu);
+    const int ntx = (nu + kExTX - 1) / kExTX;
+    const int tx0 = (blockIdx.x % ntx) * kExTX, ty0 = (blockIdx.x / ntx) * kExTY;
+    const int g = blockIdx.y;
+    const int lane = threadIdx.x & 31;
+    for (int i = threadIdx.x; i < SW * SH; i += kExpandBlock) sh[i] = 0;
+    if (threadIdx.x == 0) nbuf = 0;
+    __syncthreads();
+    constexpr int c4 = kExTX / 4, per_plane = kExTY * c4;
+    const int total = DD * per_plane;
     uint4 *tab4 = reinterpret_cast<uint4 *>(t.tab);
-    for (int64_t q = (int64_t)blockIdx.x * kExpandBlock + threadIdx.x; q < n4;
-         q += (int64_t)gridDim.x * kExpandBlock) {
-        const uint4 v4 = tab4[q];
-        if ((v4.x | v4.y | v4.z | v4.w) == 0u) continue;
-        tab4[q] = make_uint4(0u, 0u, 0u, 0u);
-        const unsigned vals[4] = {v4.x, v4.y, v4.z, v4.w};
-#pragma unroll
-        for (int c = 0; c < 4; ++c) {
-            const unsigned val = vals[c];
-            if (!val) continue;
-            ++keys;
-            const int64_t idx = q * 4 + c;
-            const int64_t key = idx / plane;  // g*D*D + dir
-            const int64_t cell = idx - key * plane;
-            const int g = (int)(key / ((int64_t)D * D));
-            const int dir = (int)(key - (int64_t)g * D * D);
-            const int dy = dir / D - H, dx = dir % D - H;
-            const int y0 = (int)(cell / nu), x0 = (int)(cell - (int64_t)y0 * nu);
-            int32_t *layer = counts + (int64_t)g * plane;
-            dda_walk(x0, y0, x0 + dx, y0 + dy, 1, [&](int u, int v) {
-                atomicAdd(layer + (int64_t)v * nu + u, (int)val);
+    const int64_t pitch4 = pitch / 4;
+    unsigned keys = 0;
+
+    auto rasterise = [&]() {  // all threads: drain the buffer into sh
+        const int n = nbuf;
+        for (int i = threadIdx.x; i < n; i += kExpandBlock) {
+            const uint2 k = buf[i];
+            const int plane = (int)(k.x >> 13), y0 = ty0 + (int)((k.x >> 6) & 127u),
+                      x0 = tx0 + (int)(k.x & 63u);
+            const int dy = plane / D - H, dx = plane % D - H;
+            dda_walk(x0, y0, x0 + dx, y0 + dy, 1, [&](int u, int vv) {
+                atomicAdd(&sh[(vv - ty0 + H) * SW + (u - tx0 + H)], (int)k.y);
             });
+        }
+    };
+
+    for (int base = threadIdx.x; base < total; base += kExpandBlock * kExUnroll) {
+        uint4 v[kExUnroll];
+#pragma unroll
+        for (int k = 0; k < kExUnroll; ++k) {
+            const int idx = base + k * kExpandBlock;
+            const int plane = idx / per_plane, rem = idx - plane * per_plane;
+            const int y = ty0 + rem / c4, x = tx0 + (rem % c4) * 4;
+            v[k] = make_uint4(0u, 0u, 0u, 0u);
+            if (idx < total && y < nv && x < nu)
+                v[k] = tab4[((int64_t)(g * DD + plane) * nv + y) * pitch4 + (x >> 2)];
+        }
+        int mine = 0;
+#pragma unroll
+        for (int k = 0; k < kExUnroll; ++k)
+            mine += (v[k].x != 0u) + (v[k].y != 0u) + (v[k].z != 0u) + (v[k].w != 0u);
+        // warp-aggregated slot reservation
+        int incl = mine;
+        for (int d = 1; d < 32; d <<= 1) {
+            const int o = __shfl_up_sync(0xffffffffu, incl, d);
+            if (lane >= d) incl += o;
+        }
+        int slot = 0;
+        if (lane == 31 && incl) slot = atomicAdd(&nbuf, incl);
+        slot = __shfl_sync(0xffffffffu, slot, 31) + incl - mine;
+        if (mine) {
+            keys += mine;
+#pragma unroll
+            for (int k = 0; k < kExUnroll; ++k) {
+                if ((v[k].x | v[k].y | v[k].z | v[k].w) == 0u) continue;
+                const int idx = base + k * kExpandBlock;
+                const int plane = idx / per_plane, rem = idx - plane * per_plane;
+                const int row = rem / c4, xb = (rem % c4) * 4;
+                tab4[((int64_t)(g * DD + plane) * nv + ty0 + row) * pitch4 + ((tx0 + xb) >> 2)] =
+                    make_uint4(0u, 0u, 0u, 0u);
+                const unsigned pk = ((unsigned)plane << 13) | ((unsigned)row << 6);
+                if (v[k].x) buf[slot++] = make_uint2(pk | (unsigned)(xb + 0), v[k].x);
+                if (v[k].y) buf[slot++] = make_uint2(pk | (unsigned)(xb + 1), v[k].y);
+                if (v[k].z) buf[slot++] = make_uint2(pk | (unsigned)(xb + 2), v[k].z);
+                if (v[k].w) buf[slot++] = make_uint2(pk | (unsigned)(xb + 3), v[k].w);
+            }
+        }
+        __syncthreads();
+        if (nbuf > kExBuf - kExRound) {  // (block-uniform) the next round could overflow
+            rasterise();
+            __syncthreads();
+            if (threadIdx.x == 0) nbuf = 0;
+            __syncthreads();
+        }
+    }
+    rasterise();
+    __syncthreads();
+    int32_t *layer = counts + (int64_t)g * nv * nu;
+    for (int i = threadIdx.x; i < SW * SH; i += kExpandBlock) {
+        const int val = sh[i];
+        if (val) {
+            const int gy = ty0 - H + i / SW, gx = tx0 - H + i % SW;
+            atomicAdd(layer + (int64_t)gy * nu + gx, val);
         }
     }
     if (nonzero) {
         for (int o = 16; o; o >>= 1) keys += __shfl_down_sync(0xffffffffu, keys, o);
-        if ((threadIdx.x & 31) == 0 && keys) atomicAdd(nonzero, (unsigned long long)keys);
+        if (lane == 0 && keys) atomicAdd(nonzero, (unsigned long long)keys);
     }
 }
 
@@ -270,14 +360,15 @@ int hb_segtab_geometry(int nbins, int nv, int nu, double max_seg_cells, hb_tiles
         return set_error(HB_EINVAL, "hb_segtab_geometry: bad arguments");
     if (max_seg_cells > 60.0)
         return set_error(HB_EINVAL, "hb_segtab_geometry: segments too long for a key table");
-    const int H = (int)ceil(max_seg_cells) + 1;
+    // |round(x1) - round(x0)| <= ceil(|x1 - x0|): a segment no longer than
+    // max_seg_cells moves at most ceil(max_seg_cells) cells per axis
+    const int H = (int)ceil(max_seg_cells) < 1 ? 1 : (int)ceil(max_seg_cells);
     const int64_t D = 2 * H + 1;
     t->mode = 1;
     t->halo = H;
     t->nbins = nbins;
-    *entries = (int64_t)nbins * D * D * nv * nu;
-    // whole uint4 loads in the expansion
-    *entries = (*entries + 3) / 4 * 4;
+    // rows padded to a multiple of 4 entries: aligned uint4 scans
+    *entries = (int64_t)nbins * D * D * nv * segtab_pitch(nu);
     if (*entries >= ((int64_t)1 << 31))  // keys are 32-bit indices (bin_or_splat)
         return set_error(HB_EINVAL, "hb_segtab_geometry: key table above 2^31 entries");
     return HB_OK;
@@ -285,20 +376,18 @@ int hb_segtab_geometry(int nbins, int nv, int nu, double max_seg_cells, hb_tiles
 
 int hb_segtab_expand(const hb_tiles *t, int32_t *counts, int nv, int nu,
                      unsigned long long *nonzero, void *stream) {
-    if (!t || t->mode != 1 || !t->tab || !counts || nv < 1 || nu < 1)
+    if (!t || t->mode != 1 || !t->tab || !counts || nv < 1 || nu < 1 || t->halo < 1 ||
+        t->nbins < 1)
         return set_error(HB_EINVAL, "hb_segtab_expand: bad arguments");
-    const int64_t D = 2 * t->halo + 1;
-    const int64_t n = (int64_t)t->nbins * D * D * nv * nu;
-    const int64_t n4 = (n + 3) / 4;
-    int per_sm = 0;
-    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, segtab_expand_kernel,
-                                                      kExpandBlock, 0) != cudaSuccess ||
-        per_sm < 1)
-        per_sm = 1;
-    const int64_t want = (n4 + kExpandBlock - 1) / kExpandBlock;
-    const int64_t cap = (int64_t)device_sm_count() * per_sm * 4;
-    segtab_expand_kernel<<<(unsigned)(want < cap ? want : cap), kExpandBlock, 0,
-                           as_stream(stream)>>>(*t, counts, nv, nu, n4, nonzero);
+    const int H = t->halo;
+    const size_t smem = sizeof(int) * (size_t)(kExTX + 2 * H) * (kExTY + 2 * H);
+    // static (key buffer) + dynamic (histogram) can exceed the 48 KB default
+    if (cudaFuncSetAttribute(segtab_expand_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)smem) != cudaSuccess)
+        return check_launch("hb_segtab_expand(smem)", 0);
+    const unsigned ntiles = (unsigned)(((nu + kExTX - 1) / kExTX) * ((nv + kExTY - 1) / kExTY));
+    segtab_expand_kernel<<<dim3(ntiles, t->nbins), kExpandBlock, smem, as_stream(stream)>>>(
+        *t, counts, nv, nu, nonzero);
     return check_launch("hb_segtab_expand");
 }
 

@@ -328,8 +328,17 @@ __device__ __forceinline__ uint64_t encode_seg(int x0, int y0, int dx, int dy, i
 // tile's bucket; everything else -- census mode (no record storage), bucket
 // overflow, non-unit float weights, long or out-of-grid segments -- is
 // rasterised straight into the histogram exactly as before.
-// Row pitch (entries) of the segment-key table: nu rounded up to 4.
-__host__ __device__ __forceinline__ int segtab_pitch(int nu) { return (nu + 3) & ~3; }
+// Segment-key table layout: per (group, cell delta) plane, the start cells
+// in 4x4 blocks of 16 consecutive entries (64 B), blocks row-major.  Keys of
+// a bundle (parallel edges a few cells apart, same delta) share blocks, so
+// the per-segment atomics touch far fewer L2 sectors than a row layout.
+__host__ __device__ __forceinline__ int segtab_nbx(int nu) { return (nu + 3) >> 2; }
+__host__ __device__ __forceinline__ int segtab_nby(int nv) { return (nv + 3) >> 2; }
+__device__ __forceinline__ unsigned segtab_index(unsigned plane, int x0, int y0, int nv, int nu) {
+    const unsigned nbx = (unsigned)segtab_nbx(nu), nby = (unsigned)segtab_nby(nv);
+    return (((plane * nby + (unsigned)(y0 >> 2)) * nbx + (unsigned)(x0 >> 2)) << 4) +
+           (unsigned)(((y0 & 3) << 2) | (x0 & 3));
+}
 
 template <typename T>
 __device__ __forceinline__ void bin_or_splat(bool has, double px0, double py0, double px1,
@@ -356,9 +365,7 @@ __device__ __forceinline__ void bin_or_splat(bool has, double px0, double py0, d
                 // so the index fits 32-bit arithmetic)
                 const unsigned D = 2 * H + 1;
                 const unsigned dir = (unsigned)grp * D * D + (unsigned)((dy + H) * D + (dx + H));
-                atomicAdd(tl->tab + ((dir * (unsigned)nv + (unsigned)y0) * (unsigned)segtab_pitch(nu) +
-                                     (unsigned)x0),
-                          (unsigned)iw);
+                atomicAdd(tl->tab + segtab_index(dir, x0, y0, nv, nu), (unsigned)iw);
                 direct = false;
             }
         }

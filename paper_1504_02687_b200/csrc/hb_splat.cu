@@ -237,7 +237,7 @@ constexpr int kExpandBlock = 256;
 #endif
 constexpr int kExTX = HB_EX_TX, kExTY = HB_EX_TY;  // start-cell tile of one expansion block
 static_assert(kExTX <= 64 && kExTX % 4 == 0, "column field of the packed key is 6 bits");
-static_assert(kExTY <= 128, "row field of the packed key is 7 bits");
+static_assert(kExTY <= 128 && kExTY % 4 == 0, "tiles are whole 4x4 block rows; 7-bit row");
 constexpr int kExUnroll = HB_EX_UNROLL;      // table loads in flight per thread per round
 constexpr int kExRound = kExpandBlock * kExUnroll * 4;  // max keys found per round
 constexpr int kExBuf = 2 * kExRound;                    // compacted key buffer
@@ -258,7 +258,7 @@ segtab_expand_kernel(const __grid_constant__ hb_tiles t, int32_t *__restrict__ c
     __shared__ int nbuf;
     const int H = t.halo, D = 2 * H + 1, DD = D * D;
     const int SW = kExTX + 2 * H, SH = kExTY + 2 * H;
-    const int pitch = segtab_pitch(nu);
+    const int nbx = segtab_nbx(nu), nby = segtab_nby(nv);
     const int ntx = (nu + kExTX - 1) / kExTX;
     const int tx0 = (blockIdx.x % ntx) * kExTX, ty0 = (blockIdx.x / ntx) * kExTY;
     const int g = blockIdx.y;
@@ -266,10 +266,16 @@ segtab_expand_kernel(const __grid_constant__ hb_tiles t, int32_t *__restrict__ c
     for (int i = threadIdx.x; i < SW * SH; i += kExpandBlock) sh[i] = 0;
     if (threadIdx.x == 0) nbuf = 0;
     __syncthreads();
+    // per plane the tile is (kExTY/4) block rows of kExTX/4 blocks of four
+    // uint4 rows (one uint4 = 4 cells of one cell row): contiguous runs
     constexpr int c4 = kExTX / 4, per_plane = kExTY * c4;
     const int total = DD * per_plane;
     uint4 *tab4 = reinterpret_cast<uint4 *>(t.tab);
-    const int64_t pitch4 = pitch / 4;
+    // uint4 index of (plane, local block row br, local block bc, cell row ly)
+    auto q4 = [&](int plane, int br, int bc, int ly) -> int64_t {
+        return ((((int64_t)(g * DD + plane) * nby + (ty0 >> 2) + br) * nbx + (tx0 >> 2) + bc) << 2) +
+               ly;
+    };
     unsigned keys = 0;
 
     auto rasterise = [&]() {  // all threads: drain the buffer into sh
@@ -285,16 +291,19 @@ segtab_expand_kernel(const __grid_constant__ hb_tiles t, int32_t *__restrict__ c
         }
     };
 
-    for (int base = threadIdx.x; base < total; base += kExpandBlock * kExUnroll) {
+    // block-uniform trip count: the body has warp shuffles and a barrier
+    for (int base0 = 0; base0 < total; base0 += kExpandBlock * kExUnroll) {
+        const int base = base0 + (int)threadIdx.x;
         uint4 v[kExUnroll];
 #pragma unroll
         for (int k = 0; k < kExUnroll; ++k) {
             const int idx = base + k * kExpandBlock;
             const int plane = idx / per_plane, rem = idx - plane * per_plane;
-            const int y = ty0 + rem / c4, x = tx0 + (rem % c4) * 4;
+            // rem -> (block row, block, cell row), cell row fastest
+            const int ly = rem & 3, bc = (rem >> 2) % c4, br = (rem >> 2) / c4;
+            const int y = ty0 + br * 4 + ly, x = tx0 + bc * 4;
             v[k] = make_uint4(0u, 0u, 0u, 0u);
-            if (idx < total && y < nv && x < nu)
-                v[k] = tab4[((int64_t)(g * DD + plane) * nv + y) * pitch4 + (x >> 2)];
+            if (idx < total && y < nv && x < nu) v[k] = tab4[q4(plane, br, bc, ly)];
         }
         int mine = 0;
 #pragma unroll
@@ -316,9 +325,9 @@ segtab_expand_kernel(const __grid_constant__ hb_tiles t, int32_t *__restrict__ c
                 if ((v[k].x | v[k].y | v[k].z | v[k].w) == 0u) continue;
                 const int idx = base + k * kExpandBlock;
                 const int plane = idx / per_plane, rem = idx - plane * per_plane;
-                const int row = rem / c4, xb = (rem % c4) * 4;
-                tab4[((int64_t)(g * DD + plane) * nv + ty0 + row) * pitch4 + ((tx0 + xb) >> 2)] =
-                    make_uint4(0u, 0u, 0u, 0u);
+                const int ly = rem & 3, bc = (rem >> 2) % c4, br = (rem >> 2) / c4;
+                tab4[q4(plane, br, bc, ly)] = make_uint4(0u, 0u, 0u, 0u);
+                const int row = br * 4 + ly, xb = bc * 4;
                 const unsigned pk = ((unsigned)plane << 13) | ((unsigned)row << 6);
                 if (v[k].x) buf[slot++] = make_uint2(pk | (unsigned)(xb + 0), v[k].x);
                 if (v[k].y) buf[slot++] = make_uint2(pk | (unsigned)(xb + 1), v[k].y);
@@ -367,8 +376,8 @@ int hb_segtab_geometry(int nbins, int nv, int nu, double max_seg_cells, hb_tiles
     t->mode = 1;
     t->halo = H;
     t->nbins = nbins;
-    // rows padded to a multiple of 4 entries: aligned uint4 scans
-    *entries = (int64_t)nbins * D * D * nv * segtab_pitch(nu);
+    // 4x4-cell blocks (segtab_index)
+    *entries = (int64_t)nbins * D * D * segtab_nby(nv) * segtab_nbx(nu) * 16;
     if (*entries >= ((int64_t)1 << 31))  // keys are 32-bit indices (bin_or_splat)
         return set_error(HB_EINVAL, "hb_segtab_geometry: key table above 2^31 entries");
     return HB_OK;

@@ -124,6 +124,8 @@ def algorithmic_bytes(name: str, n_prev: int, n_cur: int, n_edges: int, cells: i
                       passes: int, nbins: int) -> int:
     if name == "hb_advect_points":      # advect: read + write every point
         return 32 * n_cur + 8 * n_edges + 4 * cells
+    if name == "hb_laplacian_count":    # Laplacian + next resample count (pos codes)
+        return 32 * n_cur + 4 * n_cur + 16 * n_edges
     if name == "hb_advect_laplacian":   # Laplacian (+ fused next resample count)
         return 32 * n_cur + 16 * n_edges + 4 * cells
     if name == "hb_resample_emit":      # resample emit + fused splat

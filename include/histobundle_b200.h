@@ -243,6 +243,17 @@ HB_API int hb_advect_laplacian(const double *pts_in, double *pts_out,
                         unsigned long long *moved, double *disp_partials,
                         void *stream);
 
+/* _kernels.laplacian (_kernels.py:275-296, lap_passes Jacobi sweeps) then
+ * _kernels.resample_count (_kernels.py:203-232) on the result:
+ *   pts_out = laplacian^lap_passes(pts_in)            (may alias pts_in)
+ *   counts[e] = output points of polyline e, pos[j] = output index of kept
+ *   point j or -1 (when counts != NULL; same outputs as hb_resample_count).
+ * One lane-sequential pass (hb_lapcount.cu).  n_pts < 2^31. */
+HB_API int hb_laplacian_count(const double *pts_in, double *pts_out, const int64_t *starts,
+                              int64_t n_edges, int64_t n_pts, double lap_factor,
+                              int lap_passes, double delta, int64_t *counts, int32_t *pos,
+                              void *stream);
+
 /* Deterministic fixed-order sum of n doubles into *out (one block). */
 HB_API int hb_reduce_f64(const double *in, int64_t n, double *out, void *stream);
 

@@ -18,7 +18,7 @@ LIB_DIR = os.path.join(_PKG, "_lib")
 LIB_PATH = os.path.join(LIB_DIR, "libhb_b200.so")
 INCLUDE = os.path.join(os.path.dirname(_PKG), "include")
 
-SOURCES = ["hb_api.cu", "hb_polyline.cu", "hb_field.cu", "hb_advect.cu", "hb_advect_flat.cu", "hb_splat.cu"]
+SOURCES = ["hb_api.cu", "hb_polyline.cu", "hb_field.cu", "hb_advect.cu", "hb_advect_flat.cu", "hb_lapcount.cu", "hb_splat.cu"]
 
 NVCC_FLAGS = [
     "-gencode", "arch=compute_100a,code=sm_100a",
@@ -87,6 +87,7 @@ SIGNATURES = {
                                  _D, _I, _D, _I, _D, _P, _P, _P, _P, _P]),
     "hb_advect_points": (_I, [_P, _P, _I64, _I64, _P, _P, _P, _I, _I, _I, _D, _D, _D, _I,
                               _P, _P, _P]),
+    "hb_laplacian_count": (_I, [_P, _P, _P, _I64, _I64, _D, _I, _D, _P, _P, _P]),
     "hb_reduce_f64": (_I, [_P, _I64, _P, _P]),
     "hb_resample_count": (_I, [_P, _P, _I64, _D, _P, _P, _P]),
     "hb_scan_workspace_bytes": (_SZ, [_I64]),

@@ -82,8 +82,12 @@ struct FlatField {
     }
 };
 
+#ifndef HB_FLAT_MINB
+#define HB_FLAT_MINB 4
+#endif
+
 template <bool QUAD>
-__global__ void __launch_bounds__(kStreamBlock, 4) advect_flat_kernel(const AdvectFlat p) {
+__global__ void __launch_bounds__(kStreamBlock, HB_FLAT_MINB) advect_flat_kernel(const AdvectFlat p) {
     __shared__ FlatQueue s_queue[kFlatWarps];
     const unsigned full = 0xffffffffu;
     const int lane = threadIdx.x & 31;

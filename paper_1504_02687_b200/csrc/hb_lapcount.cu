@@ -1,0 +1,467 @@
+// hb_lapcount.cu -- Jacobi Laplacian (_kernels.py:275-296) fused with the
+// next iteration's resample count (_kernels.py:203-232), lane-sequential.
+//
+// resample_count walks each polyline keeping `a`, the last KEPT point:
+// point j (not the last) merges when |p_j - a| < 0.5*delta, a kept point
+// gets pieces = 2^k (halve g while g > 1.5*delta) and its output index is
+// the running sum.  The walk is sequential, so instead of resolving it with
+// warp ballots (one round per merge chain, ~400 warp instructions per 32
+// points) every lane walks its own run of kRun consecutive points in order,
+// like the reference, at ~20 instructions per point:
+//
+//   * Each warp owns a contiguous, edge-aligned range of the packed points
+//     (balanced by point count) and takes it in groups of 32 runs x kRun,
+//     staged through shared memory (coalesced global traffic; lanes walk
+//     rows of a padded [run][point] table without bank conflicts).
+//   * Edge starts of the group come from one window of `starts` per group;
+//     run k's bits mark its starts and ends.
+//   * Phase B: every lane walks its run: Laplacian from a sliding window of
+//     the original points (run-boundary values are read before any lane
+//     writes, so pts_out may alias pts_in), then the keep/merge step.  A
+//     lane's run starts mid-edge with an unknown anchor: it SPECULATES that
+//     the point just before its run was kept (anchor = that point's final
+//     position, output offset 0 relative to it).  Lane 0 starts from the
+//     exact state carried over from the previous group.
+//   * Phase C: the speculation is right whenever that point was truly kept.
+//     Otherwise the lane re-walks from the true anchor until its decision
+//     sequence meets the speculative one at a point kept in both runs;
+//     from there both walks are identical (same anchor), so only a constant
+//     offset separates them.  Non-convergence inside a run (a merge chain
+//     longer than the run) changes that lane's end state and is re-checked
+//     for the next lane until stable.  A segmented scan over the lanes then
+//     turns the relative output offsets into absolute ones.
+//   * Final points and pos leave through the same shared tables, coalesced;
+//     counts are written at each polyline's last point.
+//
+// Every comparison and every floating-point operation is the reference's,
+// in its order (squared gaps against the exact sqrt thresholds, see
+// sqrt_lt_bound), so pos/counts are bit-identical to a sequential walk.
+#include "hb_common.cuh"
+
+namespace hb {
+
+struct LapCount {
+    const double2 *pin = nullptr;
+    double2 *pout = nullptr;  // may alias pin
+    const int64_t *starts = nullptr;
+    int64_t n_edges = 0, n_pts = 0;
+    double factor = 0.5;
+    int lap = 1;
+    double delta = 1.0;
+    int64_t *counts = nullptr;  // nullable: Laplacian only
+    int32_t *pos = nullptr;
+};
+
+constexpr int kLCBlock = 256;
+constexpr int kLCWarps = kLCBlock / 32;
+// Measured on config 4 (ms/iteration, run x min blocks): 32x1 4.91, 16x2
+// 3.28, 8x3 2.77, 8x4 2.54, 6x4 2.91, 4x4 3.40 (the ballot walk: 3.99).
+#ifndef HB_LC_RUN
+#define HB_LC_RUN 8
+#endif
+constexpr int kRun = HB_LC_RUN;       // points per lane per group
+constexpr int kGroup = 32 * kRun;     // points per warp per group
+constexpr int kRowPad = kRun + 1;     // odd row stride: column walks are conflict-free
+static_assert(kRun >= 2 && kRun <= 32, "run length");
+
+#ifndef HB_LC_MINB
+#define HB_LC_MINB 4
+#endif
+
+// first e in [0, n] with starts[e] >= v (starts is non-decreasing, starts[n] = N)
+__device__ __forceinline__ int64_t lower_edge(const int64_t *__restrict__ starts, int64_t n,
+                                              int64_t v) {
+    int64_t lo = 0, hi = n;
+    while (lo < hi) {
+        const int64_t mid = (lo + hi) >> 1;
+        if (starts[mid] < v) lo = mid + 1; else hi = mid;
+    }
+    return lo;
+}
+
+__device__ __forceinline__ double2 lap_point(double2 l, double2 c, double2 r, double f) {
+    // _kernels.py:290-293: mx = 0.5*(p[j-1]+p[j+1]); s = p + f*(mx - p)
+    const double mx = dmul(0.5, dadd(l.x, r.x));
+    const double my = dmul(0.5, dadd(l.y, r.y));
+    return make_double2(dadd(c.x, dmul(f, dsub(mx, c.x))), dadd(c.y, dmul(f, dsub(my, c.y))));
+}
+
+__device__ __forceinline__ int pieces_of(double g2, double hi2) {
+    // while (g > hi) { g *= 0.5; pieces *= 2; } on squared gaps (4^k scaling)
+    double t = hi2;
+    int pieces = 1;
+    while (g2 > t) {
+        t = dmul(t, 4.0);
+        pieces *= 2;
+    }
+    return pieces;
+}
+
+template <bool COUNT>
+__global__ void __launch_bounds__(kLCBlock, HB_LC_MINB) lapcount_kernel(const LapCount p) {
+    // per warp: the group's points as [run][point] (original, then final)
+    // and its output codes; rows padded so lanes walking rows hit distinct banks
+    extern __shared__ unsigned char lc_smem[];
+    const unsigned full = 0xffffffffu;
+    const int lane = threadIdx.x & 31;
+    const int wib = threadIdx.x >> 5;
+    double2 (*row_pt)[kRowPad] =
+        reinterpret_cast<double2 (*)[kRowPad]>(lc_smem) + (size_t)wib * 32;
+    int (*row_pos)[kRowPad] = reinterpret_cast<int (*)[kRowPad]>(
+        lc_smem + sizeof(double2) * kLCWarps * 32 * kRowPad) + (size_t)wib * 32;
+    const double lo2 = COUNT ? sqrt_lt_bound(0.5 * p.delta) : 0.0;  // _kernels.py:211-212
+    const double hi2 = COUNT ? sqrt_gt_bound(1.5 * p.delta) : 0.0;
+    constexpr unsigned run_bits = kRun == 32 ? 0xffffffffu : ((1u << kRun) - 1u);
+
+    // edge-aligned point range of this warp
+    const int64_t gw = ((int64_t)blockIdx.x * kLCBlock + threadIdx.x) >> 5;
+    const int64_t nw = (int64_t)gridDim.x * kLCWarps;
+    int64_t e0 = 0, e1 = 0;
+    if (lane == 0) {
+        e0 = lower_edge(p.starts, p.n_edges, (p.n_pts * gw) / nw);
+        e1 = lower_edge(p.starts, p.n_edges, (p.n_pts * (gw + 1)) / nw);
+    }
+    e0 = __shfl_sync(full, e0, 0);
+    e1 = __shfl_sync(full, e1, 0);
+    if (e0 >= e1) return;
+    const int64_t P0 = p.starts[e0], P1 = p.starts[e1];
+
+    int64_t e_g = e0;   // edge containing the group's first point
+    int64_t s_g = P0;   // its start
+    double2 carryA = make_double2(0.0, 0.0);  // original point base-1
+    double2 c_anc = carryA;                   // exact count state after point base-1
+    int c_off = 0;
+    bool c_kept = true;
+
+    for (int64_t base = P0; base < P1; base += kGroup) {
+        const int n = (int)(P1 - base < kGroup ? P1 - base : kGroup);
+        const double2 *pin = p.pin + base;
+        // ---- stage the group coalesced: point i -> row i / kRun, column i % kRun
+        for (int i = lane; i < n; i += 32) row_pt[i / kRun][i % kRun] = pin[i];
+        double2 next_first = make_double2(0.0, 0.0);  // original point base + kGroup
+        if (lane == 31 && base + kGroup < P1) next_first = pin[kGroup];
+
+        // ---- edge starts in (base, base + kGroup] -> per-run bit masks
+        unsigned mask = 0u;       // starts at run positions 0..kRun-1
+        bool start_next = false;  // (lane 31) point base + kGroup starts an edge
+        int64_t e_scan = e_g + 1, s_last = s_g;
+        int n_st = 0;
+        for (;;) {
+            const int64_t idx = e_scan + lane;
+            const int64_t sv = idx <= e1 ? p.starts[idx] : INT64_MAX;
+            const int64_t rel = sv - base;  // >= 1
+            const unsigned in = __ballot_sync(full, rel <= kGroup);
+            for (unsigned b = in; b; b &= b - 1) {
+                const int i = __ffs(b) - 1;
+                const int r = (int)__shfl_sync(full, rel, i);
+                if (r < kGroup) {
+                    if (r / kRun == lane) mask |= 1u << (r % kRun);
+                } else if (lane == 31) {
+                    start_next = true;
+                }
+            }
+            const int c = __popc(in);
+            n_st += c;
+            if (c) s_last = __shfl_sync(full, sv, c - 1);
+            if (in != full) break;
+            e_scan += 32;
+        }
+        if (lane == 0 && s_g == base) mask |= 1u;
+        // the run's last point ends an edge when the next run starts with one
+        const unsigned nb0 = __shfl_down_sync(full, mask, 1) & 1u;
+        const unsigned ends =
+            ((mask >> 1) | ((lane == 31 ? (start_next ? 1u : 0u) : nb0) << (kRun - 1))) & run_bits;
+        // edge of the run's first point: e_g + #starts in (0, kRun*lane]
+        const unsigned mprime = lane == 0 ? (mask & ~1u) : mask;
+        int incl = __popc(mprime);
+        for (int d = 1; d < 32; d <<= 1) {
+            const int o = __shfl_up_sync(full, incl, d);
+            if (lane >= d) incl += o;
+        }
+        const int excl = incl - __popc(mprime);
+        int64_t e_cur = e_g + excl + ((lane > 0 && (mask & 1u)) ? 1 : 0);
+        const int64_t e_first = e_cur;
+        const unsigned prev_mask = __shfl_up_sync(full, mask, 1);
+        __syncwarp();
+
+        // ---- run boundaries, read before any lane overwrites its row
+        const int j0 = lane * kRun;
+        const int len = n - j0 < 0 ? 0 : (n - j0 > kRun ? kRun : n - j0);
+        double2 firstA = make_double2(0.0, 0.0), lastA = firstA, prevA = carryA,
+                prev2 = firstA, nextA_end = next_first;
+        if (len > 0) {
+            firstA = row_pt[lane][0];
+            lastA = row_pt[lane][len - 1];
+            if (lane > 0) {
+                prevA = row_pt[lane - 1][kRun - 1];
+                prev2 = row_pt[lane - 1][kRun - 2];
+            }
+            if (lane < 31 && j0 + kRun < n) nextA_end = row_pt[lane + 1][0];
+        }
+        // speculative anchor: final position of point j0-1 (an endpoint when
+        // it starts an edge or point j0 does)
+        double2 spec_anc = prevA;
+        if (COUNT && lane > 0 && len > 0 && p.lap && !((prev_mask >> (kRun - 1)) & 1u) &&
+            !(mask & 1u))
+            spec_anc = lap_point(prev2, prevA, firstA, p.factor);
+        __syncwarp();
+
+        // ---- phase B: Laplacian + speculative count, sequential per lane.
+        // Offsets before the run's first edge start are relative to the
+        // incoming anchor (0); from the first start on they are absolute.
+        // Lane 0 starts from the exact carried state (absolute throughout).
+        double2 anc = lane == 0 ? c_anc : spec_anc;
+        int off = lane == 0 ? c_off : 0;
+        bool seen_start = false, last_kept = lane == 0 ? c_kept : true;
+        {
+            double2 A = firstA, Al = prevA;
+            for (int t = 0; t < len; ++t) {
+                const double2 An = t + 1 < len ? row_pt[lane][t + 1] : nextA_end;
+                const bool st = (mask >> t) & 1u, en = (ends >> t) & 1u;
+                const double2 F = (p.lap && !st && !en) ? lap_point(Al, A, An, p.factor) : A;
+                row_pt[lane][t] = F;
+                if (COUNT) {
+                    int pv = -1;
+                    if (st) {
+                        anc = F;
+                        off = 0;
+                        pv = 0;
+                        last_kept = true;
+                        if (t > 0) ++e_cur;
+                        seen_start = true;
+                    } else {
+                        const double g2 = dist2_ref(F.x, F.y, anc.x, anc.y);
+                        if (en || !(g2 < lo2)) {
+                            off += pieces_of(g2, hi2);
+                            anc = F;
+                            pv = off;
+                            last_kept = true;
+                        } else {
+                            last_kept = false;
+                        }
+                    }
+                    if (en && (seen_start || lane == 0)) p.counts[e_cur] = (int64_t)off + 1;
+                    row_pos[lane][t] = pv;
+                }
+                Al = A;
+                A = An;
+            }
+        }
+        const int lastlane = (n - 1) / kRun;
+        int val = off;
+        bool end_kept = last_kept;
+        double2 end_anc = anc;
+        if (COUNT) {
+            // ---- phase C: lanes whose speculative anchor was wrong.
+            // Exact: lane 0, empty runs, runs that begin with an edge start.
+            const bool exact = (lane == 0) || len == 0 || (mask & 1u);
+            const int t_fs = seen_start ? __ffs(mask) - 1 : len;  // first start in the run
+            int end_rel = off;  // relative unless seen_start / lane 0
+            bool fix = false;   // decisions before conv_t differ from phase B
+            int conv_t = 0;     // first point after which the walks agree
+            int shift = 0;      // true relative offset = phase-B offset + shift
+            bool eval = !exact;
+            for (int round = 0; round < 34; ++round) {
+                const bool in_kept = __shfl_up_sync(full, end_kept ? 1 : 0, 1) != 0;
+                const double2 in_anc = make_double2(__shfl_up_sync(full, end_anc.x, 1),
+                                                    __shfl_up_sync(full, end_anc.y, 1));
+                bool changed = false;
+                if (eval) {
+                    const double2 old_anc = end_anc;
+                    const bool old_kept = end_kept;
+                    if (in_kept) {  // point j0-1 truly kept: phase B was exact
+                        fix = false;
+                        conv_t = 0;
+                        shift = 0;
+                        end_anc = anc;
+                        end_kept = last_kept;
+                        end_rel = off;
+                    } else {  // re-walk from the true anchor until the walks meet
+                        fix = true;
+                        double2 a2 = in_anc;
+                        int o2 = 0, t = 0;
+                        bool conv = false, k2 = false;
+                        for (; t < t_fs; ++t) {
+                            const double2 F = row_pt[lane][t];
+                            const bool en = (ends >> t) & 1u;
+                            const double g2 = dist2_ref(F.x, F.y, a2.x, a2.y);
+                            k2 = en || !(g2 < lo2);
+                            if (k2) {
+                                o2 += pieces_of(g2, hi2);
+                                a2 = F;
+                                const int spv = row_pos[lane][t];
+                                if (spv >= 0) {  // kept in both walks: identical from here
+                                    conv = true;
+                                    shift = o2 - spv;
+                                    conv_t = t + 1;
+                                    break;
+                                }
+                            }
+                        }
+                        if (!conv && t_fs < len) {  // the edge start resets the state
+                            conv = true;
+                            conv_t = t_fs;
+                            shift = 0;
+                        }
+                        if (conv) {
+                            end_anc = anc;
+                            end_kept = last_kept;
+                            end_rel = seen_start ? off : off + shift;
+                        } else {  // one merge chain through the whole run
+                            conv_t = len;
+                            end_anc = a2;
+                            end_kept = k2;
+                            end_rel = o2;
+                        }
+                    }
+                    changed = old_anc.x != end_anc.x || old_anc.y != end_anc.y ||
+                              old_kept != end_kept;
+                    eval = false;
+                }
+                const unsigned chg = __ballot_sync(full, changed);
+                if (!chg) break;
+                eval = !exact && (((chg << 1) >> lane) & 1u);  // predecessor changed
+            }
+            // absolute offsets: segmented scan, restarting at lanes whose end
+            // offset is absolute (lane 0, or an edge start inside the run)
+            val = end_rel;
+            int flag = (lane == 0 || seen_start) ? 1 : 0;
+            for (int d = 1; d < 32; d <<= 1) {
+                const int ov = __shfl_up_sync(full, val, d);
+                const int of = __shfl_up_sync(full, flag, d);
+                if (lane >= d && !flag) {
+                    val += ov;
+                    flag = of;
+                }
+            }
+            const int in_off = __shfl_up_sync(full, val, 1);  // offset of the incoming anchor
+            const double2 fin_anc = make_double2(__shfl_up_sync(full, end_anc.x, 1),
+                                                 __shfl_up_sync(full, end_anc.y, 1));
+            if (!exact) {
+                // before the first start: re-walk [0, conv_t) from the final
+                // incoming anchor, shift phase B's values after it
+                double2 a2 = fin_anc;
+                int o2 = 0;
+                for (int t = 0; t < t_fs; ++t) {
+                    int v = row_pos[lane][t];
+                    if (fix && t < conv_t) {
+                        const double2 F = row_pt[lane][t];
+                        const double g2 = dist2_ref(F.x, F.y, a2.x, a2.y);
+                        v = -1;
+                        if (((ends >> t) & 1u) || !(g2 < lo2)) {
+                            o2 += pieces_of(g2, hi2);
+                            a2 = F;
+                            v = o2;
+                        }
+                    } else if (v >= 0) {
+                        v += shift;
+                    }
+                    if (v >= 0) v += in_off;
+                    row_pos[lane][t] = v;
+                    if ((ends >> t) & 1u) p.counts[e_first] = (int64_t)v + 1;
+                }
+            }
+        }
+        __syncwarp();
+        // ---- coalesced write-out of the final points (and output codes)
+        for (int i = lane; i < n; i += 32) {
+            p.pout[base + i] = row_pt[i / kRun][i % kRun];
+            if (COUNT) p.pos[base + i] = row_pos[i / kRun][i % kRun];
+        }
+        __syncwarp();
+        // ---- carry the exact state after the group's last point
+        carryA = make_double2(__shfl_sync(full, lastA.x, lastlane), __shfl_sync(full, lastA.y, lastlane));
+        if (COUNT) {
+            c_anc = make_double2(__shfl_sync(full, end_anc.x, lastlane),
+                                 __shfl_sync(full, end_anc.y, lastlane));
+            c_off = __shfl_sync(full, val, lastlane);
+            c_kept = __shfl_sync(full, end_kept ? 1 : 0, lastlane) != 0;
+        }
+        s_g = s_last;
+        e_g += n_st;
+    }
+}
+
+}  // namespace hb
+
+using namespace hb;
+
+// resident blocks (occupancy with this dynamic shared memory), never more
+// warps than there are groups of points
+template <typename K>
+static unsigned lc_grid(K kernel, int64_t groups, size_t smem) {
+    static int per_sm = 0;
+    if (per_sm == 0 &&
+        (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, kLCBlock, smem) !=
+             cudaSuccess ||
+         per_sm < 1))
+        per_sm = 1;
+    int64_t want = (groups + kLCWarps - 1) / kLCWarps;
+    const int64_t cap = (int64_t)device_sm_count() * per_sm;
+    if (want > cap) want = cap;
+    return (unsigned)(want < 1 ? 1 : want);
+}
+
+extern "C" {
+
+int hb_laplacian_count(const double *pts_in, double *pts_out, const int64_t *starts,
+                       int64_t n_edges, int64_t n_pts, double lap_factor, int lap_passes,
+                       double delta, int64_t *counts, int32_t *pos, void *stream) {
+    if (n_edges < 0 || n_pts < 0 || lap_passes < 0 || (counts && (!pos || !(delta > 0))) ||
+        (n_pts > 0 && (!pts_in || !pts_out || !starts)))
+        return set_error(HB_EINVAL, "hb_laplacian_count: bad arguments");
+    if (n_pts == 0 || n_edges == 0) return HB_OK;
+    if (n_pts >= ((int64_t)1 << 31))
+        return set_error(HB_EINVAL, "hb_laplacian_count: more than 2^31 points");
+    cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+    const double *src = pts_in;
+    // all but the last Jacobi sweep: in-place streaming sweeps
+    for (int q = 0; q + 1 < lap_passes; ++q) {
+        PolylinePass sweep{};
+        sweep.pin = reinterpret_cast<const double2 *>(src);
+        sweep.pout = reinterpret_cast<double2 *>(pts_out);
+        sweep.starts = starts;
+        sweep.n_edges = n_edges;
+        sweep.h = -1.0;
+        sweep.factor = lap_factor;
+        sweep.lap = 1;
+        sweep.delta = delta;
+        const int rc = launch_polyline_pass(sweep, st, "hb_laplacian_count(sweep)");
+        if (rc) return rc;
+        src = pts_out;
+    }
+    if (!counts && lap_passes == 0) {
+        if (src != pts_out &&
+            cudaMemcpyAsync(pts_out, src, sizeof(double) * 2 * (size_t)n_pts,
+                            cudaMemcpyDeviceToDevice, st) != cudaSuccess)
+            return check_launch("hb_laplacian_count(copy)", 0);
+        return HB_OK;
+    }
+    LapCount p;
+    p.pin = reinterpret_cast<const double2 *>(src);
+    p.pout = reinterpret_cast<double2 *>(pts_out);
+    p.starts = starts;
+    p.n_edges = n_edges;
+    p.n_pts = n_pts;
+    p.factor = lap_factor;
+    p.lap = lap_passes > 0 ? 1 : 0;
+    p.delta = delta;
+    p.counts = counts;
+    p.pos = pos;
+    const int64_t groups = (n_pts + kGroup - 1) / kGroup;
+    const size_t smem = (size_t)kLCWarps * 32 * kRowPad * (sizeof(double2) + sizeof(int));
+    if (counts) {
+        if (cudaFuncSetAttribute(lapcount_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 (int)smem) != cudaSuccess)
+            return check_launch("hb_laplacian_count(smem)", 0);
+        lapcount_kernel<true><<<lc_grid(lapcount_kernel<true>, groups, smem), kLCBlock, smem, st>>>(p);
+    } else {
+        if (cudaFuncSetAttribute(lapcount_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 (int)smem) != cudaSuccess)
+            return check_launch("hb_laplacian_count(smem)", 0);
+        lapcount_kernel<false><<<lc_grid(lapcount_kernel<false>, groups, smem), kLCBlock, smem, st>>>(p);
+    }
+    return check_launch("hb_laplacian_count");
+}
+
+}  // extern "C"

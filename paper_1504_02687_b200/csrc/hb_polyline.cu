@@ -188,7 +188,11 @@ __device__ __forceinline__ double2 interp_piece(double2 a, double2 x, int k, int
 #define HB_ST_STREAM(p, v) (*(p) = (v))
 #endif
 
-__global__ void __launch_bounds__(kStreamBlock, 3)
+#ifndef HB_EMIT_MINB
+#define HB_EMIT_MINB 3
+#endif
+
+__global__ void __launch_bounds__(kStreamBlock, HB_EMIT_MINB)
 emit_kernel(const double2 *__restrict__ pts, const int64_t *__restrict__ starts,
             int64_t n_edges, const int32_t *__restrict__ pos,
             const int64_t *__restrict__ new_starts, double2 *__restrict__ out,

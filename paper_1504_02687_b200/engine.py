@@ -416,11 +416,9 @@ class BundleEngine:
                     self.m_moved.data_ptr() + 8 * i, ptr(self._partials), s)
             if self.lap_passes > 0 or not last:
                 # Laplacian sweep(s) fused with the next resample count, in place
-                self._k("hb_advect_laplacian", ptr(self.pts), ptr(self.pts), ptr(self.starts),
-                        E, self.n_pts, None, None, None, B, nv, nu, -1.0, float(cfg.epsilon),
-                        MIN_STEP, 0, float(cfg.laplacian_factor), self.lap_passes, self.delta,
-                        None if last else ptr(self.ecounts), None if last else ptr(self.pos),
-                        None, None, s)
+                self._k("hb_laplacian_count", ptr(self.pts), ptr(self.pts), ptr(self.starts),
+                        E, self.n_pts, float(cfg.laplacian_factor), self.lap_passes, self.delta,
+                        None if last else ptr(self.ecounts), None if last else ptr(self.pos), s)
             self._k("hb_reduce_f64", ptr(self._partials), self._partials.numel(),
                     self.m_disp.data_ptr() + 8 * i, s)
             self._k("hb_used_cells", ptr(self.field), ptr(self.peak), B, nv, nu, 0.01,

@@ -425,3 +425,114 @@ def test_accumulate_edges_spec_overlap():
     se = B.initial_sample(g, tr, 3.0)
     f = R.accumulate_edges(se, g, np.eye(1, dtype=np.float32), tr)
     assert f.values.max() == 2.0
+
+
+# ---------------------------------------------------------------------------
+# lane-sequential Laplacian + resample count (hb_lapcount.cu)
+
+def _lc_case(shape: str):
+    """Polylines stressing the speculative per-lane walk: merge chains longer
+    than a 32-point run, pieces > 1, 2-point edges, ranges spanning many
+    1024-point groups."""
+    rng = np.random.default_rng({"random": 3, "chains": 4, "short": 5, "big": 6}[shape])
+    delta = 1.7
+    if shape == "random":
+        pts, starts = _random_polylines(rng, 400, 96, 128, max_pts=700)
+        return pts, starts, delta
+    if shape == "short":
+        lens = rng.integers(2, 5, size=20000)
+    elif shape == "chains":
+        lens = rng.integers(2, 900, size=300)
+    else:  # big: > 1024 points per warp range on a full B200 grid
+        lens = rng.integers(300, 700, size=12000)
+    starts = np.zeros(len(lens) + 1, dtype=np.int64)
+    np.cumsum(lens, out=starts[1:])
+    n = int(starts[-1])
+    step = rng.normal(0, 1.0, size=(n, 2)) * delta
+    u = rng.uniform(size=n)
+    if shape == "chains":
+        # runs of tiny steps (merge chains of random length) and big jumps
+        tiny = np.zeros(n, dtype=bool)
+        i = 0
+        while i < n:
+            k = int(rng.integers(1, 120))
+            if rng.uniform() < 0.5:
+                tiny[i:i + k] = True
+            i += k
+        step[tiny] *= 0.02
+        step[u < 0.03] *= 8.0
+    else:
+        step[u < 0.25] *= 0.05
+        step[u > 0.97] *= 6.0
+    pts = np.cumsum(step, axis=0) + 500.0
+    return pts, starts, delta
+
+
+@pytest.mark.parametrize("inplace", [False, True])
+@pytest.mark.parametrize("shape", ["random", "chains", "short", "big"])
+def test_laplacian_count_vs_oracle(shape, inplace):
+    pts, starts, delta = _lc_case(shape)
+    E, n = len(starts) - 1, len(pts)
+    ref = pts.copy()
+    O.laplacian(ref, starts, 0.5, 1)
+    ref_counts = np.empty(E, dtype=np.int64)
+    O.lib().orc_resample_count(O._p(ref), O._p(starts), delta, O._p(ref_counts), 0, E)
+    dp, ds = dev(pts), dev(starts)
+    out = dp if inplace else torch.empty((n, 2), dtype=torch.float64, device="cuda")
+    counts = torch.full((E,), -7, dtype=torch.int64, device="cuda")
+    pos = torch.full((n,), -7, dtype=torch.int32, device="cuda")
+    N.call("hb_laplacian_count", ptr(dp), ptr(out), ptr(ds), E, n, 0.5, 1, delta, ptr(counts),
+           ptr(pos), stream_ptr())
+    sync()
+    assert np.array_equal(out.cpu().numpy(), ref)
+    assert np.array_equal(counts.cpu().numpy(), ref_counts)
+    # pos: the per-edge (ballot) implementation on the same final points, and
+    # the emitted polylines against the oracle's resample
+    pos2 = torch.empty_like(pos)
+    counts2 = torch.empty_like(counts)
+    moved = torch.zeros(1, dtype=torch.int64, device="cuda")
+    part = torch.zeros(int(N.lib().hb_advect_partials()), dtype=torch.float64, device="cuda")
+    N.call("hb_advect_laplacian", ptr(dev(ref)), ptr(torch.empty_like(out)), ptr(ds), E, n, None,
+           None, None, 1, 3, 3, -1.0, 1e-8, 0.25, 0, 0.5, 0, delta, ptr(counts2), ptr(pos2),
+           ptr(moved), ptr(part), stream_ptr())
+    sync()
+    assert np.array_equal(pos.cpu().numpy(), pos2.cpu().numpy())
+    assert np.array_equal(counts2.cpu().numpy(), ref_counts)
+    if shape in ("random", "chains"):
+        ref_pts, ref_starts = O.resample(ref, starts, delta)
+        ns = torch.zeros(E + 1, dtype=torch.int64, device="cuda")
+        ns[1:] = torch.cumsum(counts, 0)
+        emitted = torch.empty((int(ns[-1].item()), 2), dtype=torch.float64, device="cuda")
+        status = torch.zeros(1, dtype=torch.int32, device="cuda")
+        N.call("hb_resample_emit", ptr(out), ptr(ds), E, n, ptr(pos), ptr(ns), ptr(emitted),
+               None, None, None, 1, 1, ptr(status), None, stream_ptr())
+        sync()
+        assert np.array_equal(ns.cpu().numpy(), ref_starts)
+        assert np.array_equal(emitted.cpu().numpy(), ref_pts)
+
+
+def test_laplacian_count_passes_and_count_only():
+    pts, starts, delta = _lc_case("random")
+    E, n = len(starts) - 1, len(pts)
+    for passes, factor in [(0, 0.5), (3, 0.3)]:
+        ref = pts.copy()
+        if passes:
+            O.laplacian(ref, starts, factor, passes)
+        ref_counts = np.empty(E, dtype=np.int64)
+        O.lib().orc_resample_count(O._p(ref), O._p(starts), delta, O._p(ref_counts), 0, E)
+        out = torch.empty((n, 2), dtype=torch.float64, device="cuda")
+        counts = torch.empty(E, dtype=torch.int64, device="cuda")
+        pos = torch.empty(n, dtype=torch.int32, device="cuda")
+        N.call("hb_laplacian_count", ptr(dev(pts)), ptr(out), ptr(dev(starts)), E, n, factor,
+               passes, delta, ptr(counts), ptr(pos), stream_ptr())
+        sync()
+        assert np.array_equal(out.cpu().numpy(), ref)
+        assert np.array_equal(counts.cpu().numpy(), ref_counts)
+    # Laplacian only (no counts)
+    ref = pts.copy()
+    O.laplacian(ref, starts, 0.5, 1)
+    out = torch.empty((n, 2), dtype=torch.float64, device="cuda")
+    N.call("hb_laplacian_count", ptr(dev(pts)), ptr(out), ptr(dev(starts)), E, n, 0.5, 1, delta,
+           None, None, stream_ptr())
+    sync()
+    assert np.array_equal(out.cpu().numpy(), ref)

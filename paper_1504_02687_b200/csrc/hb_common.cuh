@@ -328,6 +328,17 @@ __device__ __forceinline__ uint64_t encode_seg(int x0, int y0, int dx, int dy, i
 // tile's bucket; everything else -- census mode (no record storage), bucket
 // overflow, non-unit float weights, long or out-of-grid segments -- is
 // rasterised straight into the histogram exactly as before.
+// first e in [0, n] with starts[e] >= v (starts is non-decreasing, starts[n] = N)
+__device__ __forceinline__ int64_t lower_edge(const int64_t *__restrict__ starts, int64_t n,
+                                              int64_t v) {
+    int64_t lo = 0, hi = n;
+    while (lo < hi) {
+        const int64_t mid = (lo + hi) >> 1;
+        if (starts[mid] < v) lo = mid + 1; else hi = mid;
+    }
+    return lo;
+}
+
 // Segment-key table layout: per (group, cell delta) plane, the start cells
 // in 4x4 blocks of 16 consecutive entries (64 B), blocks row-major.  Keys of
 // a bundle (parallel edges a few cells apart, same delta) share blocks, so

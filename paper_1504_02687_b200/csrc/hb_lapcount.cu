@@ -68,17 +68,6 @@ static_assert(kRun >= 2 && kRun <= 32, "run length");
 #define HB_LC_MINB 4
 #endif
 
-// first e in [0, n] with starts[e] >= v (starts is non-decreasing, starts[n] = N)
-__device__ __forceinline__ int64_t lower_edge(const int64_t *__restrict__ starts, int64_t n,
-                                              int64_t v) {
-    int64_t lo = 0, hi = n;
-    while (lo < hi) {
-        const int64_t mid = (lo + hi) >> 1;
-        if (starts[mid] < v) lo = mid + 1; else hi = mid;
-    }
-    return lo;
-}
-
 __device__ __forceinline__ double2 lap_point(double2 l, double2 c, double2 r, double f) {
     // _kernels.py:290-293: mx = 0.5*(p[j-1]+p[j+1]); s = p + f*(mx - p)
     const double mx = dmul(0.5, dadd(l.x, r.x));

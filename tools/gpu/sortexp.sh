@@ -1,5 +1,5 @@
 mkdir -p gpurun_out
-for srt in none srcdst mid; do
+for srt in none srcdst; do
   timeout 400 python tools/kernel_probe.py --config 4 --iters 6 --sort-edges $srt > gpurun_out/probe_sort_$srt.json 2>&1
   python - "$srt" <<'PY'
 import json, sys

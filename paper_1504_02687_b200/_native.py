@@ -55,6 +55,24 @@ def build(verbose: bool = False, out: str = LIB_PATH, defines: tuple = ()) -> st
     return out
 
 
+HOST_IO_SRC = os.path.join(_PKG, "csrc_host", "hb_io.cpp")
+HOST_IO_LIB = os.path.join(LIB_DIR, "libhb_io.so")
+
+
+def build_host_io(verbose: bool = False) -> str:
+    """Compile the host polyline I/O library (g++, no GPU code)."""
+    os.makedirs(LIB_DIR, exist_ok=True)
+    cxx = os.environ.get("CXX", "g++")
+    tmp = HOST_IO_LIB + ".tmp"
+    cmd = [cxx, "-O3", "-std=c++17", "-shared", "-fPIC", "-pthread", "-fvisibility=hidden",
+           HOST_IO_SRC, "-o", tmp]
+    if verbose:
+        print(" ".join(cmd))
+    subprocess.run(cmd, check=True)
+    os.replace(tmp, HOST_IO_LIB)
+    return HOST_IO_LIB
+
+
 _P, _I64, _I, _D, _SZ = (ctypes.c_void_p, ctypes.c_int64, ctypes.c_int,
                          ctypes.c_double, ctypes.c_size_t)
 

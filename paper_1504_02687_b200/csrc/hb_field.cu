@@ -8,20 +8,19 @@
 // (raster.py:147-169).  Pass inputs after the first are non-integer float32
 // values, so the fold ORDER decides the last bits of the table; we keep the
 // reference's order exactly:
-//   col_scan : one thread per (layer, column), sequential in v, coalesced rows
-//   row_scan : one lane per (layer, row), 32x32 tiles staged through shared
-//              memory so global traffic stays coalesced, sequential in u
+//   col_fold : one lane per (layer, column), sequential in v; 32-row tiles
+//              stream through a 4-deep cp.async ring, rows stored coalesced
+//   row_scan : one lane per (layer, row), 32x32 tiles through a 4-deep
+//              cp.async ring so global traffic stays coalesced, sequential in u
 //   box      : one thread per cell, 4 table gathers, IEEE divide, f32 round
 #include "hb_common.cuh"
 
 namespace hb {
 
-constexpr int kColBlock = 128;
-
-// Pass-1 column fold straight from the per-group histograms (int32 counts or
-// float32 sums), mixing the layers on the fly: H[l] = float32(sum_b M[l,b] *
-// G[b]) (float64 sum in ascending b, one rounding -- exact whenever the
-// reference's float32 sums are exact).  M == NULL means identity.
+// Layer mixing of the per-group histograms (int32 counts or float32 sums):
+// H[l] = float32(sum_b M[l,b] * G[b]) (float64 sum in ascending b, one
+// rounding -- exact whenever the reference's float32 sums are exact,
+// SURVEY §8a).  M == NULL means identity.
 template <typename T>
 __device__ __forceinline__ float mixed_value(const T *__restrict__ g, const float *__restrict__ mat,
                                              int nb, int l, int64_t plane, int64_t off) {
@@ -32,81 +31,20 @@ __device__ __forceinline__ float mixed_value(const T *__restrict__ g, const floa
     return __double2float_rn(acc);
 }
 
-// Column folds: the values of a batch of kColBatch rows are loaded (and
-// mixed) first, independent of the running sum, so every thread keeps
-// kColBatch loads in flight; only the float64 adds are sequential.
-constexpr int kColBatch = 16;
-
-template <typename T>
-__global__ void __launch_bounds__(kColBlock)
-col_scan_mix_kernel(const T *__restrict__ groups, const float *__restrict__ mat, int nb, int nv,
-                    int nu, double *__restrict__ table) {
-    const int u = blockIdx.x * kColBlock + threadIdx.x;
-    const int l = blockIdx.y;
-    if (u >= nu) return;
-    const int64_t plane = (int64_t)nv * nu;
-    double *dst = table + l * plane + u;
-    double c = 0.0;
-    for (int v0 = 0; v0 < nv; v0 += kColBatch) {
-        double hv[kColBatch];
-#pragma unroll
-        for (int k = 0; k < kColBatch; ++k)
-            hv[k] = (v0 + k < nv)
-                        ? (double)mixed_value<T>(groups, mat, nb, l, plane, (int64_t)(v0 + k) * nu + u)
-                        : 0.0;
-#pragma unroll
-        for (int k = 0; k < kColBatch; ++k) {
-            if (v0 + k < nv) {
-                c = (v0 + k == 0) ? hv[k] : dadd(c, hv[k]);
-                dst[(int64_t)(v0 + k) * nu] = c;
-            }
-        }
-    }
-}
-
-__global__ void __launch_bounds__(kColBlock)
-col_scan_f32_kernel(const float *__restrict__ in, int nv, int nu,
-                    double *__restrict__ table) {
-    const int u = blockIdx.x * kColBlock + threadIdx.x;
-    const int l = blockIdx.y;
-    if (u >= nu) return;
-    const int64_t plane = (int64_t)nv * nu;
-    const float *src = in + l * plane + u;
-    double *dst = table + l * plane + u;
-    double c = 0.0;
-    float nxt[kColBatch];
-#pragma unroll
-    for (int k = 0; k < kColBatch; ++k) nxt[k] = k < nv ? __ldg(src + (int64_t)k * nu) : 0.0f;
-    for (int v0 = 0; v0 < nv; v0 += kColBatch) {
-        float cur[kColBatch];
-#pragma unroll
-        for (int k = 0; k < kColBatch; ++k) cur[k] = nxt[k];
-        // prefetch the next batch before the dependent adds of this one
-#pragma unroll
-        for (int k = 0; k < kColBatch; ++k) {
-            const int v = v0 + kColBatch + k;
-            nxt[k] = v < nv ? __ldg(src + (int64_t)v * nu) : 0.0f;
-        }
-#pragma unroll
-        for (int k = 0; k < kColBatch; ++k) {
-            if (v0 + k < nv) {
-                const double x = (double)cur[k];
-                c = (v0 + k == 0) ? x : dadd(c, x);
-                dst[(int64_t)(v0 + k) * nu] = c;
-            }
-        }
-    }
-}
-
-// Row fold in place.  Rows are flattened over (layer, v).  A warp owns 32
-// rows and walks them in 32x32 tiles: tile t+1 is copied into shared memory
-// with cp.async while each lane folds its own row of tile t left to right,
-// then tile t is stored back coalesced.
-constexpr int kRowWarps = 2;
-
 __device__ __forceinline__ void cp_async8(void *smem, const void *gmem) {
     const unsigned sa = (unsigned)__cvta_generic_to_shared(smem);
     asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(sa), "l"(gmem));
+}
+// 16 / 4 bytes, zero-filled (nothing read) when !ok
+__device__ __forceinline__ void cp_async16z(void *smem, const void *gmem, bool ok) {
+    const unsigned sa = (unsigned)__cvta_generic_to_shared(smem);
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(sa), "l"(gmem),
+                 "r"(ok ? 16 : 0));
+}
+__device__ __forceinline__ void cp_async4z(void *smem, const void *gmem, bool ok) {
+    const unsigned sa = (unsigned)__cvta_generic_to_shared(smem);
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 4, %2;\n" ::"r"(sa), "l"(gmem),
+                 "r"(ok ? 4 : 0));
 }
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n"); }
 template <int N>
@@ -114,40 +52,135 @@ __device__ __forceinline__ void cp_async_wait() {
     asm volatile("cp.async.wait_group %0;\n" ::"n"(N));
 }
 
-__global__ void __launch_bounds__(kRowWarps * 32)
-row_scan_kernel(double *__restrict__ table, int64_t n_rows, int nu) {
-    __shared__ double tile[kRowWarps][2][32][33];
+// Column fold, C[v][u] = C[v-1][u] + (double)L[v][u] strictly in v.  A warp
+// owns 32 columns (lane = column) and streams them in 32-row tiles through a
+// kColStages-deep cp.async ring in shared memory, so the loads of the next
+// tiles are in flight while the lanes run the dependent float64 adds; every
+// row of C leaves as one coalesced 256-byte store.
+constexpr int kColWarps = 2;  // 32 KB of static shared memory per block
+constexpr int kColStages = 4;
+
+__global__ void __launch_bounds__(kColWarps * 32)
+col_fold_kernel(const float *__restrict__ in, int nbins, int nv, int nu,
+                double *__restrict__ table) {
+    __shared__ __align__(16) float ring[kColWarps][kColStages][32][32];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int64_t r0 = ((int64_t)blockIdx.x * kRowWarps + warp) * 32;
+    const int ncg = (nu + 31) / 32;
+    const int64_t g = (int64_t)blockIdx.x * kColWarps + warp;  // column group
+    if (g >= (int64_t)nbins * ncg) return;
+    const int l = (int)(g / ncg), u0 = (int)(g % ncg) * 32;
+    const int64_t plane = (int64_t)nv * nu;
+    const float *src = in + l * plane + u0;
+    double *dst = table + l * plane + u0;
+    const int ncols = nu - u0 < 32 ? nu - u0 : 32;
+    const bool vec = (nu % 4) == 0;  // rows 16-byte aligned
+    const int ntiles = (nv + 31) / 32;
+    auto issue = [&](int t) {
+        if (t < ntiles) {
+            float (*tt)[32] = ring[warp][t % kColStages];
+            const int r0 = t * 32;
+            if (vec) {  // a row is 8 chunks of 16 B: 4 rows per warp instruction
+                const int ch = lane & 7;
+#pragma unroll
+                for (int k = 0; k < 8; ++k) {
+                    const int r = (lane >> 3) + 4 * k;
+                    const bool ok = r0 + r < nv && ch * 4 < ncols;
+                    cp_async16z(&tt[r][ch * 4], ok ? src + (int64_t)(r0 + r) * nu + ch * 4 : src,
+                                ok);
+                }
+            } else {
+                for (int r = 0; r < 32; ++r) {
+                    const bool ok = r0 + r < nv && lane < ncols;
+                    cp_async4z(&tt[r][lane], ok ? src + (int64_t)(r0 + r) * nu + lane : src, ok);
+                }
+            }
+        }
+        cp_async_commit();  // one group per tile, possibly empty: uniform wait counts
+    };
+#pragma unroll
+    for (int t = 0; t < kColStages - 1; ++t) issue(t);
+    double c = 0.0;
+    for (int t = 0; t < ntiles; ++t) {
+        issue(t + kColStages - 1);
+        cp_async_wait<kColStages - 1>();
+        __syncwarp();
+        const float (*tt)[32] = ring[warp][t % kColStages];
+        const int r0 = t * 32;
+        const int nr = nv - r0 < 32 ? nv - r0 : 32;
+        double *d = dst + (int64_t)r0 * nu;
+        if (nr == 32 && t > 0) {
+            // full tile: all 32 values into registers first, so only the
+            // float64 adds form the dependent chain (in-order issue)
+            float xv[32];
+#pragma unroll
+            for (int r = 0; r < 32; ++r) xv[r] = tt[r][lane];
+#pragma unroll
+            for (int r = 0; r < 32; ++r) {
+                c = dadd(c, (double)xv[r]);
+                if (lane < ncols) d[(int64_t)r * nu + lane] = c;
+            }
+        } else {
+            for (int r = 0; r < nr; ++r) {
+                const double x = (double)tt[r][lane];
+                c = (r0 + r == 0) ? x : dadd(c, x);
+                if (lane < ncols) d[(int64_t)r * nu + lane] = c;
+            }
+        }
+        __syncwarp();
+    }
+}
+
+// Row fold in place, T[v][u] = T[v][u-1] + C[v][u] strictly in u.  Rows are
+// flattened over (layer, v).  A warp owns 32 rows and walks them in 32x32
+// tiles through a kRowStages-deep cp.async ring (rows padded to 33 doubles:
+// the lanes' column walks hit distinct banks); each lane folds its own row
+// of a tile left to right, then the tile is stored back coalesced.
+constexpr int kRowStages = 4;
+
+__global__ void __launch_bounds__(32)
+row_scan_kernel(double *__restrict__ table, int64_t n_rows, int nu) {
+    __shared__ double ring[kRowStages][32][33];
+    const int lane = threadIdx.x & 31;
+    const int64_t r0 = (int64_t)blockIdx.x * 32;
     if (r0 >= n_rows) return;
     const int nr = (int)(n_rows - r0 < 32 ? n_rows - r0 : 32);
     const int ntiles = (nu + 31) / 32;
     auto issue = [&](int t) {
-        const int c0 = t * 32;
-        const int nc = nu - c0 < 32 ? nu - c0 : 32;
-        if (lane < nc)
-            for (int i = 0; i < nr; ++i)
-                cp_async8(&tile[warp][t & 1][i][lane], table + (r0 + i) * nu + c0 + lane);
+        if (t < ntiles) {
+            const int c0 = t * 32;
+            const int nc = nu - c0 < 32 ? nu - c0 : 32;
+            if (lane < nc)
+                for (int i = 0; i < nr; ++i)
+                    cp_async8(&ring[t % kRowStages][i][lane], table + (r0 + i) * nu + c0 + lane);
+        }
         cp_async_commit();
     };
-    issue(0);
+#pragma unroll
+    for (int t = 0; t < kRowStages - 1; ++t) issue(t);
     double carry = 0.0;
     for (int t = 0; t < ntiles; ++t) {
-        if (t + 1 < ntiles) {
-            issue(t + 1);
-            cp_async_wait<1>();
-        } else {
-            cp_async_wait<0>();
-        }
+        issue(t + kRowStages - 1);
+        cp_async_wait<kRowStages - 1>();
         __syncwarp();
-        double (*tt)[33] = tile[warp][t & 1];
+        double (*tt)[33] = ring[t % kRowStages];
         const int c0 = t * 32;
         const int nc = nu - c0 < 32 ? nu - c0 : 32;
         if (lane < nr) {
             double c = carry;
-            for (int k = 0; k < nc; ++k) {
-                c = (c0 + k == 0) ? tt[lane][k] : dadd(c, tt[lane][k]);
-                tt[lane][k] = c;
+            if (nc == 32 && t > 0) {  // full tile: loads first, then the add chain
+                double xv[32];
+#pragma unroll
+                for (int k = 0; k < 32; ++k) xv[k] = tt[lane][k];
+#pragma unroll
+                for (int k = 0; k < 32; ++k) {
+                    c = dadd(c, xv[k]);
+                    tt[lane][k] = c;
+                }
+            } else {
+                for (int k = 0; k < nc; ++k) {
+                    c = (c0 + k == 0) ? tt[lane][k] : dadd(c, tt[lane][k]);
+                    tt[lane][k] = c;
+                }
             }
             carry = c;
         }
@@ -275,6 +308,11 @@ __global__ void used_cells_kernel(const float *__restrict__ rho, const float *__
 
 using namespace hb;
 
+static unsigned col_fold_blocks(int nbins, int nu) {
+    const int64_t groups = (int64_t)nbins * ((nu + 31) / 32);
+    return (unsigned)((groups + kColWarps - 1) / kColWarps);
+}
+
 static inline cudaStream_t as_stream(void *s) { return reinterpret_cast<cudaStream_t>(s); }
 
 extern "C" {
@@ -317,7 +355,6 @@ int hb_smooth(const int32_t *counts, const float *hist, const float *matrix, int
                                                           first ? matrix : nullptr, nbins,
                                                           plane, dst, pk);
         } else {
-            dim3 gc((nu + kColBlock - 1) / kColBlock, nbins);
             const float *fin = first ? hist : src;
             if (mix_first) {
                 // H = float32(M * G) as its own elementwise pass into the stage
@@ -333,10 +370,10 @@ int hb_smooth(const int32_t *counts, const float *hist, const float *matrix, int
                                                               nullptr);
                 fin = stage;
             }
-            col_scan_f32_kernel<<<gc, kColBlock, 0, st>>>(fin, nv, nu, table);
+            col_fold_kernel<<<col_fold_blocks(nbins, nu), kColWarps * 32, 0, st>>>(fin, nbins, nv,
+                                                                                   nu, table);
             const int64_t rows = (int64_t)nbins * nv;
-            const unsigned rb = (unsigned)((rows + 32 * kRowWarps - 1) / (32 * kRowWarps));
-            row_scan_kernel<<<rb, kRowWarps * 32, 0, st>>>(table, rows, nu);
+            row_scan_kernel<<<(unsigned)((rows + 31) / 32), 32, 0, st>>>(table, rows, nu);
             dim3 gb((nu + kBoxBlock - 1) / kBoxBlock, nv, nbins);
             box_kernel<<<gb, kBoxBlock, 0, st>>>(table, nv, nu, r, dst, pk);
         }
@@ -367,11 +404,10 @@ int hb_integral_image(const float *in, int nbins, int nv, int nu, double *table,
     if (!in || !table || nbins < 1 || nv < 1 || nu < 1 || nv > kMaxDim || nu > kMaxDim)
         return set_error(HB_EINVAL, "hb_integral_image: bad arguments");
     cudaStream_t st = as_stream(stream);
-    dim3 gc((nu + kColBlock - 1) / kColBlock, nbins);
-    col_scan_f32_kernel<<<gc, kColBlock, 0, st>>>(in, nv, nu, table);
+    col_fold_kernel<<<col_fold_blocks(nbins, nu), kColWarps * 32, 0, st>>>(in, nbins, nv, nu,
+                                                                           table);
     const int64_t rows = (int64_t)nbins * nv;
-    const unsigned rb = (unsigned)((rows + 32 * kRowWarps - 1) / (32 * kRowWarps));
-    row_scan_kernel<<<rb, kRowWarps * 32, 0, st>>>(table, rows, nu);
+    row_scan_kernel<<<(unsigned)((rows + 31) / 32), 32, 0, st>>>(table, rows, nu);
     return check_launch("hb_integral_image", 2);
 }
 

@@ -536,3 +536,61 @@ def test_laplacian_count_passes_and_count_only():
            None, None, stream_ptr())
     sync()
     assert np.array_equal(out.cpu().numpy(), ref)
+
+
+# ---------------------------------------------------------------------------
+# small and degenerate shapes through the public API, bit-exact vs the oracle
+
+def _graph_from(pos, src, dst, bins=None):
+    from paper_1504_02687_b200.model import Graph
+    return Graph(np.asarray(pos, dtype=np.float64), np.asarray(src, dtype=np.int64),
+                 np.asarray(dst, dtype=np.int64), None, bins)
+
+
+def _small_case(name):
+    from paper_1504_02687_b200.model import BundleConfig
+    rng = np.random.default_rng(len(name))
+    if name == "one_edge":
+        return _graph_from([[0.1, 0.2], [0.9, 0.7]], [0], [1]), BundleConfig(grid_size=32,
+                                                                             iterations=3)
+    if name == "tiny_grid":
+        pos = rng.uniform(0, 1, size=(20, 2))
+        src = rng.integers(0, 20, size=60)
+        dst = (src + 1 + rng.integers(0, 19, size=60)) % 20
+        return _graph_from(pos, src, dst), BundleConfig(grid_size=8, delta=1.0, iterations=4)
+    if name == "two_point_edges":  # delta larger than every edge: 2 samples each
+        pos = rng.uniform(0, 1, size=(300, 2))
+        src = rng.integers(0, 300, size=2000)
+        dst = (src + 1 + rng.integers(0, 299, size=2000)) % 300
+        return _graph_from(pos, src, dst), BundleConfig(grid_size=64, delta=500.0, iterations=3)
+    if name == "dense_short":  # many near-coincident clusters: merges everywhere
+        centers = rng.uniform(0.2, 0.8, size=(4, 2))
+        pos = centers[rng.integers(0, 4, size=400)] + rng.normal(0, 0.01, size=(400, 2))
+        src = rng.integers(0, 400, size=3000)
+        dst = (src + 1 + rng.integers(0, 399, size=3000)) % 400
+        return _graph_from(pos, src, dst), BundleConfig(grid_size=128, delta=0.7, iterations=5,
+                                                        lambda_=1.0)
+    if name == "groups_identity":  # 3 groups, identity matrix, 1-pass smoothing
+        pos = rng.uniform(0, 1, size=(200, 2))
+        src = rng.integers(0, 200, size=1500)
+        dst = (src + 1 + rng.integers(0, 199, size=1500)) % 200
+        bins = rng.integers(0, 3, size=1500)
+        return (_graph_from(pos, src, dst, bins),
+                BundleConfig(grid_size=96, iterations=3, smoothing_passes=1, alpha=0.0))
+    raise KeyError(name)
+
+
+@pytest.mark.parametrize("name", ["one_edge", "tiny_grid", "two_point_edges", "dense_short",
+                                  "groups_identity"])
+def test_bundle_small_shapes_vs_oracle(name):
+    g, cfg = _small_case(name)
+    res = B.bundle(g, cfg)
+    ref = O.bundle_packed(g.positions, g.sources, g.targets, g.weights, g.bins, cfg, None)
+    world = O.materialize(ref, g.positions, g.sources, g.targets)
+    assert np.array_equal(res.sampled_edges.starts, ref.starts)
+    assert np.array_equal(res.sampled_edges.world, world)
+    assert np.array_equal(res.density.values, ref.field)
+    for m, r in zip(res.metrics, ref.metrics):
+        assert (m.moved_points, m.used_cells) == (r.moved_points, r.used_cells)
+        assert m.bandwidth == r.bandwidth
+        np.testing.assert_allclose(m.mean_displacement, r.mean_displacement, rtol=DISP_RTOL)

@@ -9,6 +9,6 @@ for k in emit_kernel advect_flat_kernel; do
   timeout 900 ncu --set full --import-source on --clock-control none -k regex:$k --launch-skip 4 --launch-count 1 \
     -o gpurun_out/pr_$k -f python tools/kernel_probe.py --config 4 --iters 6 > gpurun_out/pr_$k.log 2>&1; echo $k rc=$?
 done
-timeout 900 ncu --set full --import-source on --clock-control none --kernel-name-base mangled -k regex:ILb0ELb1ELb1ELb0E \
+timeout 900 ncu --set full --import-source on --clock-control none -k regex:lapcount_kernel \
   --launch-skip 4 --launch-count 1 -o gpurun_out/pr_lapcount -f python tools/kernel_probe.py --config 4 --iters 6 \
   > gpurun_out/pr_lapcount.log 2>&1; echo lapcount rc=$?

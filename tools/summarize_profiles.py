@@ -103,8 +103,8 @@ def main():
                              npts[5]),
         "hb_advect_points": ("pr_advect_flat_kernel.ncu-rep", "advect of iteration 4 (N4 points)",
                              npts[4]),
-        "hb_advect_laplacian": ("pr_lapcount.ncu-rep",
-                                "Laplacian + resample count of iteration 4 (N4 points)", npts[4]),
+        "hb_laplacian_count": ("pr_lapcount.ncu-rep",
+                               "Laplacian + resample count of iteration 4 (N4 points)", npts[4]),
     }
     summary, traffic = {}, {}
     for api, (rep, what, n) in caps.items():

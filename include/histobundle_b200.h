@@ -43,6 +43,7 @@ extern "C" {
 
 /* status-flag bits written by device kernels (caller-owned int32) */
 #define HB_STATUS_OUT_OF_BOUNDS 1 /* raster.py:57-67 "sample out of bounds" */
+#define HB_STATUS_CAPACITY 4      /* a resample did not fit the output buffer */
 
 /* Tile-binned splatting state (all pointers caller-owned device memory).
  * The grid of every layer is cut into tile x tile cells; a segment is binned
@@ -279,6 +280,21 @@ HB_API int hb_resample_emit(const double *pts, const int64_t *starts,
                      const int32_t *group, const int32_t *weight,
                      int32_t *counts, int nv, int nu, int32_t *status,
                      const hb_tiles *tiles, void *stream);
+
+/* hb_resample_emit for a caller that does not know the output total on the
+ * host: out holds out_capacity points; if new_starts[n_edges] exceeds it the
+ * kernel writes nothing and sets HB_STATUS_CAPACITY in *status. */
+HB_API int hb_resample_emit_cap(const double *pts, const int64_t *starts, int64_t n_edges,
+                                int64_t n_pts, const int32_t *pos, const int64_t *new_starts,
+                                double *out, int64_t out_capacity, const int32_t *group,
+                                const int32_t *weight, int32_t *counts, int nv, int nu,
+                                int32_t *status, const hb_tiles *tiles, void *stream);
+
+/* total_out (nullable) = starts[n_edges]; then starts[e] = min(starts[e],
+ * cap) for every e when the total exceeds cap (keeps kernels that read the
+ * point count from starts in bounds after an HB_STATUS_CAPACITY resample). */
+HB_API int hb_clamp_starts(int64_t *starts, int64_t n_edges, int64_t cap, int64_t *total_out,
+                           void *stream);
 
 /* Per-point probes used by the single-point operator API
  * (bundler.density_at / gradient_at, bundler.py:203-217). */

@@ -112,6 +112,9 @@ SIGNATURES = {
     "hb_scan_counts": (_I, [_P, _I64, _P, _P, _SZ, _P]),
     "hb_resample_emit": (_I, [_P, _P, _I64, _I64, _P, _P, _P, _P, _P, _P, _I, _I, _P,
                               _P, _P]),
+    "hb_resample_emit_cap": (_I, [_P, _P, _I64, _I64, _P, _P, _P, _I64, _P, _P, _P, _I, _I,
+                                  _P, _P, _P]),
+    "hb_clamp_starts": (_I, [_P, _I64, _I64, _P, _P]),
     "hb_probe": (_I, [_P, _I, _I, _P, _I64, _P, _P, _P]),
 }
 

@@ -98,7 +98,10 @@ __global__ void __launch_bounds__(kStreamBlock, HB_FLAT_MINB) advect_flat_kernel
 
     const int64_t gw = ((int64_t)blockIdx.x * kStreamBlock + threadIdx.x) >> 5;
     const int64_t nw = (int64_t)gridDim.x * kFlatWarps;
-    const int64_t tiles = (p.n_pts + 31) >> 5;
+    // the point count is read on the device (n_pts is the buffer bound), so
+    // the launch needs no host copy of the current count
+    const int64_t NP = p.starts[p.n_edges] < p.n_pts ? p.starts[p.n_edges] : p.n_pts;
+    const int64_t tiles = (NP + 31) >> 5;
     const int64_t per = (tiles + nw - 1) / nw;
     int64_t t = gw * per;
     const int64_t t_end = t + per < tiles ? t + per : tiles;
@@ -164,13 +167,13 @@ __global__ void __launch_bounds__(kStreamBlock, HB_FLAT_MINB) advect_flat_kernel
         int64_t s_cur = p.starts[e_cur];
         // one tile of loads in flight ahead of the math
         int64_t i = t * 32 + lane;
-        double2 pt_nx = i < p.n_pts ? p.pts[i] : make_double2(0.0, 0.0);
+        double2 pt_nx = i < NP ? p.pts[i] : make_double2(0.0, 0.0);
         for (; t < t_end; ++t) {
             const int64_t i0 = t * 32;
             i = i0 + lane;
-            const bool valid = i < p.n_pts;
+            const bool valid = i < NP;
             const double2 pt = pt_nx;
-            if (t + 1 < t_end && i + 32 < p.n_pts) pt_nx = p.pts[i + 32];
+            if (t + 1 < t_end && i + 32 < NP) pt_nx = p.pts[i + 32];
             // edge starts strictly after i0, up to i0 + 32
             const int64_t ek = e_cur + 1 + lane;
             const int64_t sv = ek <= p.n_edges ? p.starts[ek] : INT64_MAX;

@@ -105,10 +105,12 @@ __global__ void __launch_bounds__(kLCBlock, HB_LC_MINB) lapcount_kernel(const La
     // edge-aligned point range of this warp
     const int64_t gw = ((int64_t)blockIdx.x * kLCBlock + threadIdx.x) >> 5;
     const int64_t nw = (int64_t)gridDim.x * kLCWarps;
+    // the point count is read on the device (n_pts is the buffer bound)
+    const int64_t NP = p.starts[p.n_edges] < p.n_pts ? p.starts[p.n_edges] : p.n_pts;
     int64_t e0 = 0, e1 = 0;
     if (lane == 0) {
-        e0 = lower_edge(p.starts, p.n_edges, (p.n_pts * gw) / nw);
-        e1 = lower_edge(p.starts, p.n_edges, (p.n_pts * (gw + 1)) / nw);
+        e0 = lower_edge(p.starts, p.n_edges, (NP * gw) / nw);
+        e1 = lower_edge(p.starts, p.n_edges, (NP * (gw + 1)) / nw);
     }
     e0 = __shfl_sync(full, e0, 0);
     e1 = __shfl_sync(full, e1, 0);

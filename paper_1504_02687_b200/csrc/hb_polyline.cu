@@ -198,10 +198,17 @@ emit_kernel(const double2 *__restrict__ pts, const int64_t *__restrict__ starts,
             const int64_t *__restrict__ new_starts, double2 *__restrict__ out,
             const int32_t *__restrict__ group, const int32_t *__restrict__ weight,
             int32_t *__restrict__ hist, int64_t plane, int nv, int nu,
-            int32_t *__restrict__ status, const __grid_constant__ hb_tiles tl, int use_tiles) {
+            int32_t *__restrict__ status, const __grid_constant__ hb_tiles tl, int use_tiles,
+            int64_t out_cap) {
     const hb_tiles *tiles = use_tiles ? &tl : nullptr;
     const unsigned full = 0xffffffffu;
     const int lane = threadIdx.x & 31;
+    // the output total is only known on the device: a resample that would
+    // not fit the caller's buffer writes nothing and raises a status bit
+    if (new_starts[n_edges] > out_cap) {
+        if (blockIdx.x == 0 && threadIdx.x == 0 && status) atomicOr(status, HB_STATUS_CAPACITY);
+        return;
+    }
     const unsigned below_mask = (1u << lane) - 1u;
     const int64_t nwarps = (int64_t)gridDim.x * (kStreamBlock / 32);
     int64_t e = ((int64_t)blockIdx.x * kStreamBlock + threadIdx.x) / 32;
@@ -299,6 +306,21 @@ emit_kernel(const double2 *__restrict__ pts, const int64_t *__restrict__ starts,
             apos = last_pos;
         }
     }
+}
+
+// After a resample whose total exceeded the buffers (status bit set, nothing
+// written), keep every later kernel in bounds: starts[e] = min(starts[e], cap).
+// Two launches: entries below n_edges first (all read the untouched total),
+// then the total itself (copied to total_out, nullable, before clamping).
+__global__ void clamp_starts_kernel(int64_t *__restrict__ starts, int64_t n_edges, int64_t cap) {
+    const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (e < n_edges && starts[n_edges] > cap && starts[e] > cap) starts[e] = cap;
+}
+__global__ void clamp_total_kernel(int64_t *__restrict__ starts, int64_t n_edges, int64_t cap,
+                                   int64_t *__restrict__ total_out) {
+    const int64_t total = starts[n_edges];
+    if (total_out) *total_out = total;
+    if (total > cap) starts[n_edges] = cap;
 }
 
 }  // namespace hb
@@ -445,21 +467,41 @@ int hb_scan_counts(const int64_t *counts, int64_t n_edges, int64_t *new_starts,
     return check_launch("hb_scan_counts", 2);
 }
 
-int hb_resample_emit(const double *pts, const int64_t *starts, int64_t n_edges,
-                     int64_t n_pts, const int32_t *pos, const int64_t *new_starts,
-                     double *out, const int32_t *group, const int32_t *weight,
-                     int32_t *counts, int nv, int nu, int32_t *status, const hb_tiles *tiles,
-                     void *stream) {
-    if (n_edges < 0 || n_pts < 0 ||
+int hb_resample_emit_cap(const double *pts, const int64_t *starts, int64_t n_edges,
+                         int64_t n_pts, const int32_t *pos, const int64_t *new_starts,
+                         double *out, int64_t out_capacity, const int32_t *group,
+                         const int32_t *weight, int32_t *counts, int nv, int nu, int32_t *status,
+                         const hb_tiles *tiles, void *stream) {
+    if (n_edges < 0 || n_pts < 0 || out_capacity < 0 ||
         (n_edges > 0 && (!pts || !starts || !pos || !new_starts || !out)) ||
-        (counts && (!group || !status || nv < 1 || nu < 1 || nv > kMaxDim || nu > kMaxDim)))
+        ((counts || out_capacity < INT64_MAX) && !status) ||
+        (counts && (!group || nv < 1 || nu < 1 || nv > kMaxDim || nu > kMaxDim)))
         return set_error(HB_EINVAL, "hb_resample_emit: bad arguments");
     if (n_edges == 0 || n_pts == 0) return HB_OK;
     emit_kernel<<<persistent_grid(emit_kernel, n_edges), kStreamBlock, 0, as_stream(stream)>>>(
         reinterpret_cast<const double2 *>(pts), starts, n_edges, pos, new_starts,
         reinterpret_cast<double2 *>(out), group, weight, counts, (int64_t)nv * nu, nv, nu,
-        status, tiles ? *tiles : hb_tiles{}, (counts && tiles) ? 1 : 0);
+        status, tiles ? *tiles : hb_tiles{}, (counts && tiles) ? 1 : 0, out_capacity);
     return check_launch("hb_resample_emit");
+}
+
+int hb_resample_emit(const double *pts, const int64_t *starts, int64_t n_edges,
+                     int64_t n_pts, const int32_t *pos, const int64_t *new_starts,
+                     double *out, const int32_t *group, const int32_t *weight,
+                     int32_t *counts, int nv, int nu, int32_t *status, const hb_tiles *tiles,
+                     void *stream) {
+    return hb_resample_emit_cap(pts, starts, n_edges, n_pts, pos, new_starts, out, INT64_MAX,
+                                group, weight, counts, nv, nu, status, tiles, stream);
+}
+
+int hb_clamp_starts(int64_t *starts, int64_t n_edges, int64_t cap, int64_t *total_out,
+                    void *stream) {
+    if (n_edges < 0 || !starts || cap < 0) return set_error(HB_EINVAL, "hb_clamp_starts: bad arguments");
+    if (n_edges > 0)
+        clamp_starts_kernel<<<(unsigned)((n_edges + 255) / 256), 256, 0, as_stream(stream)>>>(
+            starts, n_edges, cap);
+    clamp_total_kernel<<<1, 1, 0, as_stream(stream)>>>(starts, n_edges, cap, total_out);
+    return check_launch("hb_clamp_starts", n_edges > 0 ? 2 : 1);
 }
 
 }  // extern "C"

@@ -100,6 +100,14 @@ def stream_ptr() -> int:
     return torch.cuda.current_stream().cuda_stream
 
 
+class CapacityExceeded(RuntimeError):
+    """A sync-free resample outgrew the point buffers (retried synchronously)."""
+
+    def __init__(self, needed: int):
+        super().__init__(f"resample needs {needed} points")
+        self.needed = needed
+
+
 @dataclass
 class IterationRecord:
     iteration: int
@@ -245,6 +253,17 @@ class BundleEngine:
                 self.tiles, self.tile_mode = geo, 0
                 self.tiles_census = N.HbTiles.from_buffer_copy(geo)
                 self.tiles_census.rec = None
+        # Sync-free iterations: the resample total stays on the device (the
+        # kernels read it from `starts`, the emit checks it against the
+        # buffer), so no host read separates the iterations.  The buffers get
+        # headroom; a run that outgrows them is redone in the synchronous mode.
+        self.async_n = (self.tile_mode != 0 and self.wkind != "float"
+                        and os.environ.get("HB_SYNC_FREE", "1") != "0")
+        self._n_known = True
+        self._init = None
+        if self.async_n:
+            f = float(os.environ.get("HB_ASYNC_CAP_FACTOR", "4"))  # (tests shrink it)
+            self._ensure_capacity(int(f * self.n_pts) + (1 << 20 if f >= 1 else 0))
         self.lap_passes = int(cfg.laplacian_passes)
         self._partials = torch.zeros(int(N.lib().hb_advect_partials()), dtype=torch.float64,
                                      device=dev)
@@ -253,6 +272,7 @@ class BundleEngine:
         self.m_moved = torch.zeros(self.iters, dtype=torch.int64, device=dev)
         self.m_disp = torch.zeros(self.iters, dtype=torch.float64, device=dev)
         self.m_used = torch.zeros(self.iters, dtype=torch.int64, device=dev)
+        self.m_ntot = torch.zeros(self.iters, dtype=torch.int64, device=dev)  # N_i (async)
         self.records: list[IterationRecord] = []
         self._ev: list[tuple[torch.cuda.Event, torch.cuda.Event]] = []
         # optional per-kernel CUDA-event trace: name -> [(start, end, iteration)]
@@ -356,6 +376,9 @@ class BundleEngine:
                 self._k("hb_tiles_plan", ctypes.byref(self.tiles), ptr(self.t_total), s)
             self._k("hb_scan_counts", ptr(self.ecounts), E, ptr(self.starts_alt),
                     ptr(self.scan_ws), self.scan_ws.numel(), s)
+            if self.async_n:
+                self._resample_async(i, s)
+                return
             n_new = int(download(self.starts_alt[E:E + 1])[0]) if E else 0
             self._ensure_capacity(n_new)
             if fused and self.tile_mode == 0:
@@ -390,6 +413,30 @@ class BundleEngine:
                 self._splat(s)
         else:
             self._splat(s)
+
+    def _resample_async(self, i: int, s) -> None:
+        """Emit + splat with the new total left on the device."""
+        E, nv, nu = self.n_edges, self.nv, self.nu
+        tiles = ctypes.byref(self.tiles) if self.tile_mode == 1 else None
+        self._k("hb_resample_emit_cap", ptr(self.pts), ptr(self.starts), E, self.n_pts,
+                ptr(self.pos), ptr(self.starts_alt), ptr(self.alt), self.cap, ptr(self.groups),
+                ptr(self.wint), ptr(self.hist), nv, nu, ptr(self.status), tiles, s)
+        # N_i on the device; starts clamped into the buffers if it did not fit
+        self._k("hb_clamp_starts", ptr(self.starts_alt), E, self.cap,
+                self.m_ntot.data_ptr() + 8 * i, s)
+        if tiles is not None:
+            self._k("hb_segtab_expand", tiles, ptr(self.hist), nv, nu, ptr(self.t_keys), s)
+        self.pts, self.alt = self.alt, self.pts
+        self.starts, self.starts_alt = self.starts_alt, self.starts
+        self.n_pts = self.cap  # kernels read the count from `starts`
+        self._n_known = False
+
+    def sync_count(self) -> int:
+        """Host copy of the current point count (one device read)."""
+        if not self._n_known:
+            self.n_pts = int(download(self.starts[self.n_edges:self.n_edges + 1])[0])
+            self._n_known = True
+        return self.n_pts
 
     def step_field(self) -> IterationRecord:
         """Second half: smoothing of the (global) histogram, advection,
@@ -444,7 +491,8 @@ class BundleEngine:
         ev1 = torch.cuda.Event(enable_timing=True)
         ev1.record()
         self._ev.append((ev0, ev1))
-        rec = IterationRecord(self.iteration, h_i, self.n_pts, self.n_edges)
+        rec = IterationRecord(self.iteration, h_i, self.n_pts if self._n_known else -1,
+                              self.n_edges)
         self.records.append(rec)
         self.iteration += 1
         return rec
@@ -462,6 +510,7 @@ class BundleEngine:
         self.pts[:n0].copy_(pts0)
         self.starts.copy_(starts0)
         self.n_pts = n0
+        self._n_known = True
         self.iteration = 0
         self._tab_on, self._tab_segments, self.key_ratio = True, 0, []
         self.records = []
@@ -469,13 +518,23 @@ class BundleEngine:
         self.m_moved.zero_()
         self.m_disp.zero_()
         self.m_used.zero_()
+        self.m_ntot.zero_()
         self.status.zero_()
 
     def finish_metrics(self) -> list[IterationRecord]:
         """Synchronise once and fill moved/disp/used/seconds of all records."""
         torch.cuda.current_stream().synchronize()
-        if int(download(self.status)[0]) & 1:
+        st = int(download(self.status)[0])
+        if st & 4:
+            raise CapacityExceeded(int(download(self.m_ntot).max()))
+        if st & 1:
             raise ValueError("sample out of bounds: a polyline point left the grid")
+        if any(r.n_points < 0 for r in self.records):
+            ntot = download(self.m_ntot)
+            for r in self.records:
+                if r.n_points < 0:
+                    r.n_points = int(ntot[r.iteration])
+        self.sync_count()
         moved = download(self.m_moved)
         disp = download(self.m_disp)
         used = download(self.m_used)
@@ -487,27 +546,40 @@ class BundleEngine:
         return self.records
 
     def run(self, on_iteration=None) -> list[IterationRecord]:
-        while self.iteration < self.iters:
-            self.step()
-            if on_iteration is not None:
-                on_iteration(self)
-        return self.finish_metrics()
+        if self.async_n and self._init is None and self.iteration == 0:
+            self.keep_initial_state()  # for the (rare) capacity retry
+        start = self.iteration
+        try:
+            while self.iteration < self.iters:
+                self.step()
+                if on_iteration is not None:
+                    on_iteration(self)
+            return self.finish_metrics()
+        except CapacityExceeded as ex:
+            if start != 0 or self._init is None:
+                raise
+            # outgrew the headroom: redo the run synchronously with room to spare
+            self.status.zero_()
+            self.async_n = False
+            self.reset()
+            self._ensure_capacity(int(ex.needed * 1.25))
+            return self.run(on_iteration)
 
     # ------------------------------------------------------------------
     def packed_points(self) -> tuple[torch.Tensor, torch.Tensor]:
-        return self.pts[: self.n_pts], self.starts
+        return self.pts[: self.sync_count()], self.starts
 
     def world_points_nodes(self, origin, cell, node_pos: torch.Tensor, sources: torch.Tensor,
                            targets: torch.Tensor) -> torch.Tensor:
         """grid -> world with the endpoint pins gathered on the device."""
-        out = torch.empty((self.n_pts, 2), dtype=torch.float64, device=self.dev)
+        out = torch.empty((self.sync_count(), 2), dtype=torch.float64, device=self.dev)
         N.call("hb_to_world_nodes", ptr(self.pts), ptr(self.starts), self.n_edges,
                float(origin[0]), float(origin[1]), float(cell), ptr(node_pos), ptr(sources),
                ptr(targets), ptr(out), stream_ptr())
         return out
 
     def world_points(self, origin, cell, src_world=None, dst_world=None) -> torch.Tensor:
-        out = torch.empty((self.n_pts, 2), dtype=torch.float64, device=self.dev)
+        out = torch.empty((self.sync_count(), 2), dtype=torch.float64, device=self.dev)
         sw = None if src_world is None else upload(np.asarray(src_world, np.float64), self.dev)
         dw = None if dst_world is None else upload(np.asarray(dst_world, np.float64), self.dev)
         N.call("hb_to_world", ptr(self.pts), ptr(self.starts), self.n_edges,

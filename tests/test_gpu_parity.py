@@ -594,3 +594,19 @@ def test_bundle_small_shapes_vs_oracle(name):
         assert (m.moved_points, m.used_cells) == (r.moved_points, r.used_cells)
         assert m.bandwidth == r.bandwidth
         np.testing.assert_allclose(m.mean_displacement, r.mean_displacement, rtol=DISP_RTOL)
+
+
+def test_sync_free_capacity_overflow_retries_exactly(monkeypatch):
+    """The sync-free loop keeps N_i on the device; when a resample outgrows
+    the buffers the run restarts synchronously -- same bits either way."""
+    w = workload(1, scale=0.5)
+    cfg = w.config
+    ref = B.bundle(w.graph, cfg, bins=w.bins, matrix=w.matrix)
+    monkeypatch.setenv("HB_ASYNC_CAP_FACTOR", "1.0")  # no headroom: overflows at once
+    res = B.bundle(w.graph, cfg, bins=w.bins, matrix=w.matrix)
+    assert np.array_equal(res.sampled_edges.starts, ref.sampled_edges.starts)
+    assert np.array_equal(res.sampled_edges.world, ref.sampled_edges.world)
+    assert [m.moved_points for m in res.metrics] == [m.moved_points for m in ref.metrics]
+    monkeypatch.setenv("HB_SYNC_FREE", "0")
+    res2 = B.bundle(w.graph, cfg, bins=w.bins, matrix=w.matrix)
+    assert np.array_equal(res2.sampled_edges.world, ref.sampled_edges.world)

@@ -36,6 +36,7 @@ def main():
     eng, tr, _, _ = B.prepare_engine(w.graph, w.config, bins=w.bins, matrix=w.matrix)
     for _ in range(a.iters):
         eng.step()
+    eng.sync_count()
     torch.cuda.synchronize()
     E = eng.n_edges
     st = eng.starts[:E + 1].long()

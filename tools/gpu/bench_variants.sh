@@ -1,10 +1,15 @@
 # usage: bench_variants.sh name...  -- short bench per library variant (same box)
 mkdir -p gpurun_out
 for v in default "$@"; do
-  if [ "$v" = nodefer ]; then export HB_DEFER_LAP=0; else unset HB_DEFER_LAP; fi
-  if [ "$v" != default ] && [ "$v" != nodefer ]; then export HB_B200_LIB=paper_1504_02687_b200/_lib/var_$v/libhb_b200.so; else unset HB_B200_LIB; fi
-  timeout 600 python bench.py --steps 3 --warmup 3 --no-e2e --no-cpu-baseline > gpurun_out/bv_$v.json 2>/dev/null
-  python - "$v" <<'PY'
+  # env:NAME=VALUE variants set an environment switch, others pick a library
+  unset HB_B200_LIB HB_SYNC_FREE HB_FLAT_ADVECT
+  case "$v" in
+    default) ;;
+    env:*) export "${v#env:}" ;;
+    *) export HB_B200_LIB=paper_1504_02687_b200/_lib/var_$v/libhb_b200.so ;;
+  esac
+  timeout 600 python bench.py --steps 3 --warmup 3 --no-e2e --no-cpu-baseline > "gpurun_out/bv_${v//[:=]/_}.json" 2>/dev/null
+  python - "${v//[:=]/_}" <<'PY'
 import json, sys
 v = sys.argv[1]
 d = json.loads([l for l in open(f'gpurun_out/bv_{v}.json') if l.startswith('{')][-1])

@@ -78,6 +78,7 @@ def main():
     eng, tr, _, _ = B.prepare_engine(w.graph, w.config, bins=w.bins, matrix=w.matrix)
     for _ in range(args.iters):
         eng.step()
+    eng.sync_count()
     torch.cuda.synchronize()
     s = stream_ptr()
     E, Bn, nv, nu = eng.n_edges, eng.nbins, eng.nv, eng.nu

@@ -53,77 +53,95 @@ __device__ __forceinline__ void cp_async_wait() {
 }
 
 // Column fold, C[v][u] = C[v-1][u] + (double)L[v][u] strictly in v.  A warp
-// owns 32 columns (lane = column) and streams them in 32-row tiles through a
-// kColStages-deep cp.async ring in shared memory, so the loads of the next
-// tiles are in flight while the lanes run the dependent float64 adds; every
-// row of C leaves as one coalesced 256-byte store.
-constexpr int kColWarps = 2;  // 32 KB of static shared memory per block
+// owns 32*CPL columns (lane = column, CPL independent chains per lane so the
+// float64 add latency of one chain hides behind the others) and streams them
+// in 32-row tiles through a kColStages-deep cp.async ring in shared memory;
+// every row of C leaves as coalesced 256-byte stores.
 constexpr int kColStages = 4;
+// 1 column per lane measured best (config 4 column fold: 20.5 us vs 30.8 us
+// with 2 -- more warps beat interleaved chains on this latency-bound fold)
+#ifndef HB_COL_CPL
+#define HB_COL_CPL 1
+#endif
+constexpr int kColCPL = HB_COL_CPL;
+constexpr int kColW = 32 * kColCPL;                       // columns per warp
+constexpr int kColWarps = kColCPL == 1 ? 2 : 1;           // <= 32 KB static smem
 
 __global__ void __launch_bounds__(kColWarps * 32)
 col_fold_kernel(const float *__restrict__ in, int nbins, int nv, int nu,
                 double *__restrict__ table) {
-    __shared__ __align__(16) float ring[kColWarps][kColStages][32][32];
+    __shared__ __align__(16) float ring[kColWarps][kColStages][32][kColW];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int ncg = (nu + 31) / 32;
+    const int ncg = (nu + kColW - 1) / kColW;
     const int64_t g = (int64_t)blockIdx.x * kColWarps + warp;  // column group
     if (g >= (int64_t)nbins * ncg) return;
-    const int l = (int)(g / ncg), u0 = (int)(g % ncg) * 32;
+    const int l = (int)(g / ncg), u0 = (int)(g % ncg) * kColW;
     const int64_t plane = (int64_t)nv * nu;
     const float *src = in + l * plane + u0;
     double *dst = table + l * plane + u0;
-    const int ncols = nu - u0 < 32 ? nu - u0 : 32;
+    const int ncols = nu - u0 < kColW ? nu - u0 : kColW;
     const bool vec = (nu % 4) == 0;  // rows 16-byte aligned
     const int ntiles = (nv + 31) / 32;
     auto issue = [&](int t) {
         if (t < ntiles) {
-            float (*tt)[32] = ring[warp][t % kColStages];
+            float (*tt)[kColW] = ring[warp][t % kColStages];
             const int r0 = t * 32;
-            if (vec) {  // a row is 8 chunks of 16 B: 4 rows per warp instruction
-                const int ch = lane & 7;
+            if (vec) {  // a row is kColW/4 chunks of 16 B
+                constexpr int chunks = kColW / 4, rows_per = 32 / chunks;
+                const int ch = lane % chunks;
 #pragma unroll
-                for (int k = 0; k < 8; ++k) {
-                    const int r = (lane >> 3) + 4 * k;
+                for (int k = 0; k < 32 / rows_per; ++k) {
+                    const int r = lane / chunks + rows_per * k;
                     const bool ok = r0 + r < nv && ch * 4 < ncols;
                     cp_async16z(&tt[r][ch * 4], ok ? src + (int64_t)(r0 + r) * nu + ch * 4 : src,
                                 ok);
                 }
             } else {
-                for (int r = 0; r < 32; ++r) {
-                    const bool ok = r0 + r < nv && lane < ncols;
-                    cp_async4z(&tt[r][lane], ok ? src + (int64_t)(r0 + r) * nu + lane : src, ok);
-                }
+                for (int r = 0; r < 32; ++r)
+#pragma unroll
+                    for (int k = 0; k < kColCPL; ++k) {
+                        const int cc = lane + 32 * k;
+                        const bool ok = r0 + r < nv && cc < ncols;
+                        cp_async4z(&tt[r][cc], ok ? src + (int64_t)(r0 + r) * nu + cc : src, ok);
+                    }
             }
         }
         cp_async_commit();  // one group per tile, possibly empty: uniform wait counts
     };
 #pragma unroll
     for (int t = 0; t < kColStages - 1; ++t) issue(t);
-    double c = 0.0;
+    double c[kColCPL];
+#pragma unroll
+    for (int k = 0; k < kColCPL; ++k) c[k] = 0.0;
     for (int t = 0; t < ntiles; ++t) {
         issue(t + kColStages - 1);
         cp_async_wait<kColStages - 1>();
         __syncwarp();
-        const float (*tt)[32] = ring[warp][t % kColStages];
+        const float (*tt)[kColW] = ring[warp][t % kColStages];
         const int r0 = t * 32;
         const int nr = nv - r0 < 32 ? nv - r0 : 32;
         double *d = dst + (int64_t)r0 * nu;
         if (nr == 32 && t > 0) {
-            // full tile: all 32 values into registers first, so only the
-            // float64 adds form the dependent chain (in-order issue)
-            float xv[32];
-#pragma unroll
-            for (int r = 0; r < 32; ++r) xv[r] = tt[r][lane];
+            // full tile, unrolled: the CPL chains interleave, so only the
+            // float64 adds of each chain are dependent
 #pragma unroll
             for (int r = 0; r < 32; ++r) {
-                c = dadd(c, (double)xv[r]);
-                if (lane < ncols) d[(int64_t)r * nu + lane] = c;
+#pragma unroll
+                for (int k = 0; k < kColCPL; ++k) {
+                    c[k] = dadd(c[k], (double)tt[r][lane + 32 * k]);
+                    if (lane + 32 * k < ncols) d[lane + 32 * k] = c[k];
+                }
+                d += nu;
             }
         } else {
             for (int r = 0; r < nr; ++r) {
-                const double x = (double)tt[r][lane];
-                c = (r0 + r == 0) ? x : dadd(c, x);
-                if (lane < ncols) d[(int64_t)r * nu + lane] = c;
+#pragma unroll
+                for (int k = 0; k < kColCPL; ++k) {
+                    const double x = (double)tt[r][lane + 32 * k];
+                    c[k] = (r0 + r == 0) ? x : dadd(c[k], x);
+                    if (lane + 32 * k < ncols) d[lane + 32 * k] = c[k];
+                }
+                d += nu;
             }
         }
         __syncwarp();
@@ -167,13 +185,10 @@ row_scan_kernel(double *__restrict__ table, int64_t n_rows, int nu) {
         const int nc = nu - c0 < 32 ? nu - c0 : 32;
         if (lane < nr) {
             double c = carry;
-            if (nc == 32 && t > 0) {  // full tile: loads first, then the add chain
-                double xv[32];
-#pragma unroll
-                for (int k = 0; k < 32; ++k) xv[k] = tt[lane][k];
+            if (nc == 32 && t > 0) {  // full tile, unrolled
 #pragma unroll
                 for (int k = 0; k < 32; ++k) {
-                    c = dadd(c, xv[k]);
+                    c = dadd(c, tt[lane][k]);
                     tt[lane][k] = c;
                 }
             } else {
@@ -187,6 +202,76 @@ row_scan_kernel(double *__restrict__ table, int64_t n_rows, int nu) {
         __syncwarp();
         if (lane < nc)
             for (int i = 0; i < nr; ++i) table[(r0 + i) * nu + c0 + lane] = tt[i][lane];
+        __syncwarp();
+    }
+}
+
+// Row fold for even nu (16-byte aligned rows): rows padded to 34 doubles so
+// 16-byte cp.async / LDS.128 / STS.128 all stay aligned and, in 8-lane
+// phases, bank-conflict free; each lane folds its row two values per shared
+// load, and tiles leave as 16-byte coalesced stores (two rows per warp
+// instruction).
+constexpr int kRowPad2 = 34;
+__global__ void __launch_bounds__(32)
+row_scan2_kernel(double *__restrict__ table, int64_t n_rows, int nu) {
+    __shared__ __align__(16) double ring[kRowStages][32][kRowPad2];
+    const int lane = threadIdx.x & 31;
+    const int64_t r0 = (int64_t)blockIdx.x * 32;
+    if (r0 >= n_rows) return;
+    const int nr = (int)(n_rows - r0 < 32 ? n_rows - r0 : 32);
+    const int ntiles = (nu + 31) / 32;
+    const int half = lane >> 4, q = lane & 15;  // two rows per instruction, 16 x 16 B each
+    auto issue = [&](int t) {
+        if (t < ntiles) {
+            const int c0 = t * 32;
+            const int nc = nu - c0 < 32 ? nu - c0 : 32;  // even
+            double (*tt)[kRowPad2] = ring[t % kRowStages];
+#pragma unroll
+            for (int k = 0; k < 16; ++k) {
+                const int i = 2 * k + half;
+                const bool ok = i < nr && 2 * q < nc;
+                cp_async16z(&tt[i][2 * q], ok ? table + (r0 + i) * nu + c0 + 2 * q : table, ok);
+            }
+        }
+        cp_async_commit();
+    };
+#pragma unroll
+    for (int t = 0; t < kRowStages - 1; ++t) issue(t);
+    double carry = 0.0;
+    for (int t = 0; t < ntiles; ++t) {
+        issue(t + kRowStages - 1);
+        cp_async_wait<kRowStages - 1>();
+        __syncwarp();
+        double (*tt)[kRowPad2] = ring[t % kRowStages];
+        const int c0 = t * 32;
+        const int nc = nu - c0 < 32 ? nu - c0 : 32;
+        if (lane < nr) {
+            double c = carry;
+            double2 *tr = reinterpret_cast<double2 *>(tt[lane]);
+            if (nc == 32 && t > 0) {
+#pragma unroll
+                for (int k = 0; k < 16; ++k) {
+                    const double2 x = tr[k];
+                    const double a = dadd(c, x.x);
+                    c = dadd(a, x.y);
+                    tr[k] = make_double2(a, c);
+                }
+            } else {
+                for (int k = 0; k < nc; ++k) {
+                    c = (c0 + k == 0) ? tt[lane][k] : dadd(c, tt[lane][k]);
+                    tt[lane][k] = c;
+                }
+            }
+            carry = c;
+        }
+        __syncwarp();
+#pragma unroll
+        for (int k = 0; k < 16; ++k) {
+            const int i = 2 * k + half;
+            if (i < nr && 2 * q < nc)
+                *reinterpret_cast<double2 *>(table + (r0 + i) * nu + c0 + 2 * q) =
+                    *reinterpret_cast<const double2 *>(&tt[i][2 * q]);
+        }
         __syncwarp();
     }
 }
@@ -308,8 +393,18 @@ __global__ void used_cells_kernel(const float *__restrict__ rho, const float *__
 
 using namespace hb;
 
+static void launch_row_fold(double *table, int64_t rows, int nu, cudaStream_t st) {
+#ifndef HB_ROW_SCALAR
+    if (nu % 2 == 0) {  // 16-byte aligned rows
+        row_scan2_kernel<<<(unsigned)((rows + 31) / 32), 32, 0, st>>>(table, rows, nu);
+        return;
+    }
+#endif
+    row_scan_kernel<<<(unsigned)((rows + 31) / 32), 32, 0, st>>>(table, rows, nu);
+}
+
 static unsigned col_fold_blocks(int nbins, int nu) {
-    const int64_t groups = (int64_t)nbins * ((nu + 31) / 32);
+    const int64_t groups = (int64_t)nbins * ((nu + kColW - 1) / kColW);
     return (unsigned)((groups + kColWarps - 1) / kColWarps);
 }
 
@@ -373,7 +468,7 @@ int hb_smooth(const int32_t *counts, const float *hist, const float *matrix, int
             col_fold_kernel<<<col_fold_blocks(nbins, nu), kColWarps * 32, 0, st>>>(fin, nbins, nv,
                                                                                    nu, table);
             const int64_t rows = (int64_t)nbins * nv;
-            row_scan_kernel<<<(unsigned)((rows + 31) / 32), 32, 0, st>>>(table, rows, nu);
+            launch_row_fold(table, rows, nu, st);
             dim3 gb((nu + kBoxBlock - 1) / kBoxBlock, nv, nbins);
             box_kernel<<<gb, kBoxBlock, 0, st>>>(table, nv, nu, r, dst, pk);
         }
@@ -407,7 +502,7 @@ int hb_integral_image(const float *in, int nbins, int nv, int nu, double *table,
     col_fold_kernel<<<col_fold_blocks(nbins, nu), kColWarps * 32, 0, st>>>(in, nbins, nv, nu,
                                                                            table);
     const int64_t rows = (int64_t)nbins * nv;
-    row_scan_kernel<<<(unsigned)((rows + 31) / 32), 32, 0, st>>>(table, rows, nu);
+    launch_row_fold(table, rows, nu, st);
     return check_launch("hb_integral_image", 2);
 }
 

@@ -123,6 +123,19 @@ def test_library_rejects_bad_arguments_without_gpu():
     assert b"bad arguments" in lib.hb_last_error()
     assert lib.hb_advect_laplacian(None, None, None, 1, 1, None, None, None, 1, 8, 8, 1.0, 1e-8, 0.25,
                                    0, 0.5, 1, 1.0, None, None, None, None, None) == -1
+    # flat advection: null buffers, a field too small for the interior margin,
+    # a negative step
+    assert lib.hb_advect_points(None, None, 1, 1, None, None, None, 1, 8, 8, 1.0, 1e-8, 0.25, 0,
+                                None, None, None) == -1
+    assert lib.hb_advect_points(None, None, 1, 1, None, None, None, 1, 2, 8, 1.0, 1e-8, 0.25, 0,
+                                None, None, None) == -1
+    # Laplacian + count: counts without pos, multi-pass without an output
+    assert lib.hb_laplacian_count(None, None, None, 1, 1, 0.5, 1, 1.0, None, None, None) == -1
+    assert b"hb_laplacian_count" in lib.hb_last_error()
+    # capacity-checked emit needs a status word; clamp needs starts
+    assert lib.hb_resample_emit_cap(None, None, 1, 1, None, None, None, 10, None, None, None, 1,
+                                    1, None, None, None) == -1
+    assert lib.hb_clamp_starts(None, 4, 10, None, None) == -1
 
 
 def test_tiles_geometry():

@@ -211,7 +211,10 @@ HB_API int64_t hb_advect_partials(void);
  * first step candidate m = h, h/2, ... >= min_step whose bilinear density is
  * >= its own (fixed_step: m = h, always taken).  Points are processed as one
  * flat stream (bit-identical positions to the per-edge form; see
- * hb_advect_flat.cu).  grad_field: nullable hb_grad_field(rho).  Requires
+ * hb_advect_flat.cu).  The points are [starts[0], starts[n_edges]) (so a
+ * sub-range of edges is advected by offsetting starts and edge_layer);
+ * n_pts bounds that range (the buffer size).  grad_field: nullable
+ * hb_grad_field(rho).  Requires
  * nv, nu >= 3 and nbins*nv*nu < 2^31.  moved: u64 accumulator (added to);
  * disp_partials: hb_advect_partials() doubles (zeroed and filled here),
  * summed by hb_reduce_f64.  Follow with hb_advect_laplacian(h < 0) for the
@@ -249,7 +252,9 @@ HB_API int hb_advect_laplacian(const double *pts_in, double *pts_out,
  *   pts_out = laplacian^lap_passes(pts_in)            (may alias pts_in)
  *   counts[e] = output points of polyline e, pos[j] = output index of kept
  *   point j or -1 (when counts != NULL; same outputs as hb_resample_count).
- * One lane-sequential pass (hb_lapcount.cu).  n_pts < 2^31. */
+ * One lane-sequential pass (hb_lapcount.cu).  The points are [starts[0],
+ * starts[n_edges]) (edge sub-ranges by offsetting starts/counts); n_pts
+ * bounds that range (the buffer size) and must be < 2^31. */
 HB_API int hb_laplacian_count(const double *pts_in, double *pts_out, const int64_t *starts,
                               int64_t n_edges, int64_t n_pts, double lap_factor,
                               int lap_passes, double delta, int64_t *counts, int32_t *pos,

@@ -14,6 +14,7 @@ path.
 from __future__ import annotations
 
 import math
+import os
 import time
 from collections.abc import Sequence
 from dataclasses import dataclass
@@ -229,7 +230,23 @@ def bundle(graph: Graph, config: BundleConfig | None = None, *,
     """
     del workers
     cfg, bins_arr, matrix = _resolve(graph, config, bins, matrix)
-    run = _run_engine(graph, cfg, bins_arr, matrix, _fixed_step, on_iteration, group)
+    if (on_iteration is None and D.rank_world(group)[1] == 1
+            and os.environ.get("HB_STREAM_OUT", "1") != "0"):
+        # one GPU: the last iteration streams its polylines to the host while
+        # the remaining edge chunks are still being advected
+        t0 = time.perf_counter()
+        eng, tr, _, _ = _setup(graph, cfg, bins_arr, matrix, _fixed_step, group, 2.0)
+        if eng.node_arrays is not None:
+            world, recs = eng.run_streamed(tr.origin, tr.cell_size, *eng.node_arrays)
+            starts = download(eng.starts)
+            field = DensityField(tr, download(eng.field))
+            metrics = _metrics(recs, group)
+            return BundleResult(graph, PackedPolylines(world, starts), field, metrics,
+                                sum(m.seconds for m in metrics))
+        recs = eng.run()
+        run = _Run(eng, tr, 0, graph.n_edges, recs, time.perf_counter() - t0)
+    else:
+        run = _run_engine(graph, cfg, bins_arr, matrix, _fixed_step, on_iteration, group)
     eng, tr = run.engine, run.transform
     if eng.node_arrays is not None:
         world_dev = eng.world_points_nodes(tr.origin, tr.cell_size, *eng.node_arrays)

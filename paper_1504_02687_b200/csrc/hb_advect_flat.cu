@@ -100,8 +100,11 @@ __global__ void __launch_bounds__(kStreamBlock, HB_FLAT_MINB) advect_flat_kernel
     const int64_t nw = (int64_t)gridDim.x * kFlatWarps;
     // the point count is read on the device (n_pts is the buffer bound), so
     // the launch needs no host copy of the current count
+    // points [starts[0], starts[n_edges]) -- an edge sub-range may start
+    // anywhere -- clamped to the buffer bound n_pts
+    const int64_t P_lo = p.starts[0];
     const int64_t NP = p.starts[p.n_edges] < p.n_pts ? p.starts[p.n_edges] : p.n_pts;
-    const int64_t tiles = (NP + 31) >> 5;
+    const int64_t tiles = NP > P_lo ? (NP - P_lo + 31) >> 5 : 0;
     const int64_t per = (tiles + nw - 1) / nw;
     int64_t t = gw * per;
     const int64_t t_end = t + per < tiles ? t + per : tiles;
@@ -155,7 +158,7 @@ __global__ void __launch_bounds__(kStreamBlock, HB_FLAT_MINB) advect_flat_kernel
         // edge cursor: the edge containing point 32*t (last e: starts[e] <= i0)
         int64_t e_cur = 0;
         if (lane == 0) {
-            const int64_t i0 = t * 32;
+            const int64_t i0 = P_lo + t * 32;
             int64_t lo = 0, hi = p.n_edges - 1;
             while (lo < hi) {
                 const int64_t mid = (lo + hi + 1) >> 1;
@@ -166,10 +169,10 @@ __global__ void __launch_bounds__(kStreamBlock, HB_FLAT_MINB) advect_flat_kernel
         e_cur = __shfl_sync(full, e_cur, 0);
         int64_t s_cur = p.starts[e_cur];
         // one tile of loads in flight ahead of the math
-        int64_t i = t * 32 + lane;
+        int64_t i = P_lo + t * 32 + lane;
         double2 pt_nx = i < NP ? p.pts[i] : make_double2(0.0, 0.0);
         for (; t < t_end; ++t) {
-            const int64_t i0 = t * 32;
+            const int64_t i0 = P_lo + t * 32;
             i = i0 + lane;
             const bool valid = i < NP;
             const double2 pt = pt_nx;

@@ -106,11 +106,14 @@ __global__ void __launch_bounds__(kLCBlock, HB_LC_MINB) lapcount_kernel(const La
     const int64_t gw = ((int64_t)blockIdx.x * kLCBlock + threadIdx.x) >> 5;
     const int64_t nw = (int64_t)gridDim.x * kLCWarps;
     // the point count is read on the device (n_pts is the buffer bound)
+    // points [starts[0], starts[n_edges]) (an edge sub-range may start anywhere)
+    const int64_t P_lo = p.starts[0];
     const int64_t NP = p.starts[p.n_edges] < p.n_pts ? p.starts[p.n_edges] : p.n_pts;
+    const int64_t span = NP > P_lo ? NP - P_lo : 0;
     int64_t e0 = 0, e1 = 0;
     if (lane == 0) {
-        e0 = lower_edge(p.starts, p.n_edges, (NP * gw) / nw);
-        e1 = lower_edge(p.starts, p.n_edges, (NP * (gw + 1)) / nw);
+        e0 = lower_edge(p.starts, p.n_edges, P_lo + (span * gw) / nw);
+        e1 = lower_edge(p.starts, p.n_edges, P_lo + (span * (gw + 1)) / nw);
     }
     e0 = __shfl_sync(full, e0, 0);
     e1 = __shfl_sync(full, e1, 0);

@@ -460,15 +460,7 @@ class BundleEngine:
         if self.gfield is not None:
             self._k("hb_grad_field", ptr(self.field), B, nv, nu, ptr(self.gfield), s)
         if self.flat_advect:
-            self._k("hb_advect_points", ptr(self.pts), ptr(self.starts), E, self.n_pts,
-                    ptr(self.groups), ptr(self.field), ptr(self.gfield), B, nv, nu,
-                    float(h_i), float(cfg.epsilon), MIN_STEP, int(self.fixed_step),
-                    self.m_moved.data_ptr() + 8 * i, ptr(self._partials), s)
-            if self.lap_passes > 0 or not last:
-                # Laplacian sweep(s) fused with the next resample count, in place
-                self._k("hb_laplacian_count", ptr(self.pts), ptr(self.pts), ptr(self.starts),
-                        E, self.n_pts, float(cfg.laplacian_factor), self.lap_passes, self.delta,
-                        None if last else ptr(self.ecounts), None if last else ptr(self.pos), s)
+            self._field_points(i, h_i, 0, E, last)
             self._k("hb_reduce_f64", ptr(self._partials), self._partials.numel(),
                     self.m_disp.data_ptr() + 8 * i, s)
             self._k("hb_used_cells", ptr(self.field), ptr(self.peak), B, nv, nu, 0.01,
@@ -489,6 +481,94 @@ class BundleEngine:
         self._k("hb_used_cells", ptr(self.field), ptr(self.peak), B, nv, nu, 0.01,
                 self.m_used.data_ptr() + 8 * i, s)
         return self._close_iteration(ev0, h_i)
+
+    def _field_points(self, i: int, h_i: float, e_lo: int, e_hi: int, last: bool) -> None:
+        """Flat advection + Laplacian (+ next resample count) of edges
+        [e_lo, e_hi), in place; disp partials left in self._partials."""
+        cfg, s = self.cfg, stream_ptr()
+        B, nv, nu = self.nbins, self.nv, self.nu
+        ne = e_hi - e_lo
+        st = self.starts.data_ptr() + 8 * e_lo
+        self._k("hb_advect_points", ptr(self.pts), st, ne, self.n_pts,
+                self.groups.data_ptr() + 4 * e_lo, ptr(self.field), ptr(self.gfield), B, nv, nu,
+                float(h_i), float(cfg.epsilon), MIN_STEP, int(self.fixed_step),
+                self.m_moved.data_ptr() + 8 * i, ptr(self._partials), s)
+        if self.lap_passes > 0 or not last:
+            # Laplacian sweep(s) fused with the next resample count, in place
+            self._k("hb_laplacian_count", ptr(self.pts), ptr(self.pts), st, ne, self.n_pts,
+                    float(cfg.laplacian_factor), self.lap_passes, self.delta,
+                    None if last else self.ecounts.data_ptr() + 8 * e_lo,
+                    None if last else ptr(self.pos), s)
+
+    def run_streamed(self, origin, cell, node_pos: torch.Tensor, sources: torch.Tensor,
+                     targets: torch.Tensor, chunks: int = 8):
+        """run() + world_points_nodes() + the host copy, with the last
+        iteration's advection, Laplacian and grid -> world conversion done
+        in edge chunks whose device -> host copies (pinned, side stream)
+        overlap the next chunk's kernels.  Returns (host world (N,2) numpy,
+        records).  Results are those of run(): points are independent per
+        edge (the displacement metric sums in chunk order)."""
+        if not self.flat_advect or self.iters < 1 or self.n_edges < chunks:
+            self.run()
+            return download_pinned(self.world_points_nodes(origin, cell, node_pos, sources,
+                                                           targets)), self.records
+        if self.async_n and self._init is None and self.iteration == 0:
+            self.keep_initial_state()
+        try:
+            while self.iteration < self.iters - 1:
+                self.step()
+            out = self._last_iteration_streamed(origin, cell, node_pos, sources, targets, chunks)
+            return out, self.finish_metrics()
+        except CapacityExceeded as ex:
+            self.status.zero_()
+            self.async_n = False
+            self.reset()
+            self._ensure_capacity(int(ex.needed * 1.25))
+            return self.run_streamed(origin, cell, node_pos, sources, targets, chunks)
+
+    def _last_iteration_streamed(self, origin, cell, node_pos, sources, targets, chunks):
+        E, B, nv, nu, s = self.n_edges, self.nbins, self.nv, self.nu, stream_ptr()
+        self.step_splat()
+        i, cfg = self.iteration, self.cfg
+        ev0 = self._ev_open
+        is_int = self.wkind != "float"
+        self._k("hb_smooth", ptr(self.hist) if is_int else None,
+                None if is_int else ptr(self.hist), ptr(self.mat_dev), B, nv, nu,
+                self.radii.data_ptr(), int(self.radii.numel()), ptr(self.field),
+                ptr(self.smooth_ws), self.smooth_ws.numel(), ptr(self.peak), s)
+        if self.gfield is not None:
+            self._k("hb_grad_field", ptr(self.field), B, nv, nu, ptr(self.gfield), s)
+        h_i = cfg.lambda_ ** i * cfg.h_max
+        n = self.sync_count()  # one read: sizes the host buffer
+        cuts = [E * k // chunks for k in range(chunks + 1)]
+        bounds = download(self.starts[torch.tensor(cuts, device=self.dev)])
+        world = torch.empty((n, 2), dtype=torch.float64, device=self.dev)
+        host = torch.empty((n, 2), dtype=torch.float64, pin_memory=True)
+        IO_BYTES["d2h"] += n * 16
+        disp = torch.zeros(chunks, dtype=torch.float64, device=self.dev)
+        copy = torch.cuda.Stream(device=self.dev)
+        cur = torch.cuda.current_stream()
+        for k in range(chunks):
+            e_lo, e_hi = cuts[k], cuts[k + 1]
+            self._field_points(i, h_i, e_lo, e_hi, True)
+            self._k("hb_reduce_f64", ptr(self._partials), self._partials.numel(),
+                    disp.data_ptr() + 8 * k, s)
+            self._k("hb_to_world_nodes", ptr(self.pts), self.starts.data_ptr() + 8 * e_lo,
+                    e_hi - e_lo, float(origin[0]), float(origin[1]), float(cell), ptr(node_pos),
+                    sources.data_ptr() + 8 * e_lo, targets.data_ptr() + 8 * e_lo, ptr(world), s)
+            a, b = int(bounds[k]), int(bounds[k + 1])
+            done = torch.cuda.Event()
+            done.record(cur)
+            copy.wait_event(done)
+            with torch.cuda.stream(copy):
+                host[a:b].copy_(world[a:b], non_blocking=True)
+        self._k("hb_reduce_f64", ptr(disp), chunks, self.m_disp.data_ptr() + 8 * i, s)
+        self._k("hb_used_cells", ptr(self.field), ptr(self.peak), B, nv, nu, 0.01,
+                self.m_used.data_ptr() + 8 * i, s)
+        self._close_iteration(ev0, h_i)
+        cur.wait_stream(copy)  # the host buffer is complete once the stream is
+        world.record_stream(copy)
+        return host.numpy()
 
     def _close_iteration(self, ev0, h_i: float) -> IterationRecord:
         ev1 = torch.cuda.Event(enable_timing=True)

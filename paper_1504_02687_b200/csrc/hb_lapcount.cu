@@ -76,9 +76,11 @@ __device__ __forceinline__ double2 lap_point(double2 l, double2 c, double2 r, do
 }
 
 __device__ __forceinline__ int pieces_of(double g2, double hi2) {
-    // while (g > hi) { g *= 0.5; pieces *= 2; } on squared gaps (4^k scaling)
-    double t = hi2;
-    int pieces = 1;
+    // while (g > hi) { g *= 0.5; pieces *= 2; } on squared gaps (4^k scaling);
+    // one compare for the common single piece
+    if (!(g2 > hi2)) return 1;
+    double t = dmul(hi2, 4.0);
+    int pieces = 2;
     while (g2 > t) {
         t = dmul(t, 4.0);
         pieces *= 2;
@@ -209,8 +211,8 @@ __global__ void __launch_bounds__(kLCBlock, HB_LC_MINB) lapcount_kernel(const La
         bool seen_start = false, last_kept = lane == 0 ? c_kept : true;
         {
             double2 A = firstA, Al = prevA;
-            for (int t = 0; t < len; ++t) {
-                const double2 An = t + 1 < len ? row_pt[lane][t + 1] : nextA_end;
+            // one point of the walk (full runs unroll it: no loop-carried select)
+            auto walk = [&](int t, const double2 An) {
                 const bool st = (mask >> t) & 1u, en = (ends >> t) & 1u;
                 const double2 F = (p.lap && !st && !en) ? lap_point(Al, A, An, p.factor) : A;
                 row_pt[lane][t] = F;
@@ -239,6 +241,13 @@ __global__ void __launch_bounds__(kLCBlock, HB_LC_MINB) lapcount_kernel(const La
                 }
                 Al = A;
                 A = An;
+            };
+            if (len == kRun) {
+#pragma unroll
+                for (int t = 0; t < kRun; ++t)
+                    walk(t, t + 1 < kRun ? row_pt[lane][t + 1] : nextA_end);
+            } else {
+                for (int t = 0; t < len; ++t) walk(t, t + 1 < len ? row_pt[lane][t + 1] : nextA_end);
             }
         }
         const int lastlane = (n - 1) / kRun;

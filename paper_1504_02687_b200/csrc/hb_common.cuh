@@ -376,7 +376,7 @@ __device__ __forceinline__ void bin_or_splat(bool has, double px0, double py0, d
                 // so the index fits 32-bit arithmetic)
                 const unsigned D = 2 * H + 1;
                 const unsigned dir = (unsigned)grp * D * D + (unsigned)((dy + H) * D + (dx + H));
-                atomicAdd(tl->tab + segtab_index(dir, x0, y0, nv, nu), (unsigned)iw);
+atomicAdd(tl->tab + segtab_index(dir, x0, y0, nv, nu), (unsigned)iw);
                 direct = false;
             }
         }

@@ -241,6 +241,11 @@ static_assert(kExTY <= 128 && kExTY % 4 == 0, "tiles are whole 4x4 block rows; 7
 constexpr int kExUnroll = HB_EX_UNROLL;      // table loads in flight per thread per round
 constexpr int kExRound = kExpandBlock * kExUnroll * 4;  // max keys found per round
 constexpr int kExBuf = 2 * kExRound;                    // compacted key buffer
+#ifdef HB_EX_STREAM
+#define HB_EX_LOAD(p) __ldcs(p)
+#else
+#define HB_EX_LOAD(p) (*(p))
+#endif
 
 // One block per (start-cell tile, group).  The block scans every delta plane
 // of the key table over its tile (aligned uint4 rows), zeroing what it reads
@@ -291,58 +296,80 @@ segtab_expand_kernel(const __grid_constant__ hb_tiles t, int32_t *__restrict__ c
         }
     };
 
-    // block-uniform trip count: the body has warp shuffles and a barrier
-    for (int base0 = 0; base0 < total; base0 += kExpandBlock * kExUnroll) {
-        const int base = base0 + (int)threadIdx.x;
-        uint4 v[kExUnroll];
-#pragma unroll
-        for (int k = 0; k < kExUnroll; ++k) {
-            const int idx = base + k * kExpandBlock;
-            const int plane = idx / per_plane, rem = idx - plane * per_plane;
-            // rem -> (block row, block, cell row), cell row fastest
-            const int ly = rem & 3, bc = (rem >> 2) % c4, br = (rem >> 2) / c4;
-            const int y = ty0 + br * 4 + ly, x = tx0 + bc * 4;
-            v[k] = make_uint4(0u, 0u, 0u, 0u);
-            if (idx < total && y < nv && x < nu) v[k] = tab4[q4(plane, br, bc, ly)];
-        }
-        int mine = 0;
-#pragma unroll
-        for (int k = 0; k < kExUnroll; ++k)
-            mine += (v[k].x != 0u) + (v[k].y != 0u) + (v[k].z != 0u) + (v[k].w != 0u);
-        // warp-aggregated slot reservation
-        int incl = mine;
-        for (int d = 1; d < 32; d <<= 1) {
-            const int o = __shfl_up_sync(0xffffffffu, incl, d);
-            if (lane >= d) incl += o;
-        }
-        int slot = 0;
-        if (lane == 31 && incl) slot = atomicAdd(&nbuf, incl);
-        slot = __shfl_sync(0xffffffffu, slot, 31) + incl - mine;
-        if (mine) {
-            keys += mine;
+    // Scan n table rows (uint4 = 4 cells of one cell row); decode(idx, plane,
+    // br, bc, ly) names row idx.  Block-uniform trip count: the body has warp
+    // shuffles and a barrier.
+    auto consume = [&](int n, auto decode) {
+        uint4 v[kExUnroll], vn[kExUnroll];
+        int64_t at[kExUnroll], atn[kExUnroll];
+        unsigned pkey[kExUnroll], pkn[kExUnroll];
+        auto load = [&](int base) {  // rows of the round starting at base
 #pragma unroll
             for (int k = 0; k < kExUnroll; ++k) {
-                if ((v[k].x | v[k].y | v[k].z | v[k].w) == 0u) continue;
                 const int idx = base + k * kExpandBlock;
-                const int plane = idx / per_plane, rem = idx - plane * per_plane;
-                const int ly = rem & 3, bc = (rem >> 2) % c4, br = (rem >> 2) / c4;
-                tab4[q4(plane, br, bc, ly)] = make_uint4(0u, 0u, 0u, 0u);
-                const int row = br * 4 + ly, xb = bc * 4;
-                const unsigned pk = ((unsigned)plane << 13) | ((unsigned)row << 6);
-                if (v[k].x) buf[slot++] = make_uint2(pk | (unsigned)(xb + 0), v[k].x);
-                if (v[k].y) buf[slot++] = make_uint2(pk | (unsigned)(xb + 1), v[k].y);
-                if (v[k].z) buf[slot++] = make_uint2(pk | (unsigned)(xb + 2), v[k].z);
-                if (v[k].w) buf[slot++] = make_uint2(pk | (unsigned)(xb + 3), v[k].w);
+                int plane = 0, br = 0, bc = 0, ly = 0;
+                vn[k] = make_uint4(0u, 0u, 0u, 0u);
+                atn[k] = -1;
+                pkn[k] = 0;
+                if (idx < n && decode(idx, plane, br, bc, ly)) {
+                    atn[k] = q4(plane, br, bc, ly);
+                    vn[k] = HB_EX_LOAD(tab4 + atn[k]);
+                    pkn[k] = ((unsigned)plane << 13) | ((unsigned)(br * 4 + ly) << 6) |
+                             (unsigned)(bc * 4);
+                }
+            }
+        };
+        constexpr int kStep = kExpandBlock * kExUnroll;
+        if (n > 0) load((int)threadIdx.x);
+        for (int base0 = 0; base0 < n; base0 += kStep) {
+#pragma unroll
+            for (int k = 0; k < kExUnroll; ++k) v[k] = vn[k], at[k] = atn[k], pkey[k] = pkn[k];
+            // the next round's rows are in flight while this round compacts
+            if (base0 + kStep < n) load(base0 + kStep + (int)threadIdx.x);
+            int mine = 0;
+#pragma unroll
+            for (int k = 0; k < kExUnroll; ++k)
+                mine += (v[k].x != 0u) + (v[k].y != 0u) + (v[k].z != 0u) + (v[k].w != 0u);
+            // warp-aggregated slot reservation
+            int incl = mine;
+            for (int d = 1; d < 32; d <<= 1) {
+                const int o = __shfl_up_sync(0xffffffffu, incl, d);
+                if (lane >= d) incl += o;
+            }
+            int slot = 0;
+            if (lane == 31 && incl) slot = atomicAdd(&nbuf, incl);
+            slot = __shfl_sync(0xffffffffu, slot, 31) + incl - mine;
+            if (mine) {
+                keys += mine;
+#pragma unroll
+                for (int k = 0; k < kExUnroll; ++k) {
+                    if ((v[k].x | v[k].y | v[k].z | v[k].w) == 0u) continue;
+                    tab4[at[k]] = make_uint4(0u, 0u, 0u, 0u);
+                    const unsigned pk = pkey[k];
+                    if (v[k].x) buf[slot++] = make_uint2(pk + 0u, v[k].x);
+                    if (v[k].y) buf[slot++] = make_uint2(pk + 1u, v[k].y);
+                    if (v[k].z) buf[slot++] = make_uint2(pk + 2u, v[k].z);
+                    if (v[k].w) buf[slot++] = make_uint2(pk + 3u, v[k].w);
+                }
+            }
+            __syncthreads();
+            if (nbuf > kExBuf - kExRound) {  // (block-uniform) the next round could overflow
+                rasterise();
+                __syncthreads();
+                if (threadIdx.x == 0) nbuf = 0;
+                __syncthreads();
             }
         }
-        __syncthreads();
-        if (nbuf > kExBuf - kExRound) {  // (block-uniform) the next round could overflow
-            rasterise();
-            __syncthreads();
-            if (threadIdx.x == 0) nbuf = 0;
-            __syncthreads();
-        }
-    }
+    };
+
+    // every row of every plane over the tile
+    consume(total, [&](int idx, int &plane, int &br, int &bc, int &ly) {
+        plane = idx / per_plane;
+        const int rem = idx - plane * per_plane;
+        // rem -> (block row, block, cell row), cell row fastest
+        ly = rem & 3, bc = (rem >> 2) % c4, br = (rem >> 2) / c4;
+        return ty0 + br * 4 + ly < nv && tx0 + bc * 4 < nu;
+    });
     rasterise();
     __syncthreads();
     int32_t *layer = counts + (int64_t)g * nv * nu;

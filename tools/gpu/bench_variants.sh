@@ -1,4 +1,5 @@
 # usage: bench_variants.sh name...  -- short bench per library variant (same box)
+# BV_ARGS: extra bench.py arguments (e.g. "--scale 0.125")
 mkdir -p gpurun_out
 for v in default "$@"; do
   # env:NAME=VALUE variants set an environment switch, others pick a library
@@ -8,7 +9,7 @@ for v in default "$@"; do
     env:*) export "${v#env:}" ;;
     *) export HB_B200_LIB=paper_1504_02687_b200/_lib/var_$v/libhb_b200.so ;;
   esac
-  timeout 600 python bench.py --steps 3 --warmup 3 --no-e2e --no-cpu-baseline > "gpurun_out/bv_${v//[:=]/_}.json" 2>/dev/null
+  timeout 600 python bench.py --steps 3 --warmup 3 --no-e2e --no-cpu-baseline $BV_ARGS > "gpurun_out/bv_${v//[:=]/_}.json" 2>/dev/null
   python - "${v//[:=]/_}" <<'PY'
 import json, sys
 v = sys.argv[1]

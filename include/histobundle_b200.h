@@ -194,12 +194,14 @@ HB_API int hb_integral_image(const float *in, int nbins, int nv, int nu, double 
 HB_API int hb_used_cells(const float *rho, const float *layer_peak, int nbins, int nv,
                   int nu, double rel, unsigned long long *count, void *stream);
 
-/* Quad advection field: B*V*U records of three float4 {Q, GX, GY} (48 bytes
- * per cell, 16-byte aligned): Q = rho at the cell's 2x2 corners, GX/GY = the
- * float32 central differences of _cell_gradient (_kernels.py:101-114) at
- * those corners.  Optional input of hb_advect_points / hb_advect_laplacian
- * (same results; one 48-byte record per gradient sample and one 16-byte
- * load per bilinear sample instead of ~9 scattered ones). */
+/* Quad advection field: B*V*U records {Q, GX, GY} of three float4 (48
+ * bytes per cell, 16-byte aligned; size hb_grad_field_bytes): Q = rho at the
+ * cell's 2x2 corners, GX/GY = the float32 central differences of
+ * _cell_gradient (_kernels.py:101-114) at those corners.  Optional input of
+ * hb_advect_points / hb_advect_laplacian (same results; three 16-byte loads
+ * from one record per gradient sample and one 16-byte load per bilinear sample
+ * instead of ~9 scattered ones). */
+HB_API int64_t hb_grad_field_bytes(int nbins, int nv, int nu);
 HB_API int hb_grad_field(const float *rho, int nbins, int nv, int nu, float *out,
                          void *stream);
 

@@ -100,6 +100,7 @@ SIGNATURES = {
     "hb_integral_image": (_I, [_P, _I, _I, _I, _P, _P]),
     "hb_used_cells": (_I, [_P, _P, _I, _I, _I, _D, _P, _P]),
     "hb_advect_partials": (_I64, []),
+    "hb_grad_field_bytes": (_I64, [_I, _I, _I]),
     "hb_grad_field": (_I, [_P, _I, _I, _I, _P, _P]),
     "hb_advect_laplacian": (_I, [_P, _P, _P, _I64, _I64, _P, _P, _P, _I, _I, _I, _D, _D,
                                  _D, _I, _D, _I, _D, _P, _P, _P, _P, _P]),

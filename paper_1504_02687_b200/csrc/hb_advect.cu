@@ -364,7 +364,7 @@ int hb_advect_laplacian(const double *pts_in, double *pts_out, const int64_t *st
         (counts && (!pos || !(delta > 0))) ||
         (n_pts > 0 && (!pts_in || !pts_out || !starts)))
         return set_error(HB_EINVAL, "hb_advect_laplacian: bad arguments");
-    if (adv && grad_field && 3 * (int64_t)nbins * nv * nu >= ((int64_t)1 << 32))
+    if (adv && grad_field && (int64_t)kQuadRec * nbins * nv * nu >= ((int64_t)1 << 32))
         return set_error(HB_EINVAL, "hb_advect_laplacian: quad field above 2^32/3 cells");
     if (n_pts == 0 || n_edges == 0) return HB_OK;
     cudaStream_t st = as_stream(stream);

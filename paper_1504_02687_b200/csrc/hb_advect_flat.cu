@@ -288,7 +288,7 @@ int hb_advect_points(double *pts, const int64_t *starts, int64_t n_edges, int64_
         (n_pts > 0 && (!pts || !starts || !edge_layer || !rho)))
         return set_error(HB_EINVAL, "hb_advect_points: bad arguments");
     if ((int64_t)nbins * nv * nu >= ((int64_t)1 << 31) ||
-        (grad_field && 3 * (int64_t)nbins * nv * nu >= ((int64_t)1 << 32)))
+        (grad_field && (int64_t)kQuadRec * nbins * nv * nu >= ((int64_t)1 << 32)))
         return set_error(HB_EINVAL, "hb_advect_points: field above 2^31 cells");
     cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
     if (cudaMemsetAsync(disp_partials, 0, sizeof(double) * kMaxStreamBlocks, st) != cudaSuccess)

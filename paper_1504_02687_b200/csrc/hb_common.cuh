@@ -187,6 +187,22 @@ struct QuadField {
     unsigned base;
 };
 
+// float4s per quad record: {Q, GX, GY} (48 bytes).  4 pads the record to 64
+// bytes (never straddles a 128-byte line; Q+GX is one 256-bit load) -- measured
+// slower: advect 5.24 -> 5.31 ms on config 4, 33.5 -> 37.2 ms on config 5
+#ifndef HB_QUAD_REC
+#define HB_QUAD_REC 3
+#endif
+constexpr unsigned kQuadRec = HB_QUAD_REC;
+static_assert(kQuadRec == 3 || kQuadRec == 4, "quad record: 48 or 64 bytes");
+
+// 32 bytes (two float4) with one load; p 32-byte aligned
+__device__ __forceinline__ void ldg_2x4(const float4 *p, float4 &a, float4 &b) {
+    asm("ld.global.nc.v8.f32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+        : "=f"(a.x), "=f"(a.y), "=f"(a.z), "=f"(a.w), "=f"(b.x), "=f"(b.y), "=f"(b.z), "=f"(b.w)
+        : "l"(p));
+}
+
 __device__ __forceinline__ void gradient2_value_quad(const QuadField &f, int nv, int nu, double x,
                                                      double y, double &Gx, double &Gy,
                                                      double &val) {
@@ -194,8 +210,15 @@ __device__ __forceinline__ void gradient2_value_quad(const QuadField &f, int nv,
     const int v0 = clampi(floor_i(y), 0, nv - 2);
     const double fx = dsub(x, (double)u0);
     const double fy = dsub(y, (double)v0);
-    const float4 *rec = f.q + 3u * (f.base + (unsigned)(v0 * nu + u0));
-    const float4 q = __ldg(rec), dx = __ldg(rec + 1), dy = __ldg(rec + 2);
+    const float4 *rec = f.q + kQuadRec * (f.base + (unsigned)(v0 * nu + u0));
+    float4 q, dx;
+    if (kQuadRec == 4) {
+        ldg_2x4(rec, q, dx);
+    } else {
+        q = __ldg(rec);
+        dx = __ldg(rec + 1);
+    }
+    const float4 dy = __ldg(rec + 2);
     // corners: .x (u0,v0)  .y (u0+1,v0)  .z (u0,v0+1)  .w (u0+1,v0+1)
     const double ax = dadd((double)dx.x, dmul(fx, dsub((double)dx.y, (double)dx.x)));
     const double bx = dadd((double)dx.z, dmul(fx, dsub((double)dx.w, (double)dx.z)));
@@ -217,7 +240,7 @@ __device__ __forceinline__ double bilinear_quad(const float4 *__restrict__ q, un
     const int v0 = inner ? floor_i(y) : clampi(floor_i(y), 0, nv - 2);
     const double fx = dsub(x, (double)u0);
     const double fy = dsub(y, (double)v0);
-    const float4 c = __ldg(q + 3u * (base + (unsigned)(v0 * nu + u0)));
+    const float4 c = __ldg(q + kQuadRec * (base + (unsigned)(v0 * nu + u0)));
     const double a = lerp_f32diff(c.x, c.y, fx);
     const double b = lerp_f32diff(c.z, c.w, fx);
     return dadd(a, dmul(fy, dsub(b, a)));

@@ -357,7 +357,7 @@ __global__ void grad_field_kernel(const float *__restrict__ rho, int nv, int nu,
     if (u >= nu) return;
     const int64_t plane = (int64_t)nv * nu;
     const float *r = rho + l * plane;
-    float4 *rec = out + 3 * (l * plane + (int64_t)v * nu + u);  // {Q, GX, GY} of the cell
+    float4 *rec = out + kQuadRec * (l * plane + (int64_t)v * nu + u);  // {Q, GX, GY} of the cell
     if (u > nu - 2 || v > nv - 2) {
         rec[0] = rec[1] = rec[2] = make_float4(0.f, 0.f, 0.f, 0.f);
         return;
@@ -504,6 +504,14 @@ int hb_integral_image(const float *in, int nbins, int nv, int nu, double *table,
     const int64_t rows = (int64_t)nbins * nv;
     launch_row_fold(table, rows, nu, st);
     return check_launch("hb_integral_image", 2);
+}
+
+int64_t hb_grad_field_bytes(int nbins, int nv, int nu) {
+    if (nbins < 1 || nv < 1 || nu < 1) {
+        set_error(HB_EINVAL, "hb_grad_field_bytes: bad arguments");
+        return -1;
+    }
+    return (int64_t)sizeof(float4) * kQuadRec * nbins * nv * nu;
 }
 
 int hb_grad_field(const float *rho, int nbins, int nv, int nu, float *out, void *stream) {

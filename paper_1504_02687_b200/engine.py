@@ -201,10 +201,10 @@ class BundleEngine:
         # quad advection field (hb_grad_field), 48 B per cell, whenever memory
         # allows: it beats gathering rho even when it does not fit L2 (config
         # 5's 805 MB field cut its advect from 40.4 to 33.4 ms per iteration)
-        quad_bytes = 48 * B * self.nv * self.nu
+        quad_bytes = N.lib().hb_grad_field_bytes(B, self.nv, self.nu)
         quad_limit = min(int(float(os.environ.get("HB_QUAD_LIMIT_MB", "4096")) * (1 << 20)),
                          torch.cuda.mem_get_info(dev)[0] // 8)
-        self.gfield = (torch.empty((B, self.nv, self.nu, 3, 4), dtype=torch.float32, device=dev)
+        self.gfield = (torch.empty(quad_bytes // 4, dtype=torch.float32, device=dev)
                        if quad_bytes <= quad_limit else None)
         # resample count as its own launch after the advect pass (measured
         # faster than fusing it: the fused build's register footprint halves

@@ -224,7 +224,8 @@ def main():
     h = cfg.lambda_ ** args.iters * cfg.h_max
     work = torch.empty_like(eng.alt)
 
-    gfield = torch.empty((Bn, nv, nu, 3, 4), dtype=torch.float32, device="cuda")
+    gfield = torch.empty(N.lib().hb_grad_field_bytes(Bn, nv, nu) // 4, dtype=torch.float32,
+                         device="cuda")
     N.call("hb_grad_field", ptr(eng.field), Bn, nv, nu, ptr(gfield), s)
     out["grad_field_ms"] = timed(lambda: N.call("hb_grad_field", ptr(eng.field), Bn, nv, nu,
                                                 ptr(gfield), s))

@@ -450,15 +450,27 @@ int device_sm_count();  // cached SM count of the current device (hb_api.cu)
 // more blocks than there are warps' worth of edges.  For a given GPU model
 // this is a pure function of n_edges, so per-block metric partials sum in a
 // reproducible order.
+// Resident blocks per SM, cached by (kernel address, block, dynamic smem):
+// kernels sharing a signature must not share an entry.
+inline int resident_blocks(const void *kernel, int block = kStreamBlock, size_t smem = 0) {
+    struct Entry { const void *k; int block; size_t smem; int per_sm; };
+    static Entry cache[64];
+    static int n = 0;
+    for (int i = 0; i < n; ++i)
+        if (cache[i].k == kernel && cache[i].block == block && cache[i].smem == smem)
+            return cache[i].per_sm;
+    int per_sm = 0;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, block, smem) !=
+            cudaSuccess ||
+        per_sm < 1)
+        per_sm = 1;
+    if (n < 64) cache[n++] = Entry{kernel, block, smem, per_sm};
+    return per_sm;
+}
+
 template <typename Kernel>
 inline unsigned persistent_grid(Kernel kernel, int64_t n_edges) {
-    static int per_sm = 0;
-    if (per_sm == 0) {
-        if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, kStreamBlock, 0) !=
-                cudaSuccess ||
-            per_sm < 1)
-            per_sm = 1;
-    }
+    const int per_sm = resident_blocks(reinterpret_cast<const void *>(kernel));
     int64_t want = (n_edges + kStreamBlock / 32 - 1) / (kStreamBlock / 32);
     int64_t cap = (int64_t)device_sm_count() * per_sm;
     if (cap > kMaxStreamBlocks) cap = kMaxStreamBlocks;

@@ -393,12 +393,7 @@ using namespace hb;
 // warps than there are groups of points
 template <typename K>
 static unsigned lc_grid(K kernel, int64_t groups, size_t smem) {
-    static int per_sm = 0;
-    if (per_sm == 0 &&
-        (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, kLCBlock, smem) !=
-             cudaSuccess ||
-         per_sm < 1))
-        per_sm = 1;
+    const int per_sm = resident_blocks(reinterpret_cast<const void *>(kernel), kLCBlock, smem);
     int64_t want = (groups + kLCWarps - 1) / kLCWarps;
     const int64_t cap = (int64_t)device_sm_count() * per_sm;
     if (want > cap) want = cap;

@@ -308,6 +308,212 @@ emit_kernel(const double2 *__restrict__ pts, const int64_t *__restrict__ starts,
     }
 }
 
+// ---------------------------------------------------------------------------
+// Flat, output-tiled emit: the same outputs and splat as emit_kernel, but a
+// warp works on tiles of 32 consecutive GLOBAL outputs instead of one edge at
+// a time, so every lane has an output (short edges and ragged chunk ends
+// left a third of the lanes idle) and no owner needs a shuffle search.
+//
+// Kept inputs j (pos[j] >= 0) have global output indices G(j) =
+// new_starts[e(j)] + pos[j], strictly increasing in j.  Output m is the kept
+// input with G == m, or lies between the last kept input with G < m and the
+// first with G > m -- both of m's own edge, because an edge's first and last
+// inputs are always kept (pos 0 and count-1) -- at piece m - G(prev) of
+// G(next) - G(prev) (interp_piece, bit-identical to emit_kernel's).  Per
+// tile the warp scans its current 32-input chunk (advancing while no kept
+// input reaches the tile's last output), drops the tile's kept inputs into a
+// 33-slot shared table by G - m0 (slot 32: the first kept input past the
+// tile), and each lane finds its neighbours with two bit scans of the
+// occupancy mask.  Segment m-1 -> m (splat) starts at the previous lane's
+// output; lane 0 carries the previous tile's lane 31, so each warp first
+// recomputes the tile before its range without writing anything.
+struct EmitSlots {
+    double x[33], y[33];
+    long long g[33];    // G of the kept input in the slot
+    long long nsb[33];  // new_starts of its edge
+    int e[33];
+};
+
+#ifndef HB_EMIT_FLAT_MINB
+#define HB_EMIT_FLAT_MINB 4
+#endif
+__global__ void __launch_bounds__(kStreamBlock, HB_EMIT_FLAT_MINB)
+emit_flat_kernel(const double2 *__restrict__ pts, const int64_t *__restrict__ starts,
+                 int64_t n_edges, const int32_t *__restrict__ pos,
+                 const int64_t *__restrict__ new_starts, double2 *__restrict__ out,
+                 const int32_t *__restrict__ group, const int32_t *__restrict__ weight,
+                 int32_t *__restrict__ hist, int64_t plane, int nv, int nu,
+                 int32_t *__restrict__ status, const __grid_constant__ hb_tiles tl, int use_tiles,
+                 int64_t out_cap) {
+    __shared__ EmitSlots s_slots[kStreamBlock / 32];
+    const hb_tiles *tiles = use_tiles ? &tl : nullptr;
+    const unsigned full = 0xffffffffu;
+    const int lane = threadIdx.x & 31;
+    if (new_starts[n_edges] > out_cap) {
+        if (blockIdx.x == 0 && threadIdx.x == 0 && status) atomicOr(status, HB_STATUS_CAPACITY);
+        return;
+    }
+    EmitSlots &S = s_slots[threadIdx.x >> 5];
+    const int64_t M_lo = new_starts[0], M_hi = new_starts[n_edges];
+    const int64_t J_hi = starts[n_edges];
+    const int64_t n_tiles = M_hi > M_lo ? (M_hi - M_lo + 31) >> 5 : 0;
+    const int64_t gw = ((int64_t)blockIdx.x * kStreamBlock + threadIdx.x) >> 5;
+    const int64_t nw = (int64_t)gridDim.x * (kStreamBlock / 32);
+    const int64_t per = (n_tiles + nw - 1) / nw;
+    const int64_t t_beg = gw * per;
+    const int64_t t_end = t_beg + per < n_tiles ? t_beg + per : n_tiles;
+    if (t_beg >= t_end) return;  // (warp-uniform)
+    const bool splat = hist != nullptr;
+    const int64_t t0 = t_beg > 0 ? t_beg - 1 : t_beg;  // one dry tile for the carry
+    const int64_t m_first = M_lo + t0 * 32;
+
+    // edge of output m_first: the last e with new_starts[e] <= m_first
+    int64_t e_cur = 0;
+    if (lane == 0) {
+        int64_t lo = 0, hi = n_edges - 1;
+        while (lo < hi) {
+            const int64_t mid = (lo + hi + 1) >> 1;
+            if (new_starts[mid] <= m_first) lo = mid; else hi = mid - 1;
+        }
+        e_cur = lo;
+    }
+    e_cur = __shfl_sync(full, e_cur, 0);
+    // input cursor: a kept input of that edge with output index < m_first's
+    // (the edge's first input, moved forward by a 32-way search on pos)
+    int64_t jc = starts[e_cur];
+    {
+        const int64_t lm = m_first - new_starts[e_cur];
+        int64_t hi = starts[e_cur + 1];
+        for (int it = 0; it < 6 && lm > 0 && hi - jc > 64; ++it) {
+            const int64_t step = (hi - jc + 31) / 32;
+            const int64_t j = jc + lane * step;
+            const int pj = j < hi ? pos[j] : -1;
+            const unsigned ok = __ballot_sync(full, pj >= 0 && pj < lm);  // bit 0: jc itself
+            const unsigned past = __ballot_sync(full, pj >= lm);
+            const int L = 31 - __clz(ok);
+            const unsigned after = L == 31 ? 0u : (past & (0xfffffffeu << L));
+            if (after) hi = jc + (int64_t)(__ffs(after) - 1) * step;
+            jc += (int64_t)L * step;
+            if (L == 0 && !after) break;  // a long run of dropped inputs: scan it
+        }
+    }
+
+    // current input chunk [jc, jc + 32): point, edge, G (-1: dropped / none)
+    // (measured: issuing the next chunk's loads one chunk ahead costs more in
+    // registers / occupancy than it hides, 5.88 -> 6.06 ms on config 4)
+    double2 x = make_double2(0.0, 0.0);
+    int64_t G = -1, nsb = 0;
+    int ej = 0;
+    int64_t e_next = e_cur;
+    auto load_chunk = [&]() {
+        const int64_t j = jc + lane;
+        const bool in = j < J_hi;
+        x = in ? HB_LD_STREAM(pts + j) : make_double2(0.0, 0.0);
+        const int pj = in ? HB_LD_STREAM(pos + j) : -1;
+        // edges starting in (jc, jc + 31] (every edge has >= 1 input)
+        const int64_t ek = e_cur + 1 + lane;
+        const int64_t sv = ek <= n_edges ? starts[ek] : INT64_MAX;
+        const int64_t rel = sv - jc;  // >= 1
+        const unsigned smask = __reduce_or_sync(full, rel <= 31 ? (1u << rel) : 0u);
+        int64_t e = e_cur + __popc(smask & (0xffffffffu >> (31 - lane)));
+        if (e > n_edges - 1) e = n_edges - 1;
+        ej = (int)e;
+        nsb = new_starts[e];
+        G = pj >= 0 ? nsb + pj : -1;
+        e_next = e_cur + __popc(__ballot_sync(full, rel <= 32));
+    };
+    load_chunk();
+
+    double2 cq = make_double2(0.0, 0.0);      // output m0 - 1 (previous tile's lane 31)
+    double cpx = 0.0, cpy = 0.0;               // last kept input with G < m0 ...
+    int64_t cpg = 0;                           // ... and its G
+    for (int64_t tt = t0; tt < t_end; ++tt) {
+        const bool dry = tt < t_beg;
+        const int64_t m0 = M_lo + tt * 32;
+        const int64_t m_last = m0 + 31 < M_hi - 1 ? m0 + 31 : M_hi - 1;
+        unsigned W = 0;
+        for (;;) {
+            const bool kept = G >= 0;
+            const bool inw = kept && G >= m0 && G <= m0 + 31;
+            if (inw) {
+                const int sl = (int)(G - m0);
+                S.x[sl] = x.x; S.y[sl] = x.y; S.g[sl] = G; S.nsb[sl] = nsb; S.e[sl] = ej;
+            }
+            W |= __reduce_or_sync(full, inw ? (1u << (int)(G - m0)) : 0u);
+            const unsigned below = __ballot_sync(full, kept && G < m0);
+            if (below) {
+                const int L = 31 - __clz(below);
+                cpx = __shfl_sync(full, x.x, L);
+                cpy = __shfl_sync(full, x.y, L);
+                cpg = __shfl_sync(full, G, L);
+            }
+            const unsigned beyond = __ballot_sync(full, kept && G > m0 + 31);
+            if (beyond && lane == __ffs(beyond) - 1) {
+                S.x[32] = x.x; S.y[32] = x.y; S.g[32] = G; S.nsb[32] = nsb; S.e[32] = ej;
+            }
+            if (__any_sync(full, kept && G >= m_last)) {
+                break;
+            }
+            if (jc + 32 >= J_hi) break;  // (only for inconsistent, over-capacity inputs)
+            jc += 32;
+            e_cur = e_next;
+            load_chunk();
+        }
+        __syncwarp();
+        const int64_t m = m0 + lane;
+        const bool valid = m <= m_last;
+        double2 q = make_double2(0.0, 0.0);
+        int64_t mb = 0;  // new_starts of m's edge
+        int me = 0;      // m's edge
+        if ((W >> lane) & 1u) {
+            q = make_double2(S.x[lane], S.y[lane]);
+            mb = S.nsb[lane];
+            me = S.e[lane];
+        } else if (valid) {
+            const unsigned above = lane == 31 ? 0u : (W & (0xfffffffeu << lane));
+            const int os = above ? __ffs(above) - 1 : 32;
+            const unsigned lo = W & ((1u << lane) - 1u);
+            double2 a;
+            int64_t ag;
+            if (lo) {
+                const int ps = 31 - __clz(lo);
+                a = make_double2(S.x[ps], S.y[ps]);
+                ag = S.g[ps];
+            } else {
+                a = make_double2(cpx, cpy);
+                ag = cpg;
+            }
+            const int64_t og = S.g[os];
+            q = interp_piece(a, make_double2(S.x[os], S.y[os]), (int)(m - ag), (int)(og - ag));
+            mb = S.nsb[os];
+            me = S.e[os];
+        }
+        if (!dry && valid) HB_ST_STREAM(out + m, q);
+        if (splat) {
+            double q0x = __shfl_up_sync(full, q.x, 1), q0y = __shfl_up_sync(full, q.y, 1);
+            if (lane == 0) { q0x = cq.x; q0y = cq.y; }
+            cq = make_double2(__shfl_sync(full, q.x, 31), __shfl_sync(full, q.y, 31));
+            const int64_t lm = m - mb;
+            const bool seg = !dry && valid && lm >= 1;
+            // (clamped: after a capacity clamp, empty edges can leave stale slots)
+            me = me < 0 ? 0 : (me > (int)n_edges - 1 ? (int)n_edges - 1 : me);
+            const int grp = seg ? group[me] : 0;
+            const int32_t w = seg && weight ? weight[me] : 1;
+            bin_or_splat<int32_t>(seg, q0x, q0y, q.x, q.y, lm == 1 ? 0 : 1, w, grp, hist, plane,
+                                  nv, nu, status, tiles);
+        }
+        // the tile's last kept input is the next tile's predecessor unless
+        // the chunk scan finds a later one
+        if (W) {
+            const int ls = 31 - __clz(W);
+            cpx = S.x[ls];
+            cpy = S.y[ls];
+            cpg = S.g[ls];
+        }
+        __syncwarp();
+    }
+}
+
 // After a resample whose total exceeded the buffers (status bit set, nothing
 // written), keep every later kernel in bounds: starts[e] = min(starts[e], cap).
 // Two launches: entries below n_edges first (all read the untouched total),
@@ -478,7 +684,14 @@ int hb_resample_emit_cap(const double *pts, const int64_t *starts, int64_t n_edg
         (counts && (!group || nv < 1 || nu < 1 || nv > kMaxDim || nu > kMaxDim)))
         return set_error(HB_EINVAL, "hb_resample_emit: bad arguments");
     if (n_edges == 0 || n_pts == 0) return HB_OK;
+#ifdef HB_EMIT_PER_EDGE
     emit_kernel<<<persistent_grid(emit_kernel, n_edges), kStreamBlock, 0, as_stream(stream)>>>(
+#else
+    // work items: output tiles (the output total is on the device; the input
+    // count bounds it well enough for the grid size)
+    emit_flat_kernel<<<persistent_grid(emit_flat_kernel, (n_pts + 31) / 32), kStreamBlock, 0,
+                       as_stream(stream)>>>(
+#endif
         reinterpret_cast<const double2 *>(pts), starts, n_edges, pos, new_starts,
         reinterpret_cast<double2 *>(out), group, weight, counts, (int64_t)nv * nu, nv, nu,
         status, tiles ? *tiles : hb_tiles{}, (counts && tiles) ? 1 : 0, out_capacity);

@@ -232,6 +232,50 @@ def test_resample_emit_splat_random_vs_oracle(seed):
     assert np.array_equal(hist.cpu().numpy(), ref_counts)
 
 
+def test_resample_emit_long_edges_vs_oracle():
+    """Edges of tens of thousands of points with long merged runs: warps of
+    the flat emit start deep inside an edge (the 32-way cursor search on pos)
+    and behind runs of dropped inputs (its linear fall-back)."""
+    rng = np.random.default_rng(11)
+    nv, nu = 200, 220
+    lens = np.array([2, 60000, 3, 25000, 2, 2, 9000, 40000, 5], dtype=np.int64)
+    starts = np.zeros(lens.size + 1, dtype=np.int64)
+    np.cumsum(lens, out=starts[1:])
+    steps = rng.normal(0, 0.9, size=(int(starts[-1]), 2))
+    steps[starts[1] + 100:starts[1] + 9000] *= 1e-3   # a 8900-point cluster: one long merge
+    steps[starts[7] + 5000:starts[7] + 30000:2] *= 1e-2  # alternating merges
+    pts = np.empty_like(steps)
+    for e in range(lens.size):
+        s_, t_ = starts[e], starts[e + 1]
+        p = np.cumsum(steps[s_:t_], axis=0) * 0.05 + rng.uniform([20, 20], [nu - 20, nv - 20])
+        pts[s_:t_] = np.clip(p, 1.0, [nu - 2.0, nv - 2.0])
+    E, n = len(starts) - 1, len(pts)
+    groups = rng.integers(0, 2, size=E)
+    delta = 0.9
+    ref_pts, ref_starts = O.resample(pts.copy(), starts, delta, workers=1)
+    ref_counts = O.accumulate_counts(ref_pts, ref_starts, groups, (nv, nu), 2)
+    dp, ds = dev(pts), dev(starts)
+    counts = torch.empty(E, dtype=torch.int64, device="cuda")
+    pos = torch.empty(n, dtype=torch.int32, device="cuda")
+    ns = torch.empty(E + 1, dtype=torch.int64, device="cuda")
+    ws = torch.empty(int(N.lib().hb_scan_workspace_bytes(E)), dtype=torch.uint8, device="cuda")
+    hist = torch.zeros((2, nv, nu), dtype=torch.int32, device="cuda")
+    status = torch.zeros(1, dtype=torch.int32, device="cuda")
+    s = stream_ptr()
+    N.call("hb_resample_count", ptr(dp), ptr(ds), E, delta, ptr(counts), ptr(pos), s)
+    N.call("hb_scan_counts", ptr(counts), E, ptr(ns), ptr(ws), ws.numel(), s)
+    m = int(ns[-1].item())
+    out = torch.empty((m, 2), dtype=torch.float64, device="cuda")
+    N.call("hb_resample_emit", ptr(dp), ptr(ds), E, n, ptr(pos), ptr(ns), ptr(out),
+           ptr(dev(groups.astype(np.int32))), None, ptr(hist), nv, nu, ptr(status), None, s)
+    sync()
+    pos_h = pos.cpu().numpy()
+    assert (pos_h < 0).sum() > 9000  # the merged runs are really there
+    assert np.array_equal(ns.cpu().numpy(), ref_starts)
+    assert np.array_equal(out.cpu().numpy(), ref_pts)
+    assert np.array_equal(hist.cpu().numpy(), ref_counts)
+
+
 def test_advect_laplacian_random_vs_oracle():
     rng = np.random.default_rng(7)
     nv, nu = 96, 128

@@ -282,33 +282,81 @@ __device__ __forceinline__ double tz(const double *__restrict__ t, int nu, int r
 }
 
 constexpr int kBoxBlock = 256;
+#ifndef HB_BOX_ROWS
+#define HB_BOX_ROWS 4  // measured on the config-5 map: 1 0.595, 2 0.552, 4 0.545, 8 0.582 ms per hb_smooth
+#endif
+constexpr int kBoxRows = HB_BOX_ROWS;  // output rows per thread (4 independent table loads each)
 
+// Layer peak, max(rho, initial=0): non-negative floats order like their int
+// bits.  One atomic per block, and none when the block's maximum does not
+// exceed the peak already stored (the peak only grows, so the final value is
+// the true maximum whatever the order).  A warp-level atomic per 32 cells
+// onto B addresses serialised in L2: 0.36 ms of the config-5 smoothing.
+__device__ __forceinline__ void block_peak(float *__restrict__ peak, float m) {
+    __shared__ float s_max[32];
+    for (int d = 16; d; d >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, d));
+    const int warp = threadIdx.x >> 5, nw = (blockDim.x + 31) >> 5;
+    if ((threadIdx.x & 31) == 0) s_max[warp] = m;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        for (int w = 1; w < nw; ++w) m = fmaxf(m, s_max[w]);
+        if (m > 0.0f && m > *reinterpret_cast<volatile float *>(peak))
+            atomicMax(reinterpret_cast<int *>(peak), __float_as_int(m));
+    }
+}
+
+// float32(s / area) with the float64 quotient correctly rounded, as the
+// reference computes it (raster.py:169), without a float64 divide per cell:
+// q = s * (1/area) is within 2 ulp of the true quotient s/area, and rounding
+// to float32 can only differ between the two when a float32 rounding
+// midpoint (low 29 bits of the float64 significand == 2^28) lies within
+// those ulps -- then, and for results near float32's subnormal range, the
+// IEEE divide decides.  The divide was 60 % of the box pass's instructions.
+__device__ __forceinline__ float box_quotient_f32(double s, double area, double inv_area) {
+    const double q = dmul(s, inv_area);
+    const unsigned low = (unsigned)(__double_as_longlong(q) & 0x1fffffffull);
+    if (low - (0x10000000u - 8u) <= 16u || (q != 0.0 && fabs(q) < 0x1p-120))
+        return __double2float_rn(__ddiv_rn(s, area));
+    return __double2float_rn(q);
+}
+
+// Each thread produces kBoxRows cells of one column; all 4*kBoxRows table
+// reads are issued before the first quotient.
 __global__ void __launch_bounds__(kBoxBlock)
 box_kernel(const double *__restrict__ table, int nv, int nu, int radius,
            float *__restrict__ out, float *__restrict__ peak) {
     const int u = blockIdx.x * kBoxBlock + threadIdx.x;
-    const int v = blockIdx.y;
+    const int vb = blockIdx.y * kBoxRows;
     const int l = blockIdx.z;
-    float val = 0.0f;
+    float m = 0.0f;
     if (u < nu) {
         const int64_t plane = (int64_t)nv * nu;
         const double *t = table + l * plane;
-        const int r0 = min(max(v - radius, 0), nv), r1 = min(max(v + radius + 1, 0), nv);
         const int c0 = min(max(u - radius, 0), nu), c1 = min(max(u + radius + 1, 0), nu);
-        const double s = dadd(dsub(dsub(tz(t, nu, r1, c1), tz(t, nu, r0, c1)),
-                                   tz(t, nu, r1, c0)),
-                              tz(t, nu, r0, c0));
         const double area = (double)((2 * radius + 1) * (2 * radius + 1));
-        val = __double2float_rn(__ddiv_rn(s, area));
-        out[l * plane + (int64_t)v * nu + u] = val;
+        const double inv_area = __drcp_rn(area);
+        double t11[kBoxRows], t01[kBoxRows], t10[kBoxRows], t00[kBoxRows];
+#pragma unroll
+        for (int k = 0; k < kBoxRows; ++k) {
+            const int v = min(vb + k, nv - 1);
+            const int r0 = min(max(v - radius, 0), nv), r1 = min(max(v + radius + 1, 0), nv);
+            t11[k] = tz(t, nu, r1, c1);
+            t01[k] = tz(t, nu, r0, c1);
+            t10[k] = tz(t, nu, r1, c0);
+            t00[k] = tz(t, nu, r0, c0);
+        }
+        float *o = out + l * plane + u;
+#pragma unroll
+        for (int k = 0; k < kBoxRows; ++k) {
+            if (vb + k < nv) {
+                const double s = dadd(dsub(dsub(t11[k], t01[k]), t10[k]), t00[k]);
+                const float val = box_quotient_f32(s, area, inv_area);
+                o[(int64_t)(vb + k) * nu] = val;
+                m = fmaxf(m, val > 0.0f ? val : 0.0f);
+            }
+        }
     }
-    if (peak) {
-        // max(rho, initial=0): non-negative floats order like their bits
-        float m = val > 0.0f ? val : 0.0f;
-        for (int d = 16; d; d >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, d));
-        if ((threadIdx.x & 31) == 0 && m > 0.0f)
-            atomicMax(reinterpret_cast<int *>(peak + l), __float_as_int(m));
-    }
+    if (peak) block_peak(peak + l, m);
 }
 
 // radius-0 pass (raster.py:157-158 returns a copy) and stand-alone layer
@@ -324,12 +372,7 @@ __global__ void mix_pass_kernel(const T *__restrict__ groups, const float *__res
         val = mixed_value<T>(groups, mat, nb, l, plane, i);
         out[l * plane + i] = val;
     }
-    if (peak) {
-        float m = val > 0.0f ? val : 0.0f;
-        for (int d = 16; d; d >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, d));
-        if ((threadIdx.x & 31) == 0 && m > 0.0f)
-            atomicMax(reinterpret_cast<int *>(peak + l), __float_as_int(m));
-    }
+    if (peak) block_peak(peak + l, val > 0.0f ? val : 0.0f);
 }
 
 // Quad advection field.  For every cell (u, v) of a layer, a 48-byte record
@@ -375,18 +418,32 @@ __global__ void grad_field_kernel(const float *__restrict__ rho, int nv, int nu,
 
 // used_cell_count (bundler.py:292-305): rho > float32(rel * peak_l) when
 // peak_l > 0 (NEP 50 makes the comparison float32).
-__global__ void used_cells_kernel(const float *__restrict__ rho, const float *__restrict__ peak,
-                                  int64_t plane, double rel, unsigned long long *count) {
-    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+// kUsedPer cells per thread (strided by the block), one atomic per block.
+constexpr int kUsedPer = 8;
+__global__ void __launch_bounds__(256)
+used_cells_kernel(const float *__restrict__ rho, const float *__restrict__ peak,
+                  int64_t plane, double rel, unsigned long long *count) {
+    __shared__ unsigned s_cnt[8];
+    const int64_t i0 = (int64_t)blockIdx.x * (256 * kUsedPer) + threadIdx.x;
     const int l = blockIdx.y;
     const float pk = peak[l];
-    bool hit = false;
-    if (i < plane && (double)pk > 0.0) {
+    unsigned c = 0;
+    if ((double)pk > 0.0) {
         const float thr = __double2float_rn(dmul(rel, (double)pk));
-        hit = rho[l * plane + i] > thr;
+        const float *r = rho + l * plane;
+#pragma unroll
+        for (int k = 0; k < kUsedPer; ++k) {
+            const int64_t i = i0 + 256 * k;
+            if (i < plane && r[i] > thr) ++c;
+        }
     }
-    const unsigned m = __ballot_sync(0xffffffffu, hit);
-    if ((threadIdx.x & 31) == 0 && m) atomicAdd(count, (unsigned long long)__popc(m));
+    for (int d = 16; d; d >>= 1) c += __shfl_xor_sync(0xffffffffu, c, d);
+    if ((threadIdx.x & 31) == 0) s_cnt[threadIdx.x >> 5] = c;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        for (int w = 1; w < 8; ++w) c += s_cnt[w];
+        if (c) atomicAdd(count, (unsigned long long)c);
+    }
 }
 
 }  // namespace hb
@@ -469,7 +526,7 @@ int hb_smooth(const int32_t *counts, const float *hist, const float *matrix, int
                                                                                    nu, table);
             const int64_t rows = (int64_t)nbins * nv;
             launch_row_fold(table, rows, nu, st);
-            dim3 gb((nu + kBoxBlock - 1) / kBoxBlock, nv, nbins);
+            dim3 gb((nu + kBoxBlock - 1) / kBoxBlock, (nv + kBoxRows - 1) / kBoxRows, nbins);
             box_kernel<<<gb, kBoxBlock, 0, st>>>(table, nv, nu, r, dst, pk);
         }
         int rc = check_launch("hb_smooth", r == 0 ? 1 : (mix_first ? 4 : 3));
@@ -527,7 +584,7 @@ int hb_used_cells(const float *rho, const float *layer_peak, int nbins, int nv, 
     if (!rho || !layer_peak || !count || nbins < 1 || nv < 1 || nu < 1 || nv > kMaxDim || nu > kMaxDim)
         return set_error(HB_EINVAL, "hb_used_cells: bad arguments");
     const int64_t plane = (int64_t)nv * nu;
-    dim3 g((unsigned)((plane + 255) / 256), nbins);
+    dim3 g((unsigned)((plane + 256 * kUsedPer - 1) / (256 * kUsedPer)), nbins);
     used_cells_kernel<<<g, 256, 0, as_stream(stream)>>>(rho, layer_peak, plane, rel, count);
     return check_launch("hb_used_cells");
 }

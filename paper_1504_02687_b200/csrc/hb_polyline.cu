@@ -514,6 +514,204 @@ emit_flat_kernel(const double2 *__restrict__ pts, const int64_t *__restrict__ st
     }
 }
 
+// ---------------------------------------------------------------------------
+// Ring emit: input-major, each input read once.  A warp owns an edge-aligned
+// range of whole polylines (balanced by input points, like the Laplacian +
+// count pass) and walks it in 32-input chunks.  Kept input x (pos >= 0) with
+// previous kept input a owns outputs G(a)+1 .. G(x): the interpolants
+// a + (k/pieces)(x - a) (interp_piece, pieces = G(x) - G(a)) and x itself;
+// an edge's first input owns only itself.  Every lane writes its outputs
+// (usually one) into a per-warp ring of output slots in shared memory; as
+// soon as 32 consecutive outputs are complete, the warp stores them
+// (coalesced) and splats the segment ending at each, one output per lane.
+// The previous output of a tile's lane 0 is carried in registers.  Output
+// indices inside the range are 32-bit (a range holds < 2^31 outputs).
+//
+// Compared with the output-tiled emit_flat_kernel, no chunk is scanned
+// twice and no slot table is rebuilt per tile: ~2x fewer instructions per
+// output (that kernel issues ~560 warp instructions per 32 outputs at 73 %
+// issue utilisation).
+constexpr int kRing = 128;  // slots per warp (power of two)
+struct EmitRing {
+    double2 q[kRing];
+    int meta[kRing];  // (edge << 2) | min(local index, 2)
+    // the next 32-input chunk, fetched by cp.async while the warp works on
+    // the current one: points, pos, and starts / new_starts of the 32 edges
+    // after the chunk's first edge
+    double2 cpts[32];
+    long long csv[32], cnsv[32];
+    int cpos[32];
+};
+
+// cp.async with zero fill (src-size 0: nothing is read) for out-of-range lanes
+__device__ __forceinline__ void emit_cp(void *smem, const void *gmem, int bytes, bool ok) {
+    const unsigned sa = (unsigned)__cvta_generic_to_shared(smem);
+    if (bytes == 16)
+        asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(sa), "l"(gmem),
+                     "r"(ok ? 16 : 0));
+    else if (bytes == 8)
+        asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(sa), "l"(gmem),
+                     "r"(ok ? 8 : 0));
+    else
+        asm volatile("cp.async.ca.shared.global [%0], [%1], 4, %2;\n" ::"r"(sa), "l"(gmem),
+                     "r"(ok ? 4 : 0));
+}
+
+#ifndef HB_EMIT_RING_MINB
+#define HB_EMIT_RING_MINB 4
+#endif
+__global__ void __launch_bounds__(kStreamBlock, HB_EMIT_RING_MINB)
+emit_ring_kernel(const double2 *__restrict__ pts, const int64_t *__restrict__ starts,
+                 int64_t n_edges, const int32_t *__restrict__ pos,
+                 const int64_t *__restrict__ new_starts, double2 *__restrict__ out,
+                 const int32_t *__restrict__ group, const int32_t *__restrict__ weight,
+                 int32_t *__restrict__ hist, int64_t plane, int nv, int nu,
+                 int32_t *__restrict__ status, const __grid_constant__ hb_tiles tl, int use_tiles,
+                 int64_t out_cap) {
+    __shared__ __align__(16) EmitRing s_ring[kStreamBlock / 32];
+    const hb_tiles *tiles = use_tiles ? &tl : nullptr;
+    const unsigned full = 0xffffffffu;
+    const int lane = threadIdx.x & 31;
+    const unsigned lt_mask = (1u << lane) - 1u;
+    if (new_starts[n_edges] > out_cap) {
+        if (blockIdx.x == 0 && threadIdx.x == 0 && status) atomicOr(status, HB_STATUS_CAPACITY);
+        return;
+    }
+    EmitRing &R = s_ring[threadIdx.x >> 5];
+    const bool splat = hist != nullptr;
+
+    // edge-aligned input range [J_a, J_b) = edges [e0, e1)
+    const int64_t gw = ((int64_t)blockIdx.x * kStreamBlock + threadIdx.x) >> 5;
+    const int64_t nw = (int64_t)gridDim.x * (kStreamBlock / 32);
+    const int64_t P_lo = starts[0], P_hi = starts[n_edges];
+    const int64_t span = P_hi > P_lo ? P_hi - P_lo : 0;
+    int64_t e0 = 0, e1 = 0;
+    if (lane == 0) {
+        e0 = lower_edge(starts, n_edges, P_lo + (span * gw) / nw);
+        e1 = lower_edge(starts, n_edges, P_lo + (span * (gw + 1)) / nw);
+    }
+    e0 = __shfl_sync(full, e0, 0);
+    e1 = __shfl_sync(full, e1, 0);
+    if (e0 >= e1) return;  // (warp-uniform)
+    const int64_t J_a = starts[e0], J_b = starts[e1];
+    const int64_t O_a = new_starts[e0];
+    const int O_n = (int)(new_starts[e1] - O_a);  // outputs of the range
+    double2 *const outw = out + O_a;
+
+    int F = 0;                              // first output not yet flushed
+    double2 cq = make_double2(0.0, 0.0);    // output F - 1 (previous tile's lane 31)
+    double2 ca = cq;                        // last kept input so far ...
+    int cg = -1;                            // ... and its output index
+
+    // store + splat outputs [F, F + cnt), cnt <= 32, all present in the ring
+    auto flush = [&](int cnt) {
+        __syncwarp();
+        const int o = F + lane;
+        const bool valid = lane < cnt;
+        const int sl = o & (kRing - 1);
+        const double2 q = valid ? R.q[sl] : cq;
+        const int meta = valid ? R.meta[sl] : 0;
+        if (valid) HB_ST_STREAM(outw + o, q);
+        if (splat) {
+            double q0x = __shfl_up_sync(full, q.x, 1), q0y = __shfl_up_sync(full, q.y, 1);
+            if (lane == 0) { q0x = cq.x; q0y = cq.y; }
+            const int cls = meta & 3;
+            const int e = meta >> 2;
+            const bool seg = valid && cls >= 1;
+            const int grp = seg && group ? group[e] : 0;
+            const int32_t w = seg && weight ? weight[e] : 1;
+            bin_or_splat<int32_t>(seg, q0x, q0y, q.x, q.y, cls == 1 ? 0 : 1, w, grp, hist, plane,
+                                  nv, nu, status, tiles);
+        }
+        cq = make_double2(__shfl_sync(full, q.x, cnt - 1), __shfl_sync(full, q.y, cnt - 1));
+        F += cnt;
+        __syncwarp();
+    };
+
+    // chunk [jn, jn + 32) of the range, jn's edge en -> R.c* (one cp.async group)
+    auto prefetch = [&](int64_t jn, int64_t en) {
+        const int64_t j = jn + lane;
+        const bool in = j < J_b;
+        emit_cp(&R.cpts[lane], in ? pts + j : pts, 16, in);
+        emit_cp(&R.cpos[lane], in ? pos + j : pos, 4, in);
+        const int64_t ek = en + 1 + lane;
+        const bool ev = ek <= e1;
+        emit_cp(&R.csv[lane], ev ? starts + ek : starts, 8, ev);
+        emit_cp(&R.cnsv[lane], ev ? new_starts + ek : new_starts, 8, ev);
+        asm volatile("cp.async.commit_group;\n" ::: "memory");
+    };
+    int64_t e_c = e0;                   // edge of input jc
+    int64_t ns_c = new_starts[e0];      // its new_starts
+    prefetch(J_a, e0);
+    for (int64_t jc = J_a; jc < J_b; jc += 32) {
+        asm volatile("cp.async.wait_group 0;\n" ::: "memory");
+        __syncwarp();
+        const int64_t j = jc + lane;
+        const bool in = j < J_b;
+        const double2 x = R.cpts[lane];
+        const int pj = in ? R.cpos[lane] : -1;
+        // edges starting in (jc, jc + 31] (every edge has >= 1 input)
+        const int64_t ek = e_c + 1 + lane;
+        const int64_t sv = ek <= e1 ? (int64_t)R.csv[lane] : INT64_MAX;
+        const int64_t rel = sv - jc;  // >= 1
+        const unsigned smask = __reduce_or_sync(full, rel <= 31 ? (1u << rel) : 0u);
+        int d = __popc(smask & (0xffffffffu >> (31 - lane)));  // e - e_c
+        if (e_c + d > e1 - 1) d = (int)(e1 - 1 - e_c);
+        const int64_t e = e_c + d;
+        const int64_t nsb = d > 0 ? (int64_t)R.cnsv[d - 1] : ns_c;
+        const int nst = __popc(__ballot_sync(full, rel <= 32));
+        if (nst) ns_c = R.cnsv[nst - 1];
+        __syncwarp();  // R.c* is refilled below
+        e_c += nst;
+        if (jc + 32 < J_b) prefetch(jc + 32, e_c);
+        const bool kept = pj >= 0;
+        int g = -1;
+        if (kept) {
+            g = (int)(nsb + pj - O_a);
+            if ((unsigned)g >= (unsigned)O_n) g = -1;  // (inconsistent inputs: write nothing)
+        }
+        const unsigned kb = __ballot_sync(full, g >= 0);
+        // previous kept input: nearest kept lane below, else the carry
+        const unsigned lower = kb & lt_mask;
+        const int pl = lower ? 31 - __clz(lower) : 0;
+        double2 a = make_double2(__shfl_sync(full, x.x, pl), __shfl_sync(full, x.y, pl));
+        int ga = __shfl_sync(full, g, pl);
+        if (!lower) { a = ca; ga = cg; }
+        if (kb) {
+            const int L = 31 - __clz(kb);
+            ca = make_double2(__shfl_sync(full, x.x, L), __shfl_sync(full, x.y, L));
+            cg = __shfl_sync(full, g, L);
+        }
+        // this lane's outputs [nx, g]
+        const bool own = g >= 0;
+        int nx = own ? (pj == 0 ? g : ga + 1) : 1;
+        const int last = own ? g : 0;
+        const int pieces = g - ga;
+        const int meta_hi = (int)e << 2;
+        const int c_end = cg + 1;  // every output below is owned by a kept input seen so far
+        for (;;) {
+            const int limit = F + kRing;
+            // write this lane's outputs below limit (warp-uniform trip count)
+            int todo = (own && nx <= last) ? min(last, limit - 1) - nx + 1 : 0;
+            for (int r = __reduce_max_sync(full, todo > 0 ? todo : 0); r > 0; --r) {
+                if (todo > 0) {
+                    const double2 q = nx == last ? x : interp_piece(a, x, nx - ga, pieces);
+                    const int lm = pj - (last - nx);  // local index in the edge
+                    R.q[nx & (kRing - 1)] = q;
+                    R.meta[nx & (kRing - 1)] = meta_hi | (lm < 2 ? lm : 2);
+                    ++nx;
+                    --todo;
+                }
+            }
+            // flush complete tiles
+            const int done = min(c_end, limit);
+            while (F + 32 <= done) flush(32);
+            if (!__any_sync(full, own && nx <= last)) break;
+        }
+    }
+    if (F < O_n) flush(O_n - F);
+}
+
 // After a resample whose total exceeded the buffers (status bit set, nothing
 // written), keep every later kernel in bounds: starts[e] = min(starts[e], cap).
 // Two launches: entries below n_edges first (all read the untouched total),
@@ -684,8 +882,11 @@ int hb_resample_emit_cap(const double *pts, const int64_t *starts, int64_t n_edg
         (counts && (!group || nv < 1 || nu < 1 || nv > kMaxDim || nu > kMaxDim)))
         return set_error(HB_EINVAL, "hb_resample_emit: bad arguments");
     if (n_edges == 0 || n_pts == 0) return HB_OK;
-#ifdef HB_EMIT_PER_EDGE
+#if defined(HB_EMIT_PER_EDGE)
     emit_kernel<<<persistent_grid(emit_kernel, n_edges), kStreamBlock, 0, as_stream(stream)>>>(
+#elif !defined(HB_EMIT_FLAT)
+    emit_ring_kernel<<<persistent_grid(emit_ring_kernel, (n_pts + 31) / 32), kStreamBlock, 0,
+                       as_stream(stream)>>>(
 #else
     // work items: output tiles (the output total is on the device; the input
     // count bounds it well enough for the grid size)

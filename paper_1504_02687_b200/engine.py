@@ -228,12 +228,15 @@ class BundleEngine:
         # per segment, bundled duplicates collapse); else tile records.
         self.tiles = None
         self.tile_mode = -1
-        if self.wkind != "float":
+        # HB_SPLAT_MODE=auto|table|tiles|direct forces a path (tests cover all three)
+        smode = os.environ.get("HB_SPLAT_MODE", "auto")
+        if self.wkind != "float" and smode != "direct":
             geo = N.HbTiles()
             ent = ctypes.c_int64(0)
             budget = min(8 << 30, torch.cuda.mem_get_info(dev)[0] // 8)
-            if (N.lib().hb_segtab_geometry(B, self.nv, self.nu, 1.5 * self.delta,
-                                           ctypes.byref(geo), ctypes.byref(ent)) == 0
+            if (smode != "tiles"
+                    and N.lib().hb_segtab_geometry(B, self.nv, self.nu, 1.5 * self.delta,
+                                                   ctypes.byref(geo), ctypes.byref(ent)) == 0
                     and ent.value * 4 <= budget):
                 self.t_tab = torch.zeros(ent.value, dtype=torch.int32, device=dev)
                 self.t_keys = torch.zeros(1, dtype=torch.int64, device=dev)

@@ -357,6 +357,14 @@ def test_bundle_cfg1_bit_exact():
     _check_run(1)
 
 
+@pytest.mark.parametrize("mode", ["tiles", "direct"])
+def test_bundle_cfg1_bit_exact_splat_paths(mode, monkeypatch):
+    """The emit's splat through tile records (config 5's path) and through
+    direct atomics gives the same bits as the segment-key table."""
+    monkeypatch.setenv("HB_SPLAT_MODE", mode)
+    _check_run(1)
+
+
 def test_bundle_cfg2_bit_exact():
     _check_run(2)
 

@@ -100,6 +100,10 @@ __global__ void __launch_bounds__(kLCBlock, HB_LC_MINB) lapcount_kernel(const La
         reinterpret_cast<double2 (*)[kRowPad]>(lc_smem) + (size_t)wib * 32;
     int (*row_pos)[kRowPad] = reinterpret_cast<int (*)[kRowPad]>(
         lc_smem + sizeof(double2) * kLCWarps * 32 * kRowPad) + (size_t)wib * 32;
+    // phase C's re-walk decisions (relative offsets, -1 = merged), so the
+    // final write-out does not walk again
+    int (*row_fix)[kRowPad] = reinterpret_cast<int (*)[kRowPad]>(
+        lc_smem + (sizeof(double2) + sizeof(int)) * kLCWarps * 32 * kRowPad) + (size_t)wib * 32;
     const double lo2 = COUNT ? sqrt_lt_bound(0.5 * p.delta) : 0.0;  // _kernels.py:211-212
     const double hi2 = COUNT ? sqrt_gt_bound(1.5 * p.delta) : 0.0;
     constexpr unsigned run_bits = kRun == 32 ? 0xffffffffu : ((1u << kRun) - 1u);
@@ -289,9 +293,11 @@ __global__ void __launch_bounds__(kLCBlock, HB_LC_MINB) lapcount_kernel(const La
                             const bool en = (ends >> t) & 1u;
                             const double g2 = dist2_ref(F.x, F.y, a2.x, a2.y);
                             k2 = en || !(g2 < lo2);
+                            row_fix[lane][t] = -1;
                             if (k2) {
                                 o2 += pieces_of(g2, hi2);
                                 a2 = F;
+                                row_fix[lane][t] = o2;
                                 const int spv = row_pos[lane][t];
                                 if (spv >= 0) {  // kept in both walks: identical from here
                                     conv = true;
@@ -338,24 +344,15 @@ __global__ void __launch_bounds__(kLCBlock, HB_LC_MINB) lapcount_kernel(const La
                 }
             }
             const int in_off = __shfl_up_sync(full, val, 1);  // offset of the incoming anchor
-            const double2 fin_anc = make_double2(__shfl_up_sync(full, end_anc.x, 1),
-                                                 __shfl_up_sync(full, end_anc.y, 1));
             if (!exact) {
-                // before the first start: re-walk [0, conv_t) from the final
-                // incoming anchor, shift phase B's values after it
-                double2 a2 = fin_anc;
-                int o2 = 0;
+                // before the first start: phase C's last re-walk (from the
+                // final incoming anchor: a lane is re-evaluated whenever its
+                // predecessor's end state changes) decides [0, conv_t);
+                // phase B's values are shifted after it
                 for (int t = 0; t < t_fs; ++t) {
                     int v = row_pos[lane][t];
                     if (fix && t < conv_t) {
-                        const double2 F = row_pt[lane][t];
-                        const double g2 = dist2_ref(F.x, F.y, a2.x, a2.y);
-                        v = -1;
-                        if (((ends >> t) & 1u) || !(g2 < lo2)) {
-                            o2 += pieces_of(g2, hi2);
-                            a2 = F;
-                            v = o2;
-                        }
+                        v = row_fix[lane][t];
                     } else if (v >= 0) {
                         v += shift;
                     }
@@ -447,7 +444,7 @@ int hb_laplacian_count(const double *pts_in, double *pts_out, const int64_t *sta
     p.counts = counts;
     p.pos = pos;
     const int64_t groups = (n_pts + kGroup - 1) / kGroup;
-    const size_t smem = (size_t)kLCWarps * 32 * kRowPad * (sizeof(double2) + sizeof(int));
+    const size_t smem = (size_t)kLCWarps * 32 * kRowPad * (sizeof(double2) + 2 * sizeof(int));
     if (counts) {
         if (cudaFuncSetAttribute(lapcount_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  (int)smem) != cudaSuccess)

@@ -99,7 +99,7 @@ def main():
     g = json.load(open(os.path.join(ROOT, "tests", "golden", "cfg4.json")))
     npts = [it["n_points"] for it in g["iterations"]]
     caps = {
-        "hb_resample_emit": ("pr_emit_flat_kernel.ncu-rep", "emit of iteration 5 (reads N4, writes N5)",
+        "hb_resample_emit": ("pr_emit_ring_kernel.ncu-rep", "emit of iteration 5 (reads N4, writes N5)",
                              npts[5]),
         "hb_advect_points": ("pr_advect_flat_kernel.ncu-rep", "advect of iteration 4 (N4 points)",
                              npts[4]),

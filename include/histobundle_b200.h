@@ -310,6 +310,41 @@ HB_API int hb_clamp_starts(int64_t *starts, int64_t n_edges, int64_t cap, int64_
 HB_API int hb_probe(const float *rho_layer, int nv, int nu, const double *xy,
              int64_t n, double *value, double *grad, void *stream);
 
+/* ---- edge binning (binning.py:81-177): best-of-restarts Lloyd K-means ----
+ * features (n, d) float64 row-major, d <= 4; centroids (restarts, k, d);
+ * assign (restarts, n) int8 cluster ids (k <= 64); restart lists are int32.
+ * Arithmetic and order follow numpy's (einsum pairs d = 4 products as
+ * (p0 + p2) + (p1 + p3); np.add.at folds in edge order; argmin / argmax take
+ * the first extremum). */
+/* KMeans._assign (binning.py:112-116) for the restarts in active[]: new
+ * nearest centroid per edge; changed[r] |= 1 when any edge moved. */
+HB_API int hb_kmeans_assign(const double *features, int64_t n, int d, int k,
+                            const double *centroids, const int32_t *active, int n_active,
+                            int8_t *assign, int32_t *changed, void *stream);
+/* _update_centroids (binning.py:136-143) for restarts upd[]: sums in edge
+ * order / counts; a cluster left empty keeps its centroid and sets empty[r]. */
+HB_API int hb_kmeans_update(const double *features, int64_t n, int d, int k,
+                            double *centroids, const int32_t *upd, int n_upd,
+                            const int8_t *assign, int32_t *empty, void *stream);
+/* The empty-cluster re-seed (binning.py:145-154) for restarts rs[]; the
+ * workspace holds n_rs * n float64 distances. */
+HB_API size_t hb_kmeans_reseed_workspace_bytes(int64_t n, int n_rs);
+HB_API int hb_kmeans_reseed(const double *features, int64_t n, int d, int k,
+                            double *centroids, const int32_t *rs, int n_rs,
+                            const int8_t *assign, void *workspace, size_t workspace_bytes,
+                            void *stream);
+/* Per-restart inertia partials (restarts x hb_kmeans_inertia_blocks()),
+ * summed by the caller in order: picks the best restart (binning.py:124-130). */
+HB_API int hb_kmeans_inertia_blocks(void);
+HB_API int hb_kmeans_inertia(const double *features, int64_t n, int d, int k,
+                             const double *centroids, int restarts, const int8_t *assign,
+                             double *partial, void *stream);
+/* Davies-Bouldin scatter sums and counts of one clustering (binning.py:
+ * 165-171): scatter[c] = sum of norm(f_i - centroid_c) in edge order. */
+HB_API int hb_kmeans_scatter(const double *features, int64_t n, int d, int k,
+                             const double *centroids, const int8_t *assign, double *scatter,
+                             int64_t *counts, void *stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -18,7 +18,7 @@ LIB_DIR = os.path.join(_PKG, "_lib")
 LIB_PATH = os.path.join(LIB_DIR, "libhb_b200.so")
 INCLUDE = os.path.join(os.path.dirname(_PKG), "include")
 
-SOURCES = ["hb_api.cu", "hb_polyline.cu", "hb_field.cu", "hb_advect.cu", "hb_advect_flat.cu", "hb_lapcount.cu", "hb_splat.cu"]
+SOURCES = ["hb_api.cu", "hb_polyline.cu", "hb_field.cu", "hb_advect.cu", "hb_advect_flat.cu", "hb_lapcount.cu", "hb_splat.cu", "hb_binning.cu"]
 
 NVCC_FLAGS = [
     "-gencode", "arch=compute_100a,code=sm_100a",
@@ -81,6 +81,13 @@ SIGNATURES = {
     "hb_abi_version": (_I, []),
     "hb_last_error": (ctypes.c_char_p, []),
     "hb_device_sm_count": (_I, []),
+    "hb_kmeans_assign": (_I, [_P, _I64, _I, _I, _P, _P, _I, _P, _P, _P]),
+    "hb_kmeans_update": (_I, [_P, _I64, _I, _I, _P, _P, _I, _P, _P, _P]),
+    "hb_kmeans_reseed_workspace_bytes": (_SZ, [_I64, _I]),
+    "hb_kmeans_reseed": (_I, [_P, _I64, _I, _I, _P, _P, _I, _P, _P, _SZ, _P]),
+    "hb_kmeans_inertia_blocks": (_I, []),
+    "hb_kmeans_inertia": (_I, [_P, _I64, _I, _I, _P, _I, _P, _P, _P]),
+    "hb_kmeans_scatter": (_I, [_P, _I64, _I, _I, _P, _P, _P, _P, _P]),
     "hb_launch_count": (ctypes.c_longlong, []),
     "hb_edge_prepare": (_I, [_P, _P, _P, _I64, _D, _D, _D, _D, _P, _P, _P, _P]),
     "hb_to_world_nodes": (_I, [_P, _P, _I64, _D, _D, _D, _P, _P, _P, _P, _P]),

@@ -97,6 +97,7 @@ class _DeviceFeatures:
         if self.d > 4:
             raise ValueError("features with more than 4 columns are not supported")
         self.t = torch.from_numpy(np.ascontiguousarray(features)).to(_dev())
+        self.unique_rows = np.unique(features, axis=0)  # shared by every k
 
 
 def _kmeans_device(df: _DeviceFeatures, k: int, restarts: int,
@@ -109,7 +110,7 @@ def _kmeans_device(df: _DeviceFeatures, k: int, restarts: int,
         raise ValueError("restarts must be >= 1")
     if n < k:
         raise ValueError("k exceeds distinct points")
-    unique_rows = np.unique(f, axis=0)
+    unique_rows = df.unique_rows
     if unique_rows.shape[0] < k:
         raise ValueError("k exceeds distinct points")
     if k > 64:

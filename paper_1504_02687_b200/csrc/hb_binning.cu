@@ -3,15 +3,15 @@
 //
 // Every restart is independent, so the device runs all active restarts of an
 // iteration at once: one thread per (restart, edge) for the assignment step
-// and one warp per (restart, cluster) for the centroid update.  The
+// and one block per restart for the centroid update.  The
 // arithmetic repeats numpy's, in numpy's order:
 //   * squared distance einsum("rnkd,rnkd->rnk") (binning.py:114): for d = 4
 //     numpy pairs the products as (p0 + p2) + (p1 + p3), for d <= 2 it adds
 //     them in order (checked against numpy 2.3 in this container);
 //   * argmin over clusters takes the first minimum (np.argmin);
 //   * np.add.at(sums, assign, features) (binning.py:143) is a left fold in
-//     edge order per (cluster, column): the update warp walks the edges in
-//     order 32 at a time and folds the matching ones lane by lane;
+//     edge order per (cluster, column): the update block stages the edges in
+//     shared-memory tiles and a warp folds each cluster's hits in order;
 //   * centroid = sums / counts (IEEE divide), empty clusters keep their
 //     centroid until re-seeded with the farthest edges (binning.py:145-154):
 //     dist = np.linalg.norm(axis=1) adds the squared columns in order, and
@@ -76,43 +76,64 @@ km_assign_kernel(const double *__restrict__ f, int64_t n, int d, int k,
     if (__any_sync(0xffffffffu, ch) && (threadIdx.x & 31) == 0) atomicOr(changed + r, 1);
 }
 
-// one warp per (restart in `upd`, cluster): sums in edge order, then
-// centroid = sums / count; an empty cluster raises empty[r]
-__global__ void __launch_bounds__(256)
+// One block per restart in `upd`: the edges stream through shared memory in
+// tiles (assignments + feature rows, loaded once for all clusters); warp w
+// folds clusters w, w + 8, ... over each tile in edge order, reading the hit
+// rows as shared-memory broadcasts.  Then centroid = sums / count; an empty
+// cluster raises empty[r].  (A warp per (restart, cluster) streaming the
+// edges from global memory waited one load latency per 32 edges.)
+constexpr int kUpdBlock = 256;
+constexpr int kUpdTile = 1024;
+__global__ void __launch_bounds__(kUpdBlock)
 km_update_kernel(const double *__restrict__ f, int64_t n, int d, int k,
-                 double *__restrict__ cent, const int32_t *__restrict__ upd, int n_upd,
+                 double *__restrict__ cent, const int32_t *__restrict__ upd,
                  const int8_t *__restrict__ assign, int32_t *__restrict__ empty) {
+    __shared__ int8_t s_a[kUpdTile];
+    __shared__ double s_f[kUpdTile * kKmMaxD];
+    __shared__ double s_acc[kKmMaxK * kKmMaxD];
+    __shared__ long long s_cnt[kKmMaxK];
     const unsigned full = 0xffffffffu;
-    const int lane = threadIdx.x & 31;
-    const int64_t w = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-    if (w >= (int64_t)n_upd * k) return;
-    const int r = upd[w / k], c = (int)(w % k);
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int r = upd[blockIdx.x];
     const int8_t *a = assign + (int64_t)r * n;
-    double acc[kKmMaxD] = {0.0, 0.0, 0.0, 0.0};
-    int64_t cnt = 0;
-    for (int64_t i0 = 0; i0 < n; i0 += 32) {
-        const int64_t i = i0 + lane;
-        const bool hit = i < n && a[i] == c;
-        unsigned m = __ballot_sync(full, hit);
-        if (!m) continue;
-        double v[kKmMaxD] = {0.0, 0.0, 0.0, 0.0};
-        if (hit)
-            for (int j = 0; j < d; ++j) v[j] = f[i * d + j];
-        cnt += __popc(m);
-        while (m) {  // np.add.at: edges in ascending order
-            const int b = __ffs(m) - 1;
-            m &= m - 1;
-            for (int j = 0; j < kKmMaxD; ++j) {
-                const double x = __shfl_sync(full, v[j], b);
-                if (j < d) acc[j] = dadd(acc[j], x);
+    for (int t = threadIdx.x; t < k * d; t += kUpdBlock) s_acc[t] = 0.0;
+    for (int t = threadIdx.x; t < k; t += kUpdBlock) s_cnt[t] = 0;
+    for (int64_t t0 = 0; t0 < n; t0 += kUpdTile) {
+        const int m = (int)(n - t0 < kUpdTile ? n - t0 : kUpdTile);
+        __syncthreads();  // previous tile consumed (and accumulators initialised)
+        for (int t = threadIdx.x; t < m; t += kUpdBlock) s_a[t] = a[t0 + t];
+        for (int t = threadIdx.x; t < m * d; t += kUpdBlock) s_f[t] = f[t0 * d + t];
+        __syncthreads();
+        // lane j < d owns column j's chain; the next hit's value is read
+        // before the current one is added (one shared load in flight)
+        const int col = lane < d ? lane : 0;
+        for (int c = warp; c < k; c += kUpdBlock / 32) {
+            double acc = lane < d ? s_acc[c * d + col] : 0.0;
+            long long cnt = 0;
+            for (int w0 = 0; w0 < m; w0 += 32) {
+                unsigned hits = __ballot_sync(full, w0 + lane < m && s_a[w0 + lane] == c);
+                if (!hits) continue;
+                cnt += __popc(hits);
+                double v = s_f[(w0 + __ffs(hits) - 1) * d + col];
+                hits &= hits - 1;
+                while (hits) {  // np.add.at: edges in ascending order
+                    const double nv = s_f[(w0 + __ffs(hits) - 1) * d + col];
+                    hits &= hits - 1;
+                    acc = dadd(acc, v);
+                    v = nv;
+                }
+                acc = dadd(acc, v);
             }
+            if (lane < d) s_acc[c * d + lane] = acc;
+            if (lane == 0) s_cnt[c] += cnt;
         }
     }
-    if (lane == 0) {
+    __syncthreads();
+    for (int c = threadIdx.x; c < k; c += kUpdBlock) {
         double *cc = cent + ((int64_t)r * k + c) * d;
-        if (cnt > 0) {
-            const double cn = (double)cnt;
-            for (int j = 0; j < d; ++j) cc[j] = __ddiv_rn(acc[j], cn);
+        if (s_cnt[c] > 0) {
+            const double cn = (double)s_cnt[c];
+            for (int j = 0; j < d; ++j) cc[j] = __ddiv_rn(s_acc[c * d + j], cn);
         } else {
             atomicOr(empty + r, 1);
         }
@@ -268,9 +289,8 @@ int hb_kmeans_update(const double *features, int64_t n, int d, int k, double *ce
         (n_upd > 0 && (!upd || !assign || !empty)))
         return set_error(HB_EINVAL, "hb_kmeans_update: bad arguments");
     if (n_upd == 0) return HB_OK;
-    const int64_t warps = (int64_t)n_upd * k;
-    km_update_kernel<<<(unsigned)((warps * 32 + 255) / 256), 256, 0, km_stream(stream)>>>(
-        features, n, d, k, cent, upd, n_upd, assign, empty);
+    km_update_kernel<<<n_upd, kUpdBlock, 0, km_stream(stream)>>>(features, n, d, k, cent, upd,
+                                                               assign, empty);
     return check_launch("hb_kmeans_update");
 }
 

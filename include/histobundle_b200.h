@@ -263,6 +263,18 @@ HB_API int hb_laplacian_count(const double *pts_in, double *pts_out, const int64
                               void *stream);
 
 /* Deterministic fixed-order sum of n doubles into *out (one block). */
+/* hb_advect_points then hb_laplacian_count (lap_passes <= 1) in one pass:
+ * each staged group of points is advected in shared memory (the flat
+ * advect's arithmetic and deferral queue), then smoothed and counted; the
+ * advected but unsmoothed points never go to memory.  In place.  Same
+ * results as the two calls; `moved` / `disp_partials` as hb_advect_points. */
+HB_API int hb_advect_laplacian_count(double *pts, const int64_t *starts, int64_t n_edges,
+                                     int64_t n_pts, const int32_t *edge_layer, const float *rho,
+                                     const float *grad_field, int nbins, int nv, int nu,
+                                     double h, double eps, double min_step, int fixed_step,
+                                     double lap_factor, int lap_passes, double delta,
+                                     int64_t *counts, int32_t *pos, unsigned long long *moved,
+                                     double *disp_partials, void *stream);
 HB_API int hb_reduce_f64(const double *in, int64_t n, double *out, void *stream);
 
 /* _kernels.resample_count (_kernels.py:203-232): counts[e] = output points

@@ -81,6 +81,8 @@ SIGNATURES = {
     "hb_abi_version": (_I, []),
     "hb_last_error": (ctypes.c_char_p, []),
     "hb_device_sm_count": (_I, []),
+    "hb_advect_laplacian_count": (_I, [_P, _P, _I64, _I64, _P, _P, _P, _I, _I, _I, _D, _D, _D,
+                                       _I, _D, _I, _D, _P, _P, _P, _P, _P]),
     "hb_kmeans_assign": (_I, [_P, _I64, _I, _I, _P, _P, _I, _P, _P, _P]),
     "hb_kmeans_update": (_I, [_P, _I64, _I, _I, _P, _P, _I, _P, _P, _P]),
     "hb_kmeans_reseed_workspace_bytes": (_SZ, [_I64, _I]),

@@ -50,6 +50,28 @@ struct LapCount {
     double delta = 1.0;
     int64_t *counts = nullptr;  // nullable: Laplacian only
     int32_t *pos = nullptr;
+    // fused advection (hb_advect_laplacian_count): _kernels.advect on each
+    // staged group before its Laplacian
+    const int32_t *edge_layer = nullptr;
+    const float *rho = nullptr;
+    const float4 *gf = nullptr;
+    int nbins = 1;
+    unsigned plane = 0;
+    int nv = 0, nu = 0;
+    double xhi = 0.0, yhi = 0.0, h = 0.0, eps = 1e-8, min_step = 0.25;
+    int fixed = 0;
+    unsigned long long *moved = nullptr;
+    double *partials = nullptr;
+};
+
+// Deferral queue of the fused advection, per warp (see hb_advect_flat.cu):
+// points whose step search did not finish with the first candidate wait here
+// with their exact state and are finished 32 at a time.
+constexpr int kAQCap = 64;
+struct AdvQueue {
+    double dx[kAQCap], dy[kAQCap], r0[kAQCap], m[kAQCap];
+    unsigned base[kAQCap];
+    int slot[kAQCap];  // 0..255: row_pt[slot / kRun][slot % kRun]; 256: the halo point
 };
 
 constexpr int kLCBlock = 256;
@@ -88,8 +110,147 @@ __device__ __forceinline__ int pieces_of(double g2, double hi2) {
     return pieces;
 }
 
-template <bool COUNT>
-__global__ void __launch_bounds__(kLCBlock, HB_LC_MINB) lapcount_kernel(const LapCount p) {
+// The advection of one staged group (_kernels.py:144-200), as the flat
+// advect does it: round k gives lane l the point base + 1 + 32k + l (the last
+// is the halo, base + kGroup); one step candidate per lane, unfinished
+// searches wait in the queue with their exact state and are finished in
+// full-warp rounds; the queue is drained before the Laplacian reads the group.
+template <int ADV>
+__device__ __forceinline__ void advect_group(const LapCount &p, double2 (*row_pt)[kRowPad],
+                                             double2 *s_halo, AdvQueue *aq, int64_t base, int n,
+                                             int64_t P1, unsigned mask, unsigned ends,
+                                             int64_t e_first, bool start_next, bool end_next,
+                                             unsigned &my_moved, double &my_disp) {
+    const unsigned full = 0xffffffffu;
+    const int lane = threadIdx.x & 31;
+    const unsigned lt_mask = (1u << lane) - 1u;
+    const bool sn = __shfl_sync(full, start_next ? 1 : 0, 31) != 0;
+    const bool en_ = __shfl_sync(full, end_next ? 1 : 0, 31) != 0;
+    const double min_step = p.min_step;
+    auto slot_ptr = [&](int sl) -> double2 * {
+        return sl < kGroup ? &row_pt[sl / kRun][sl % kRun] : s_halo;
+    };
+    auto test = [&](unsigned lb, double x, double y, double dx, double dy, double m, double r0,
+                    double &nx, double &ny) -> bool {
+        nx = clamp_ref(dadd(x, dmul(m, dx)), 1.0, p.xhi);
+        ny = clamp_ref(dadd(y, dmul(m, dy)), 1.0, p.yhi);
+        const double v = ADV == 1 ? bilinear_quad<true>(p.gf, lb, p.nv, p.nu, nx, ny)
+                                  : bilinear_ref(p.rho + lb, p.nv, p.nu, nx, ny);
+        return v >= r0;
+    };
+    auto accept = [&](int sl, double x, double y, double nx, double ny) {
+        if (nx != x || ny != y) {  // _kernels.py:187-190
+            *slot_ptr(sl) = make_double2(nx, ny);
+            ++my_moved;
+            my_disp = dadd(my_disp, hypot_ref(dsub(nx, x), dsub(ny, y)));
+        }
+    };
+    int qn = 0;
+    auto queue_round = [&](int take, int rounds) {
+        const bool have = lane < take;
+        const int q = qn - take + lane;
+        double dx = 0.0, dy = 0.0, r0 = 0.0, m = -1.0;
+        unsigned lb = 0;
+        int sl = 0;
+        if (have) {
+            dx = aq->dx[q]; dy = aq->dy[q]; r0 = aq->r0[q]; m = aq->m[q];
+            lb = aq->base[q]; sl = aq->slot[q];
+        }
+        qn -= take;
+        __syncwarp();
+        double x = 0.0, y = 0.0;
+        if (have) {
+            const double2 pt = *slot_ptr(sl);
+            x = pt.x;
+            y = pt.y;
+        }
+        for (int k = 0; have && (rounds < 0 || k < rounds) && m >= min_step; ++k) {
+            double nx, ny;
+            if (test(lb, x, y, dx, dy, m, r0, nx, ny)) {
+                accept(sl, x, y, nx, ny);
+                m = -1.0;
+                break;
+            }
+            m = dmul(m, 0.5);
+        }
+        const bool pend = have && m >= min_step;
+        const unsigned pm = __ballot_sync(full, pend);
+        if (pend) {
+            const int w = qn + __popc(pm & lt_mask);
+            aq->dx[w] = dx; aq->dy[w] = dy; aq->r0[w] = r0; aq->m[w] = m;
+            aq->base[w] = lb; aq->slot[w] = sl;
+        }
+        qn += __popc(pm);
+        __syncwarp();
+    };
+    for (int rd = 0; rd < kGroup / 32; ++rd) {
+        const int i = 1 + rd * 32 + lane;  // group index of this lane's point
+        const int r = i / kRun < 31 ? i / kRun : 31, t = i % kRun;
+        const unsigned mr = __shfl_sync(full, mask, r), er = __shfl_sync(full, ends, r);
+        const int64_t efr = __shfl_sync(full, e_first, r);
+        bool inter;
+        int64_t e;
+        if (i < kGroup) {
+            inter = i < n && !((mr >> t) & 1u) && !((er >> t) & 1u);
+            e = efr + __popc(mr & ((2u << t) - 1u) & ~1u);
+        } else {  // the halo point, base + kGroup
+            inter = base + kGroup < P1 && !sn && !en_;
+            e = efr + __popc(mr & ~1u) + (sn ? 1 : 0);
+        }
+        const unsigned lb = (p.nbins > 1 && inter) ? (unsigned)p.edge_layer[e] * p.plane : 0u;
+        bool pend = false;
+        double dx = 0.0, dy = 0.0, r0 = 0.0, m = -1.0;
+        if (inter) {
+            const double2 pt = *slot_ptr(i);
+            const double x = pt.x, y = pt.y;
+            double Gx, Gy;  // _kernels.py:163-175 (G = 2*gradient)
+            if (ADV == 1)
+                gradient2_value_quad(QuadField{p.gf, lb}, p.nv, p.nu, x, y, Gx, Gy, r0);
+            else
+                gradient2_value_ref(p.rho + lb, p.nv, p.nu, x, y, Gx, Gy, r0);
+            const double Gn = hypot_ref(Gx, Gy);
+            if (Gn < 2.0 * p.eps) {
+                dx = dmul(0.5, Gx) / p.eps;
+                dy = dmul(0.5, Gy) / p.eps;
+            } else {
+                dx = Gx / Gn;
+                dy = Gy / Gn;
+            }
+            m = p.h;
+            if (p.fixed) {  // _kernels.py:177-185: one step, always taken
+                accept(i, x, y, clamp_ref(dadd(x, dmul(m, dx)), 1.0, p.xhi),
+                       clamp_ref(dadd(y, dmul(m, dy)), 1.0, p.yhi));
+                m = -1.0;
+            }
+            if (m >= min_step) {
+                double nx, ny;
+                if (test(lb, x, y, dx, dy, m, r0, nx, ny)) {
+                    accept(i, x, y, nx, ny);
+                    m = -1.0;
+                } else {
+                    m = dmul(m, 0.5);
+                }
+            }
+            pend = m >= min_step;
+        }
+        const unsigned pm = __ballot_sync(full, pend);
+        if (pm) {
+            if (pend) {
+                const int w = qn + __popc(pm & lt_mask);
+                aq->dx[w] = dx; aq->dy[w] = dy; aq->r0[w] = r0; aq->m[w] = m;
+                aq->base[w] = lb; aq->slot[w] = i;
+            }
+            qn += __popc(pm);
+            __syncwarp();
+            while (qn >= 32) queue_round(32, 1);
+        }
+    }
+    while (qn > 0) queue_round(qn < 32 ? qn : 32, -1);  // the group must be final
+}
+
+// (the fused kernels' shared memory allows 3 blocks per SM: 85 registers)
+template <bool COUNT, int ADV>  // ADV: 0 none, 1 quad field, 2 density gathers
+__global__ void __launch_bounds__(kLCBlock, ADV ? 3 : HB_LC_MINB) lapcount_kernel(const LapCount p) {
     // per warp: the group's points as [run][point] (original, then final)
     // and its output codes; rows padded so lanes walking rows hit distinct banks
     extern __shared__ unsigned char lc_smem[];
@@ -104,6 +265,15 @@ __global__ void __launch_bounds__(kLCBlock, HB_LC_MINB) lapcount_kernel(const La
     // final write-out does not walk again
     int (*row_fix)[kRowPad] = reinterpret_cast<int (*)[kRowPad]>(
         lc_smem + (sizeof(double2) + sizeof(int)) * kLCWarps * 32 * kRowPad) + (size_t)wib * 32;
+    // fused advection: the queue and the halo point (the next group's first
+    // point, advected here because this group's Laplacian needs it)
+    AdvQueue *aq = reinterpret_cast<AdvQueue *>(
+        lc_smem + (sizeof(double2) + 2 * sizeof(int)) * kLCWarps * 32 * kRowPad) + wib;
+    double2 *s_halo = reinterpret_cast<double2 *>(
+        lc_smem + (sizeof(double2) + 2 * sizeof(int)) * kLCWarps * 32 * kRowPad +
+        sizeof(AdvQueue) * kLCWarps) + wib;
+    unsigned my_moved = 0;
+    double my_disp = 0.0;
     const double lo2 = COUNT ? sqrt_lt_bound(0.5 * p.delta) : 0.0;  // _kernels.py:211-212
     const double hi2 = COUNT ? sqrt_gt_bound(1.5 * p.delta) : 0.0;
     constexpr unsigned run_bits = kRun == 32 ? 0xffffffffu : ((1u << kRun) - 1u);
@@ -123,7 +293,7 @@ __global__ void __launch_bounds__(kLCBlock, HB_LC_MINB) lapcount_kernel(const La
     }
     e0 = __shfl_sync(full, e0, 0);
     e1 = __shfl_sync(full, e1, 0);
-    if (e0 >= e1) return;
+    if (e0 < e1) {
     const int64_t P0 = p.starts[e0], P1 = p.starts[e1];
 
     int64_t e_g = e0;   // edge containing the group's first point
@@ -144,6 +314,7 @@ __global__ void __launch_bounds__(kLCBlock, HB_LC_MINB) lapcount_kernel(const La
         // ---- edge starts in (base, base + kGroup] -> per-run bit masks
         unsigned mask = 0u;       // starts at run positions 0..kRun-1
         bool start_next = false;  // (lane 31) point base + kGroup starts an edge
+        bool end_next = false;    // point base + kGroup ends one
         int64_t e_scan = e_g + 1, s_last = s_g;
         int n_st = 0;
         for (;;) {
@@ -163,7 +334,11 @@ __global__ void __launch_bounds__(kLCBlock, HB_LC_MINB) lapcount_kernel(const La
             const int c = __popc(in);
             n_st += c;
             if (c) s_last = __shfl_sync(full, sv, c - 1);
-            if (in != full) break;
+            if (in != full) {
+                // (fused advection) does point base + kGroup end an edge?
+                end_next = __shfl_sync(full, rel, c) == kGroup + 1;
+                break;
+            }
             e_scan += 32;
         }
         if (lane == 0 && s_g == base) mask |= 1u;
@@ -183,6 +358,18 @@ __global__ void __launch_bounds__(kLCBlock, HB_LC_MINB) lapcount_kernel(const La
         const int64_t e_first = e_cur;
         const unsigned prev_mask = __shfl_up_sync(full, mask, 1);
         __syncwarp();
+        if (ADV) {
+            // _kernels.advect (in place) on points base+1 .. base+kGroup; point
+            // base was the previous group's halo (or starts the range: an
+            // endpoint, never moved)
+            if (lane == 0 && base != P0) row_pt[0][0] = *s_halo;
+            if (lane == 31) *s_halo = next_first;
+            __syncwarp();
+            advect_group<ADV>(p, row_pt, s_halo, aq, base, n, P1, mask, ends, e_first,
+                              start_next, end_next, my_moved, my_disp);
+            __syncwarp();
+            if (lane == 31) next_first = *s_halo;
+        }
 
         // ---- run boundaries, read before any lane overwrites its row
         const int j0 = lane * kRun;
@@ -380,6 +567,31 @@ __global__ void __launch_bounds__(kLCBlock, HB_LC_MINB) lapcount_kernel(const La
         s_g = s_last;
         e_g += n_st;
     }
+    }  // e0 < e1
+    if (ADV) {
+        // per-block metrics in a fixed order (deterministic for a fixed grid)
+        __shared__ double red_d[kLCWarps];
+        __shared__ unsigned red_m[kLCWarps];
+        for (int o = 16; o; o >>= 1) {
+            my_moved += __shfl_down_sync(full, my_moved, o);
+            my_disp = dadd(my_disp, __shfl_down_sync(full, my_disp, o));
+        }
+        if (lane == 0) {
+            red_d[wib] = my_disp;
+            red_m[wib] = my_moved;
+        }
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            double sd = 0.0;
+            unsigned long long sm = 0;
+            for (int w = 0; w < kLCWarps; ++w) {
+                sd = dadd(sd, red_d[w]);
+                sm += red_m[w];
+            }
+            p.partials[blockIdx.x] = sd;
+            if (sm) atomicAdd(p.moved, sm);
+        }
+    }
 }
 
 }  // namespace hb
@@ -397,7 +609,75 @@ static unsigned lc_grid(K kernel, int64_t groups, size_t smem) {
     return (unsigned)(want < 1 ? 1 : want);
 }
 
+template <bool COUNT, int ADV>
+static int launch_lc(const LapCount &p, int64_t groups, size_t smem, cudaStream_t st) {
+    if (cudaFuncSetAttribute(lapcount_kernel<COUNT, ADV>,
+                             cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
+        return check_launch("hb_laplacian_count(smem)", 0);
+    lapcount_kernel<COUNT, ADV>
+        <<<lc_grid(lapcount_kernel<COUNT, ADV>, groups, smem), kLCBlock, smem, st>>>(p);
+    return HB_OK;
+}
+
 extern "C" {
+
+int hb_advect_laplacian_count(double *pts, const int64_t *starts, int64_t n_edges, int64_t n_pts,
+                              const int32_t *edge_layer, const float *rho,
+                              const float *grad_field, int nbins, int nv, int nu, double h,
+                              double eps, double min_step, int fixed_step, double lap_factor,
+                              int lap_passes, double delta, int64_t *counts, int32_t *pos,
+                              unsigned long long *moved, double *disp_partials, void *stream) {
+    if (n_edges < 0 || n_pts < 0 || lap_passes < 0 || lap_passes > 1 || nbins < 1 || nv < 3 ||
+        nu < 3 || nv > kMaxDim || nu > kMaxDim || !moved || !disp_partials || !(h >= 0.0) ||
+        (counts && (!pos || !(delta > 0))) ||
+        (n_pts > 0 && (!pts || !starts || !edge_layer || !rho)))
+        return set_error(HB_EINVAL, "hb_advect_laplacian_count: bad arguments");
+    if ((int64_t)nbins * nv * nu >= ((int64_t)1 << 31) ||
+        (grad_field && (int64_t)kQuadRec * nbins * nv * nu >= ((int64_t)1 << 32)))
+        return set_error(HB_EINVAL, "hb_advect_laplacian_count: field above 2^31 cells");
+    if (n_pts >= ((int64_t)1 << 31))
+        return set_error(HB_EINVAL, "hb_advect_laplacian_count: more than 2^31 points");
+    cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+    if (cudaMemsetAsync(disp_partials, 0, sizeof(double) * kMaxStreamBlocks, st) != cudaSuccess)
+        return check_launch("hb_advect_laplacian_count(memset)", 0);
+    if (n_pts == 0 || n_edges == 0) return HB_OK;
+    LapCount p;
+    p.pin = reinterpret_cast<const double2 *>(pts);
+    p.pout = reinterpret_cast<double2 *>(pts);
+    p.starts = starts;
+    p.n_edges = n_edges;
+    p.n_pts = n_pts;
+    p.factor = lap_factor;
+    p.lap = lap_passes;
+    p.delta = delta;
+    p.counts = counts;
+    p.pos = pos;
+    p.edge_layer = edge_layer;
+    p.rho = rho;
+    p.gf = reinterpret_cast<const float4 *>(grad_field);
+    p.nbins = nbins;
+    p.plane = (unsigned)((int64_t)nv * nu);
+    p.nv = nv;
+    p.nu = nu;
+    p.xhi = (double)(nu - 2);  // == (nu - 1.0) - 1.0 exactly (_kernels.py:158-159)
+    p.yhi = (double)(nv - 2);
+    p.h = h;
+    p.eps = eps;
+    p.min_step = min_step;
+    p.fixed = fixed_step;
+    p.moved = moved;
+    p.partials = disp_partials;
+    const int64_t groups = (n_pts + kGroup - 1) / kGroup;
+    const size_t smem = (size_t)kLCWarps * 32 * kRowPad * (sizeof(double2) + 2 * sizeof(int)) +
+                        (sizeof(AdvQueue) + sizeof(double2)) * kLCWarps;
+    int rc;
+    if (p.gf)
+        rc = counts ? launch_lc<true, 1>(p, groups, smem, st) : launch_lc<false, 1>(p, groups, smem, st);
+    else
+        rc = counts ? launch_lc<true, 2>(p, groups, smem, st) : launch_lc<false, 2>(p, groups, smem, st);
+    if (rc) return rc;
+    return check_launch("hb_advect_laplacian_count");
+}
 
 int hb_laplacian_count(const double *pts_in, double *pts_out, const int64_t *starts,
                        int64_t n_edges, int64_t n_pts, double lap_factor, int lap_passes,
@@ -445,17 +725,9 @@ int hb_laplacian_count(const double *pts_in, double *pts_out, const int64_t *sta
     p.pos = pos;
     const int64_t groups = (n_pts + kGroup - 1) / kGroup;
     const size_t smem = (size_t)kLCWarps * 32 * kRowPad * (sizeof(double2) + 2 * sizeof(int));
-    if (counts) {
-        if (cudaFuncSetAttribute(lapcount_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 (int)smem) != cudaSuccess)
-            return check_launch("hb_laplacian_count(smem)", 0);
-        lapcount_kernel<true><<<lc_grid(lapcount_kernel<true>, groups, smem), kLCBlock, smem, st>>>(p);
-    } else {
-        if (cudaFuncSetAttribute(lapcount_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 (int)smem) != cudaSuccess)
-            return check_launch("hb_laplacian_count(smem)", 0);
-        lapcount_kernel<false><<<lc_grid(lapcount_kernel<false>, groups, smem), kLCBlock, smem, st>>>(p);
-    }
+    const int rc = counts ? launch_lc<true, 0>(p, groups, smem, st)
+                          : launch_lc<false, 0>(p, groups, smem, st);
+    if (rc) return rc;
     return check_launch("hb_laplacian_count");
 }
 

@@ -365,6 +365,14 @@ def test_bundle_cfg1_bit_exact_splat_paths(mode, monkeypatch):
     _check_run(1)
 
 
+@pytest.mark.parametrize("k", [1, 2])
+def test_bundle_bit_exact_fused_field(k, monkeypatch):
+    """hb_advect_laplacian_count (advection inside the Laplacian + count
+    pass) gives the same bits as the two kernels."""
+    monkeypatch.setenv("HB_FUSED_FIELD", "1")
+    _check_run(k)
+
+
 def test_bundle_cfg2_bit_exact():
     _check_run(2)
 

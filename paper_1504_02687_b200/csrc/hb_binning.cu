@@ -76,65 +76,96 @@ km_assign_kernel(const double *__restrict__ f, int64_t n, int d, int k,
     if (__any_sync(0xffffffffu, ch) && (threadIdx.x & 31) == 0) atomicOr(changed + r, 1);
 }
 
-// One block per restart in `upd`: the edges stream through shared memory in
-// tiles (assignments + feature rows, loaded once for all clusters); warp w
-// folds clusters w, w + 8, ... over each tile in edge order, reading the hit
-// rows as shared-memory broadcasts.  Then centroid = sums / count; an empty
-// cluster raises empty[r].  (A warp per (restart, cluster) streaming the
-// edges from global memory waited one load latency per 32 edges.)
+// One block per restart in `upd`.  The edges stream through shared memory in
+// tiles of 1024 (assignments + feature rows); each tile is bucketed by
+// cluster, stably (per 32-edge window: rank among same-cluster lanes by
+// __match_any_sync, then window and cluster prefixes), and thread (c, j)
+// folds column j of cluster c's rows in edge order -- one float64 chain per
+// (cluster, column), as np.add.at orders it, with the next row read ahead.
+// Then centroid = sums / count; an empty cluster raises empty[r].
 constexpr int kUpdBlock = 256;
 constexpr int kUpdTile = 1024;
+constexpr int kUpdWin = kUpdTile / 32;
 __global__ void __launch_bounds__(kUpdBlock)
 km_update_kernel(const double *__restrict__ f, int64_t n, int d, int k,
                  double *__restrict__ cent, const int32_t *__restrict__ upd,
                  const int8_t *__restrict__ assign, int32_t *__restrict__ empty) {
     __shared__ int8_t s_a[kUpdTile];
+    __shared__ short s_list[kUpdTile];
     __shared__ double s_f[kUpdTile * kKmMaxD];
-    __shared__ double s_acc[kKmMaxK * kKmMaxD];
-    __shared__ long long s_cnt[kKmMaxK];
+    __shared__ short s_wc[kUpdWin][kKmMaxK];  // per (window, cluster): count, then offset
+    __shared__ int s_base[kKmMaxK + 1];
     const unsigned full = 0xffffffffu;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int r = upd[blockIdx.x];
     const int8_t *a = assign + (int64_t)r * n;
-    for (int t = threadIdx.x; t < k * d; t += kUpdBlock) s_acc[t] = 0.0;
-    for (int t = threadIdx.x; t < k; t += kUpdBlock) s_cnt[t] = 0;
+    // thread t < k*d owns the chain of cluster t / d, column t % d
+    const int my_c = threadIdx.x / d, my_j = threadIdx.x % d;
+    const bool chain = threadIdx.x < k * d;
+    double acc = 0.0;
+    long long cnt = 0;
     for (int64_t t0 = 0; t0 < n; t0 += kUpdTile) {
         const int m = (int)(n - t0 < kUpdTile ? n - t0 : kUpdTile);
-        __syncthreads();  // previous tile consumed (and accumulators initialised)
+        __syncthreads();  // the previous tile is consumed
         for (int t = threadIdx.x; t < m; t += kUpdBlock) s_a[t] = a[t0 + t];
         for (int t = threadIdx.x; t < m * d; t += kUpdBlock) s_f[t] = f[t0 * d + t];
+        for (int t = threadIdx.x; t < kUpdWin * k; t += kUpdBlock) s_wc[t / k][t % k] = 0;
         __syncthreads();
-        // lane j < d owns column j's chain; the next hit's value is read
-        // before the current one is added (one shared load in flight)
-        const int col = lane < d ? lane : 0;
-        for (int c = warp; c < k; c += kUpdBlock / 32) {
-            double acc = lane < d ? s_acc[c * d + col] : 0.0;
-            long long cnt = 0;
-            for (int w0 = 0; w0 < m; w0 += 32) {
-                unsigned hits = __ballot_sync(full, w0 + lane < m && s_a[w0 + lane] == c);
-                if (!hits) continue;
-                cnt += __popc(hits);
-                double v = s_f[(w0 + __ffs(hits) - 1) * d + col];
-                hits &= hits - 1;
-                while (hits) {  // np.add.at: edges in ascending order
-                    const double nv = s_f[(w0 + __ffs(hits) - 1) * d + col];
-                    hits &= hits - 1;
+        // window counts and ranks
+        int rank[kUpdWin / (kUpdBlock / 32)];
+        for (int q = 0; q < kUpdWin / (kUpdBlock / 32); ++q) {
+            const int wi = warp + q * (kUpdBlock / 32);
+            const int e = wi * 32 + lane;
+            const int c = e < m ? s_a[e] : -1;
+            const unsigned peers = __match_any_sync(full, c);
+            rank[q] = __popc(peers & ((1u << lane) - 1u));
+            if (c >= 0 && rank[q] == 0) s_wc[wi][c] = (short)__popc(peers);
+        }
+        __syncthreads();
+        // per cluster: window offsets (exclusive) and the tile count
+        if (threadIdx.x < k) {
+            int run = 0;
+            for (int wi = 0; wi < kUpdWin; ++wi) {
+                const int v = s_wc[wi][threadIdx.x];
+                s_wc[wi][threadIdx.x] = (short)run;
+                run += v;
+            }
+            s_base[threadIdx.x + 1] = run;
+        }
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            s_base[0] = 0;
+            for (int c = 0; c < k; ++c) s_base[c + 1] += s_base[c];
+        }
+        __syncthreads();
+        for (int q = 0; q < kUpdWin / (kUpdBlock / 32); ++q) {
+            const int wi = warp + q * (kUpdBlock / 32);
+            const int e = wi * 32 + lane;
+            if (e < m) {
+                const int c = s_a[e];
+                s_list[s_base[c] + s_wc[wi][c] + rank[q]] = (short)e;
+            }
+        }
+        __syncthreads();
+        if (chain) {
+            const int lo = s_base[my_c], hi = s_base[my_c + 1];
+            cnt += hi - lo;
+            if (lo < hi) {
+                double v = s_f[s_list[lo] * d + my_j];
+                for (int q = lo + 1; q < hi; ++q) {  // np.add.at: edges in order
+                    const double nv = s_f[s_list[q] * d + my_j];
                     acc = dadd(acc, v);
                     v = nv;
                 }
                 acc = dadd(acc, v);
             }
-            if (lane < d) s_acc[c * d + lane] = acc;
-            if (lane == 0) s_cnt[c] += cnt;
         }
     }
-    __syncthreads();
-    for (int c = threadIdx.x; c < k; c += kUpdBlock) {
-        double *cc = cent + ((int64_t)r * k + c) * d;
-        if (s_cnt[c] > 0) {
-            const double cn = (double)s_cnt[c];
-            for (int j = 0; j < d; ++j) cc[j] = __ddiv_rn(s_acc[c * d + j], cn);
-        } else {
+    if (chain) {
+        double *cc = cent + ((int64_t)r * k + my_c) * d;
+        if (cnt > 0) {
+            cc[my_j] = __ddiv_rn(acc, (double)cnt);
+        } else if (my_j == 0) {
             atomicOr(empty + r, 1);
         }
     }

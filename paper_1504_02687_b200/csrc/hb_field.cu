@@ -57,7 +57,10 @@ __device__ __forceinline__ void cp_async_wait() {
 // float64 add latency of one chain hides behind the others) and streams them
 // in 32-row tiles through a kColStages-deep cp.async ring in shared memory;
 // every row of C leaves as coalesced 256-byte stores.
-constexpr int kColStages = 4;
+#ifndef HB_COL_STAGES
+#define HB_COL_STAGES 4
+#endif
+constexpr int kColStages = HB_COL_STAGES;
 // 1 column per lane measured best (config 4 column fold: 20.5 us vs 30.8 us
 // with 2 -- more warps beat interleaved chains on this latency-bound fold)
 #ifndef HB_COL_CPL
@@ -65,7 +68,10 @@ constexpr int kColStages = 4;
 #endif
 constexpr int kColCPL = HB_COL_CPL;
 constexpr int kColW = 32 * kColCPL;                       // columns per warp
-constexpr int kColWarps = kColCPL == 1 ? 2 : 1;           // <= 32 KB static smem
+#ifndef HB_COL_WARPS
+#define HB_COL_WARPS (kColCPL == 1 ? 2 : 1)
+#endif
+constexpr int kColWarps = HB_COL_WARPS;  // kColWarps * kColStages * 4 KB <= 48 KB static smem
 
 __global__ void __launch_bounds__(kColWarps * 32)
 col_fold_kernel(const float *__restrict__ in, int nbins, int nv, int nu,
@@ -153,7 +159,10 @@ col_fold_kernel(const float *__restrict__ in, int nbins, int nv, int nu,
 // tiles through a kRowStages-deep cp.async ring (rows padded to 33 doubles:
 // the lanes' column walks hit distinct banks); each lane folds its own row
 // of a tile left to right, then the tile is stored back coalesced.
-constexpr int kRowStages = 4;
+#ifndef HB_ROW_STAGES
+#define HB_ROW_STAGES 4
+#endif
+constexpr int kRowStages = HB_ROW_STAGES;
 
 __global__ void __launch_bounds__(32)
 row_scan_kernel(double *__restrict__ table, int64_t n_rows, int nu) {

@@ -292,7 +292,8 @@ HB_API int hb_scan_counts(const int64_t *counts, int64_t n_edges, int64_t *new_s
 /* _kernels.resample_emit (_kernels.py:235-272) fused with the next
  * iteration's accumulate: writes the resampled polylines into `out` at
  * new_starts and, when counts != NULL, rasterises every output segment into
- * counts (same contract as hb_splat).  Warps take work off one per-device
+ * counts (same contract as hb_splat; group may be NULL: every edge in
+ * group 0).  Warps take work off one per-device
  * counter that the call zeroes on `stream` first, so emits on one device
  * must not run concurrently on different streams. */
 HB_API int hb_resample_emit(const double *pts, const int64_t *starts,

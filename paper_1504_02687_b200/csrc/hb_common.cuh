@@ -260,13 +260,11 @@ __device__ __forceinline__ void gradient_ref(const float *__restrict__ rho, int 
 // (0 for an edge's first segment, 1 otherwise: the junction cell belongs to
 // the earlier segment).  A zero-length segment contributes only when k0 == 0.
 // Cell = floor(x0 + (k*dx)*(1/steps) + 0.5) exactly as the reference.
+// (endpoint cells already rounded: x = floor(px + 0.5))
 template <typename T>
-__device__ __forceinline__ void dda_splat(double px0, double py0, double px1,
-                                          double py1, int k0, T w,
-                                          T *__restrict__ layer, int nv, int nu,
-                                          int32_t *__restrict__ status) {
-    const int x0 = cell_round(px0), y0 = cell_round(py0);
-    const int x1 = cell_round(px1), y1 = cell_round(py1);
+__device__ __forceinline__ void dda_splat_cells(int x0, int y0, int x1, int y1, int k0, T w,
+                                                T *__restrict__ layer, int nv, int nu,
+                                                int32_t *__restrict__ status) {
     const int dx = x1 - x0, dy = y1 - y0;
     const int steps = max(abs(dx), abs(dy));
     if (steps == 0) {
@@ -313,6 +311,15 @@ __device__ __forceinline__ void dda_splat(double px0, double py0, double px1,
             atomicAdd(layer + (y0 + sy * k) * nu + u, w);
         }
     }
+}
+
+template <typename T>
+__device__ __forceinline__ void dda_splat(double px0, double py0, double px1,
+                                          double py1, int k0, T w,
+                                          T *__restrict__ layer, int nv, int nu,
+                                          int32_t *__restrict__ status) {
+    dda_splat_cells<T>(cell_round(px0), cell_round(py0), cell_round(px1), cell_round(py1), k0, w,
+                       layer, nv, nu, status);
 }
 
 // The same cell chain from integer endpoint cells already known to be inside
@@ -375,18 +382,18 @@ __device__ __forceinline__ unsigned segtab_index(unsigned plane, int x0, int y0,
 }
 
 template <typename T>
-__device__ __forceinline__ void bin_or_splat(bool has, double px0, double py0, double px1,
-                                             double py1, int k0, T w, int grp,
-                                             T *__restrict__ hist, int64_t plane, int nv, int nu,
-                                             int32_t *__restrict__ status,
-                                             const hb_tiles *__restrict__ tl) {
+__device__ __forceinline__ void bin_or_splat_cells(bool has, int cx0, int cy0, int cx1, int cy1,
+                                                   int k0, T w, int grp, T *__restrict__ hist,
+                                                   int64_t plane, int nv, int nu,
+                                                   int32_t *__restrict__ status,
+                                                   const hb_tiles *__restrict__ tl) {
     bool direct = has;
     int tile = -1;
     uint64_t rec = 0;
     if (tl && tl->mode == 1) {  // segment-key table: one atomic per segment
         if (has) {
-            const int x0 = cell_round(px0), y0 = cell_round(py0);
-            const int dx = cell_round(px1) - x0, dy = cell_round(py1) - y0;
+            const int x0 = cx0, y0 = cy0;
+            const int dx = cx1 - x0, dy = cy1 - y0;
             const int H = tl->halo, iw = (int)w;
             if (k0 == 1 && dx == 0 && dy == 0) {
                 direct = false;  // adds nothing (_kernels.py:67-71)
@@ -404,12 +411,13 @@ atomicAdd(tl->tab + segtab_index(dir, x0, y0, nv, nu), (unsigned)iw);
             }
         }
         if (direct)
-            dda_splat<T>(px0, py0, px1, py1, k0, w, hist + (int64_t)grp * plane, nv, nu, status);
+            dda_splat_cells<T>(cx0, cy0, cx1, cy1, k0, w, hist + (int64_t)grp * plane, nv, nu,
+                               status);
         return;
     }
     if (has && tl) {
-        const int x0 = cell_round(px0), y0 = cell_round(py0);
-        const int dx = cell_round(px1) - x0, dy = cell_round(py1) - y0;
+        const int x0 = cx0, y0 = cy0;
+        const int dx = cx1 - x0, dy = cy1 - y0;
         const int iw = (int)w;
         if (dx == 0 && dy == 0 && k0 == 1) {
             direct = false;  // adds nothing (_kernels.py:67-71)
@@ -436,7 +444,18 @@ atomicAdd(tl->tab + segtab_index(dir, x0, y0, nv, nu), (unsigned)iw);
             }
         }
     }
-    if (direct) dda_splat<T>(px0, py0, px1, py1, k0, w, hist + (int64_t)grp * plane, nv, nu, status);
+    if (direct)
+        dda_splat_cells<T>(cx0, cy0, cx1, cy1, k0, w, hist + (int64_t)grp * plane, nv, nu, status);
+}
+
+template <typename T>
+__device__ __forceinline__ void bin_or_splat(bool has, double px0, double py0, double px1,
+                                             double py1, int k0, T w, int grp,
+                                             T *__restrict__ hist, int64_t plane, int nv, int nu,
+                                             int32_t *__restrict__ status,
+                                             const hb_tiles *__restrict__ tl) {
+    bin_or_splat_cells<T>(has, cell_round(px0), cell_round(py0), cell_round(px1),
+                          cell_round(py1), k0, w, grp, hist, plane, nv, nu, status, tl);
 }
 
 // ---- persistent warp-per-edge kernels ---------------------------------------

@@ -222,7 +222,7 @@ emit_kernel(const double2 *__restrict__ pts, const int64_t *__restrict__ starts,
         if (e + nwarps < n_edges) { s_nx = starts[e + nwarps]; t_nx = starts[e + nwarps + 1]; }
         double2 *o = out + new_starts[e];
         const bool splat = hist != nullptr;
-        const int grp = splat ? group[e] : 0;
+        const int grp = splat && group ? group[e] : 0;
         const int32_t w = weight ? weight[e] : 1;
         // carry: last kept point so far and its output index (none yet)
         double2 a = make_double2(0.0, 0.0);
@@ -497,7 +497,7 @@ emit_flat_kernel(const double2 *__restrict__ pts, const int64_t *__restrict__ st
             const bool seg = !dry && valid && lm >= 1;
             // (clamped: after a capacity clamp, empty edges can leave stale slots)
             me = me < 0 ? 0 : (me > (int)n_edges - 1 ? (int)n_edges - 1 : me);
-            const int grp = seg ? group[me] : 0;
+            const int grp = seg && group ? group[me] : 0;
             const int32_t w = seg && weight ? weight[me] : 1;
             bin_or_splat<int32_t>(seg, q0x, q0y, q.x, q.y, lm == 1 ? 0 : 1, w, grp, hist, plane,
                                   nv, nu, status, tiles);
@@ -632,8 +632,8 @@ emit_ring_kernel(const double2 *__restrict__ pts, const int64_t *__restrict__ st
     double2 *const outw = out + O_a;
 
     int F = 0;                              // first output not yet flushed
-    double2 cq = make_double2(0.0, 0.0);    // output F - 1 (previous tile's lane 31)
-    double2 ca = cq;                        // last kept input so far ...
+    int cqx = 0, cqy = 0;                   // cell of output F - 1 (previous tile's last)
+    double2 ca = make_double2(0.0, 0.0);    // last kept input so far ...
     int cg = -1;                            // ... and its output index
 
     // store + splat outputs [F, F + cnt), cnt <= 32, all present in the ring
@@ -642,21 +642,25 @@ emit_ring_kernel(const double2 *__restrict__ pts, const int64_t *__restrict__ st
         const int o = F + lane;
         const bool valid = lane < cnt;
         const int sl = o & (kRing - 1);
-        const double2 q = valid ? R.q[sl] : cq;
+        const double2 q = valid ? R.q[sl] : make_double2(0.0, 0.0);
         const int meta = valid ? R.meta[sl] : 0;
         if (valid) HB_ST_STREAM(outw + o, q);
         if (splat) {
-            double q0x = __shfl_up_sync(full, q.x, 1), q0y = __shfl_up_sync(full, q.y, 1);
-            if (lane == 0) { q0x = cq.x; q0y = cq.y; }
+            // each output's cell is rounded once; segment m-1 -> m takes the
+            // previous lane's (or the carried) cell
+            const int cx = cell_round(q.x), cy = cell_round(q.y);
+            int px = __shfl_up_sync(full, cx, 1), py = __shfl_up_sync(full, cy, 1);
+            if (lane == 0) { px = cqx; py = cqy; }
             const int cls = meta & 3;
             const int e = meta >> 2;
             const bool seg = valid && cls >= 1;
             const int grp = seg && group ? group[e] : 0;
             const int32_t w = seg && weight ? weight[e] : 1;
-            bin_or_splat<int32_t>(seg, q0x, q0y, q.x, q.y, cls == 1 ? 0 : 1, w, grp, hist, plane,
-                                  nv, nu, status, tiles);
+            bin_or_splat_cells<int32_t>(seg, px, py, cx, cy, cls == 1 ? 0 : 1, w, grp, hist,
+                                        plane, nv, nu, status, tiles);
+            cqx = __shfl_sync(full, cx, cnt - 1);
+            cqy = __shfl_sync(full, cy, cnt - 1);
         }
-        cq = make_double2(__shfl_sync(full, q.x, cnt - 1), __shfl_sync(full, q.y, cnt - 1));
         F += cnt;
         __syncwarp();
     };
@@ -913,7 +917,7 @@ int hb_resample_emit_cap(const double *pts, const int64_t *starts, int64_t n_edg
     if (n_edges < 0 || n_pts < 0 || out_capacity < 0 ||
         (n_edges > 0 && (!pts || !starts || !pos || !new_starts || !out)) ||
         ((counts || out_capacity < INT64_MAX) && !status) ||
-        (counts && (!group || nv < 1 || nu < 1 || nv > kMaxDim || nu > kMaxDim)))
+        (counts && (nv < 1 || nu < 1 || nv > kMaxDim || nu > kMaxDim)))
         return set_error(HB_EINVAL, "hb_resample_emit: bad arguments");
     if (n_edges == 0 || n_pts == 0) return HB_OK;
 #if defined(HB_EMIT_PER_EDGE)

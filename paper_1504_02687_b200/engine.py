@@ -326,6 +326,11 @@ class BundleEngine:
         b.record()
         self.trace.setdefault(name, []).append((a, b, self.iteration))
 
+    def _emit_groups(self):
+        """Group ids for the emit's splat; NULL (= all group 0) for one group,
+        which saves a gather per output."""
+        return None if self.nbins == 1 else ptr(self.groups)
+
     def _splat(self, s) -> None:
         """Straight splat of the current points (iteration 0 / float weights);
         with tiles it also takes the per-tile census for the next plan."""
@@ -408,7 +413,7 @@ class BundleEngine:
                 tiles = ctypes.byref(self.tiles)
                 self._tab_segments = n_new - E
             self._k("hb_resample_emit", ptr(self.pts), ptr(self.starts), E, self.n_pts,
-                    ptr(self.pos), ptr(self.starts_alt), ptr(self.alt), ptr(self.groups),
+                    ptr(self.pos), ptr(self.starts_alt), ptr(self.alt), self._emit_groups(),
                     ptr(self.wint), ptr(self.hist) if fused else None, nv, nu,
                     ptr(self.status), tiles, s)
             if self.tile_mode == 0 and tiles is not None:
@@ -428,7 +433,7 @@ class BundleEngine:
         E, nv, nu = self.n_edges, self.nv, self.nu
         tiles = ctypes.byref(self.tiles) if self.tile_mode == 1 else None
         self._k("hb_resample_emit_cap", ptr(self.pts), ptr(self.starts), E, self.n_pts,
-                ptr(self.pos), ptr(self.starts_alt), ptr(self.alt), self.cap, ptr(self.groups),
+                ptr(self.pos), ptr(self.starts_alt), ptr(self.alt), self.cap, self._emit_groups(),
                 ptr(self.wint), ptr(self.hist), nv, nu, ptr(self.status), tiles, s)
         # N_i on the device; starts clamped into the buffers if it did not fit
         self._k("hb_clamp_starts", ptr(self.starts_alt), E, self.cap,

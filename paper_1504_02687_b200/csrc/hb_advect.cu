@@ -121,8 +121,10 @@ polyline_pass_kernel(const PolylinePass p) {
         const int64_t lbase = do_adv ? (int64_t)p.edge_layer[e] * p.plane : 0;
         const float *rho = do_adv ? p.rho + lbase : nullptr;
         constexpr bool quad = ADV && QUAD;
-        QuadField qf{nullptr, 0u};
-        if (quad) qf = QuadField{p.gf, (unsigned)lbase};
+        QuadField qf{nullptr, 0u, nullptr};
+        if (quad)
+            qf = QuadField{p.gf, (unsigned)lbase,
+                           quad_gy(p.gf, (uint64_t)p.nbins_field * (uint64_t)p.plane)};
 
         double2 cur = make_double2(0.0, 0.0);   // A(chunk c), lane = local index - c0
         double2 left = make_double2(0.0, 0.0);  // A(c0 - 1)

@@ -203,7 +203,8 @@ __global__ void __launch_bounds__(kStreamBlock, HB_FLAT_MINB) advect_flat_kernel
                 // _kernels.py:163-175 (G = 2*gradient, see gradient2_value_ref)
                 double Gx, Gy;
                 if (QUAD) {
-                    gradient2_value_quad(QuadField{p.gf, base}, p.nv, p.nu, x, y, Gx, Gy, r0);
+                    gradient2_value_quad(QuadField{p.gf, base, quad_gy(p.gf, (uint64_t)p.nbins * p.plane)},
+                                         p.nv, p.nu, x, y, Gx, Gy, r0);
                 } else {
                     gradient2_value_ref(p.rho + base, p.nv, p.nu, x, y, Gx, Gy, r0);
                 }

@@ -185,7 +185,19 @@ __device__ __forceinline__ void gradient2_value_ref(const float *__restrict__ rh
 struct QuadField {
     const float4 *q;
     unsigned base;
+    const float4 *gy;  // split layout: the GY region (quad_gy)
 };
+
+// HB_QUAD_SPLIT=1 stores the field as two regions of the same buffer: {Q, GX}
+// per cell (32 bytes, one 256-bit load for a gradient sample's first half,
+// and the candidates' Q quads 32 bytes apart), then GY per cell (16 bytes).
+// Same 48 bytes per cell as the interleaved {Q, GX, GY} record.
+#ifndef HB_QUAD_SPLIT
+#define HB_QUAD_SPLIT 0  // measured: advect 5.26 -> 5.32 ms (config 4), 33.4 -> 41.1 ms (config 5)
+#endif
+__host__ __device__ __forceinline__ const float4 *quad_gy(const float4 *gf, uint64_t total_cells) {
+    return (HB_QUAD_SPLIT && gf) ? gf + 2 * total_cells : nullptr;
+}
 
 // float4s per quad record: {Q, GX, GY} (48 bytes).  4 pads the record to 64
 // bytes (never straddles a 128-byte line; Q+GX is one 256-bit load) -- measured
@@ -210,15 +222,21 @@ __device__ __forceinline__ void gradient2_value_quad(const QuadField &f, int nv,
     const int v0 = clampi(floor_i(y), 0, nv - 2);
     const double fx = dsub(x, (double)u0);
     const double fy = dsub(y, (double)v0);
-    const float4 *rec = f.q + kQuadRec * (f.base + (unsigned)(v0 * nu + u0));
-    float4 q, dx;
-    if (kQuadRec == 4) {
-        ldg_2x4(rec, q, dx);
+    const unsigned cell = f.base + (unsigned)(v0 * nu + u0);
+    float4 q, dx, dy;
+    if (HB_QUAD_SPLIT) {
+        ldg_2x4(f.q + 2 * cell, q, dx);
+        dy = __ldg(f.gy + cell);
     } else {
-        q = __ldg(rec);
-        dx = __ldg(rec + 1);
+        const float4 *rec = f.q + kQuadRec * cell;
+        if (kQuadRec == 4) {
+            ldg_2x4(rec, q, dx);
+        } else {
+            q = __ldg(rec);
+            dx = __ldg(rec + 1);
+        }
+        dy = __ldg(rec + 2);
     }
-    const float4 dy = __ldg(rec + 2);
     // corners: .x (u0,v0)  .y (u0+1,v0)  .z (u0,v0+1)  .w (u0+1,v0+1)
     const double ax = dadd((double)dx.x, dmul(fx, dsub((double)dx.y, (double)dx.x)));
     const double bx = dadd((double)dx.z, dmul(fx, dsub((double)dx.w, (double)dx.z)));
@@ -240,7 +258,7 @@ __device__ __forceinline__ double bilinear_quad(const float4 *__restrict__ q, un
     const int v0 = inner ? floor_i(y) : clampi(floor_i(y), 0, nv - 2);
     const double fx = dsub(x, (double)u0);
     const double fy = dsub(y, (double)v0);
-    const float4 c = __ldg(q + kQuadRec * (base + (unsigned)(v0 * nu + u0)));
+    const float4 c = __ldg(q + (HB_QUAD_SPLIT ? 2u : kQuadRec) * (base + (unsigned)(v0 * nu + u0)));
     const double a = lerp_f32diff(c.x, c.y, fx);
     const double b = lerp_f32diff(c.z, c.w, fx);
     return dadd(a, dmul(fy, dsub(b, a)));

@@ -409,9 +409,12 @@ __global__ void grad_field_kernel(const float *__restrict__ rho, int nv, int nu,
     if (u >= nu) return;
     const int64_t plane = (int64_t)nv * nu;
     const float *r = rho + l * plane;
-    float4 *rec = out + kQuadRec * (l * plane + (int64_t)v * nu + u);  // {Q, GX, GY} of the cell
+    const int64_t cell = l * plane + (int64_t)v * nu + u;
+    // {Q, GX, GY} of the cell: interleaved, or {Q, GX} + GY in two regions
+    float4 *rec = out + (HB_QUAD_SPLIT ? 2 : (int)kQuadRec) * cell;
+    float4 *gyp = HB_QUAD_SPLIT ? out + 2 * (int64_t)gridDim.z * plane + cell : rec + 2;
     if (u > nu - 2 || v > nv - 2) {
-        rec[0] = rec[1] = rec[2] = make_float4(0.f, 0.f, 0.f, 0.f);
+        rec[0] = rec[1] = *gyp = make_float4(0.f, 0.f, 0.f, 0.f);
         return;
     }
     const float *c = r + (int64_t)v * nu + u;
@@ -422,7 +425,7 @@ __global__ void grad_field_kernel(const float *__restrict__ rho, int nv, int nu,
     cell_diff(r, nv, nu, u, v + 1, x01, y01);
     cell_diff(r, nv, nu, u + 1, v + 1, x11, y11);
     rec[1] = make_float4(x00, x10, x01, x11);
-    rec[2] = make_float4(y00, y10, y01, y11);
+    *gyp = make_float4(y00, y10, y01, y11);
 }
 
 // used_cell_count (bundler.py:292-305): rho > float32(rel * peak_l) when

@@ -205,7 +205,8 @@ __device__ __forceinline__ void advect_group(const LapCount &p, double2 (*row_pt
             const double x = pt.x, y = pt.y;
             double Gx, Gy;  // _kernels.py:163-175 (G = 2*gradient)
             if (ADV == 1)
-                gradient2_value_quad(QuadField{p.gf, lb}, p.nv, p.nu, x, y, Gx, Gy, r0);
+                gradient2_value_quad(QuadField{p.gf, lb, quad_gy(p.gf, (uint64_t)p.nbins * p.plane)},
+                                     p.nv, p.nu, x, y, Gx, Gy, r0);
             else
                 gradient2_value_ref(p.rho + lb, p.nv, p.nu, x, y, Gx, Gy, r0);
             const double Gn = hypot_ref(Gx, Gy);

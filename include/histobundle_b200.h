@@ -358,6 +358,17 @@ HB_API int hb_kmeans_scatter(const double *features, int64_t n, int d, int k,
                              const double *centroids, const int8_t *assign, double *scatter,
                              int64_t *counts, void *stream);
 
+/* ---- rendering (render.py:158-179) ----
+ * Stroke width of every segment of every polyline (segments of edge e are
+ * outputs starts[e]-e .. starts[e+1]-e-2): the mean of the layer's clamped
+ * bilinear density at the segment's two ends over the layer peak, clipped to
+ * [0, 1], mapped to w_min + (w_max - w_min) * ratio (want_ratio: the ratio
+ * itself).  pts in grid coordinates; layer may be NULL (all layer 0). */
+HB_API int hb_segment_widths(const double *pts, const int64_t *starts, int64_t n_edges,
+                             const int32_t *layer, const float *rho, int nbins, int nv, int nu,
+                             const float *peaks, double w_min, double w_max, int want_ratio,
+                             double *out, void *stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -18,7 +18,7 @@ LIB_DIR = os.path.join(_PKG, "_lib")
 LIB_PATH = os.path.join(LIB_DIR, "libhb_b200.so")
 INCLUDE = os.path.join(os.path.dirname(_PKG), "include")
 
-SOURCES = ["hb_api.cu", "hb_polyline.cu", "hb_field.cu", "hb_advect.cu", "hb_advect_flat.cu", "hb_lapcount.cu", "hb_splat.cu", "hb_binning.cu"]
+SOURCES = ["hb_api.cu", "hb_polyline.cu", "hb_field.cu", "hb_advect.cu", "hb_advect_flat.cu", "hb_lapcount.cu", "hb_splat.cu", "hb_binning.cu", "hb_render.cu"]
 
 NVCC_FLAGS = [
     "-gencode", "arch=compute_100a,code=sm_100a",
@@ -81,6 +81,7 @@ SIGNATURES = {
     "hb_abi_version": (_I, []),
     "hb_last_error": (ctypes.c_char_p, []),
     "hb_device_sm_count": (_I, []),
+    "hb_segment_widths": (_I, [_P, _P, _I64, _P, _P, _I, _I, _I, _P, _D, _D, _I, _P, _P]),
     "hb_advect_laplacian_count": (_I, [_P, _P, _I64, _I64, _P, _P, _P, _I, _I, _I, _D, _D, _D,
                                        _I, _D, _I, _D, _P, _P, _P, _P, _P]),
     "hb_kmeans_assign": (_I, [_P, _I64, _I, _I, _P, _P, _I, _P, _P, _P]),

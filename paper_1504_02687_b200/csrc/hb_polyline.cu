@@ -665,46 +665,52 @@ emit_ring_kernel(const double2 *__restrict__ pts, const int64_t *__restrict__ st
         __syncwarp();
     };
 
+    // Inside the range everything is 32-bit and relative: inputs j - J_a,
+    // edges e - e0, outputs G - O_a (point counts are below 2^31, checked on
+    // the host by every pass that produces them).
+    const double2 *pts_r = pts + J_a;
+    const int32_t *pos_r = pos + J_a;
+    const int64_t *st_r = starts + e0;
+    const int64_t *ns_r = new_starts + e0;
+    const int JN = (int)(J_b - J_a), EN = (int)(e1 - e0);
     // chunk [jn, jn + 32) of the range, jn's edge en -> R.c* (one cp.async group)
-    auto prefetch = [&](int64_t jn, int64_t en) {
-        const int64_t j = jn + lane;
-        const bool in = j < J_b;
-        emit_cp(&R.cpts[lane], in ? pts + j : pts, 16, in);
-        emit_cp(&R.cpos[lane], in ? pos + j : pos, 4, in);
-        const int64_t ek = en + 1 + lane;
-        const bool ev = ek <= e1;
-        emit_cp(&R.csv[lane], ev ? starts + ek : starts, 8, ev);
-        emit_cp(&R.cnsv[lane], ev ? new_starts + ek : new_starts, 8, ev);
+    auto prefetch = [&](int jn, int en) {
+        const int j = jn + lane;
+        const bool in = j < JN;
+        emit_cp(&R.cpts[lane], pts_r + (in ? j : 0), 16, in);
+        emit_cp(&R.cpos[lane], pos_r + (in ? j : 0), 4, in);
+        const int ek = en + 1 + lane;
+        const bool ev = ek <= EN;
+        emit_cp(&R.csv[lane], st_r + (ev ? ek : 0), 8, ev);
+        emit_cp(&R.cnsv[lane], ns_r + (ev ? ek : 0), 8, ev);
         asm volatile("cp.async.commit_group;\n" ::: "memory");
     };
-    int64_t e_c = e0;                   // edge of input jc
-    int64_t ns_c = new_starts[e0];      // its new_starts
-    prefetch(J_a, e0);
-    for (int64_t jc = J_a; jc < J_b; jc += 32) {
+    int e_c = 0;   // edge of input jc
+    int ns_c = 0;  // its new_starts (relative to O_a = new_starts[e0])
+    prefetch(0, 0);
+    for (int jc = 0; jc < JN; jc += 32) {
         asm volatile("cp.async.wait_group 0;\n" ::: "memory");
         __syncwarp();
-        const int64_t j = jc + lane;
-        const bool in = j < J_b;
+        const bool in = jc + lane < JN;
         const double2 x = R.cpts[lane];
         const int pj = in ? R.cpos[lane] : -1;
         // edges starting in (jc, jc + 31] (every edge has >= 1 input)
-        const int64_t ek = e_c + 1 + lane;
-        const int64_t sv = ek <= e1 ? (int64_t)R.csv[lane] : INT64_MAX;
-        const int64_t rel = sv - jc;  // >= 1
+        const int ek = e_c + 1 + lane;
+        const int rel = ek <= EN ? (int)(R.csv[lane] - J_a) - jc : INT_MAX;  // >= 1
         const unsigned smask = __reduce_or_sync(full, rel <= 31 ? (1u << rel) : 0u);
         int d = __popc(smask & (0xffffffffu >> (31 - lane)));  // e - e_c
-        if (e_c + d > e1 - 1) d = (int)(e1 - 1 - e_c);
-        const int64_t e = e_c + d;
-        const int64_t nsb = d > 0 ? (int64_t)R.cnsv[d - 1] : ns_c;
+        if (e_c + d > EN - 1) d = EN - 1 - e_c;
+        const int e = e_c + d;
+        const int nsb = d > 0 ? (int)(R.cnsv[d - 1] - O_a) : ns_c;
         const int nst = __popc(__ballot_sync(full, rel <= 32));
-        if (nst) ns_c = R.cnsv[nst - 1];
+        if (nst) ns_c = (int)(R.cnsv[nst - 1] - O_a);
         __syncwarp();  // R.c* is refilled below
         e_c += nst;
-        if (jc + 32 < J_b) prefetch(jc + 32, e_c);
+        if (jc + 32 < JN) prefetch(jc + 32, e_c);
         const bool kept = pj >= 0;
         int g = -1;
         if (kept) {
-            g = (int)(nsb + pj - O_a);
+            g = nsb + pj;
             if ((unsigned)g >= (unsigned)O_n) g = -1;  // (inconsistent inputs: write nothing)
         }
         const unsigned kb = __ballot_sync(full, g >= 0);
@@ -724,7 +730,7 @@ emit_ring_kernel(const double2 *__restrict__ pts, const int64_t *__restrict__ st
         int nx = own ? (pj == 0 ? g : ga + 1) : 1;
         const int last = own ? g : 0;
         const int pieces = g - ga;
-        const int meta_hi = (int)e << 2;
+        const int meta_hi = (int)(e0 + e) << 2;
         const int c_end = cg + 1;  // every output below is owned by a kept input seen so far
         for (;;) {
             const int limit = F + kRing;

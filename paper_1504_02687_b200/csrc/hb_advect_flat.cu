@@ -59,7 +59,7 @@ constexpr int kFlatWarps = kStreamBlock / 32;
 
 struct FlatQueue {  // per warp, structure of arrays
     double x[kQCap], y[kQCap], dx[kQCap], dy[kQCap], r0[kQCap], m[kQCap];
-    long long i[kQCap];
+    int i[kQCap];  // point index relative to the launch's first point
     unsigned base[kQCap];
 };
 
@@ -113,9 +113,13 @@ __global__ void __launch_bounds__(kStreamBlock, HB_FLAT_MINB) advect_flat_kernel
     double my_disp = 0.0;
     int qn = 0;  // warp-uniform queue fill
 
-    auto accept = [&](int64_t i, double x, double y, double nx, double ny) {
+    // indices below are 32-bit and relative to P_lo (point counts < 2^31,
+    // checked on the host)
+    double2 *const pts_r = p.pts + P_lo;
+    const int NPr = (int)(NP - P_lo);
+    auto accept = [&](int i, double x, double y, double nx, double ny) {
         if (nx != x || ny != y) {  // _kernels.py:187-190
-            p.pts[i] = make_double2(nx, ny);
+            pts_r[i] = make_double2(nx, ny);
             ++my_moved;
             my_disp = dadd(my_disp, hypot_ref(dsub(nx, x), dsub(ny, y)));
         }
@@ -126,7 +130,7 @@ __global__ void __launch_bounds__(kStreamBlock, HB_FLAT_MINB) advect_flat_kernel
         const bool have = lane < take;
         const int slot = qn - take + lane;
         double x = 0.0, y = 0.0, dx = 0.0, dy = 0.0, r0 = 0.0, m = -1.0;
-        int64_t i = 0;
+        int i = 0;
         unsigned base = 0;
         if (have) {
             x = q.x[slot]; y = q.y[slot]; dx = q.dx[slot]; dy = q.dy[slot];
@@ -156,7 +160,7 @@ __global__ void __launch_bounds__(kStreamBlock, HB_FLAT_MINB) advect_flat_kernel
 
     if (t < t_end) {
         // edge cursor: the edge containing point 32*t (last e: starts[e] <= i0)
-        int64_t e_cur = 0;
+        int e_cur = 0;
         if (lane == 0) {
             const int64_t i0 = P_lo + t * 32;
             int64_t lo = 0, hi = p.n_edges - 1;
@@ -164,30 +168,31 @@ __global__ void __launch_bounds__(kStreamBlock, HB_FLAT_MINB) advect_flat_kernel
                 const int64_t mid = (lo + hi + 1) >> 1;
                 if (p.starts[mid] <= i0) lo = mid; else hi = mid - 1;
             }
-            e_cur = lo;
+            e_cur = (int)lo;
         }
         e_cur = __shfl_sync(full, e_cur, 0);
-        int64_t s_cur = p.starts[e_cur];
+        const int n_edges = (int)p.n_edges;
+        int s_cur = (int)(p.starts[e_cur] - P_lo);
         // one tile of loads in flight ahead of the math
-        int64_t i = P_lo + t * 32 + lane;
-        double2 pt_nx = i < NP ? p.pts[i] : make_double2(0.0, 0.0);
+        int i = (int)t * 32 + lane;
+        double2 pt_nx = i < NPr ? pts_r[i] : make_double2(0.0, 0.0);
         for (; t < t_end; ++t) {
-            const int64_t i0 = P_lo + t * 32;
+            const int i0 = (int)t * 32;
             i = i0 + lane;
-            const bool valid = i < NP;
+            const bool valid = i < NPr;
             const double2 pt = pt_nx;
-            if (t + 1 < t_end && i + 32 < NP) pt_nx = p.pts[i + 32];
+            if (t + 1 < t_end && i + 32 < NPr) pt_nx = pts_r[i + 32];
             // edge starts strictly after i0, up to i0 + 32
-            const int64_t ek = e_cur + 1 + lane;
-            const int64_t sv = ek <= p.n_edges ? p.starts[ek] : INT64_MAX;
-            const int64_t rel = sv - i0;  // >= 1
+            const int ek = e_cur + 1 + lane;
+            const int sv = ek <= n_edges ? (int)(p.starts[ek] - P_lo) : INT_MAX;
+            const int rel = sv - i0;  // >= 1
             const unsigned in_win = __ballot_sync(full, rel <= 32);
             const unsigned smask = __reduce_or_sync(full, rel <= 31 ? (1u << rel) : 0u);
             const unsigned end31 = (in_win & ~__ballot_sync(full, rel <= 31)) ? 0x80000000u : 0u;
             const unsigned emask = smask | (smask >> 1) | (s_cur == i0 ? 1u : 0u) | end31;
             unsigned base = 0;
             if (p.nbins > 1 && valid) {
-                const int64_t e = e_cur + __popc(smask & (0xffffffffu >> (31 - lane)));
+                const int e = e_cur + __popc(smask & (0xffffffffu >> (31 - lane)));
                 base = (unsigned)p.edge_layer[e] * p.plane;
             }
             const int nst = __popc(in_win);

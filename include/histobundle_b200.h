@@ -346,6 +346,14 @@ HB_API int hb_kmeans_reseed(const double *features, int64_t n, int d, int k,
                             double *centroids, const int32_t *rs, int n_rs,
                             const int8_t *assign, void *workspace, size_t workspace_bytes,
                             void *stream);
+/* `iterations` Lloyd steps of every restart with the bookkeeping on the
+ * device (no host round trip per step): flags = [live | changed | empty],
+ * 3 * restarts int32, live = 1 and the rest 0 to start; a restart whose
+ * assignment stopped changing drops out (binning.py:110-121).  The
+ * workspace holds restarts * n float64 (hb_kmeans_reseed_workspace_bytes). */
+HB_API int hb_kmeans_lloyd(const double *features, int64_t n, int d, int k, double *centroids,
+                           int restarts, int8_t *assign, int32_t *flags, int iterations,
+                           void *workspace, size_t workspace_bytes, void *stream);
 /* Per-restart inertia partials (restarts x hb_kmeans_inertia_blocks()),
  * summed by the caller in order: picks the best restart (binning.py:124-130). */
 HB_API int hb_kmeans_inertia_blocks(void);

@@ -88,6 +88,7 @@ SIGNATURES = {
     "hb_kmeans_update": (_I, [_P, _I64, _I, _I, _P, _P, _I, _P, _P, _P]),
     "hb_kmeans_reseed_workspace_bytes": (_SZ, [_I64, _I]),
     "hb_kmeans_reseed": (_I, [_P, _I64, _I, _I, _P, _P, _I, _P, _P, _SZ, _P]),
+    "hb_kmeans_lloyd": (_I, [_P, _I64, _I, _I, _P, _I, _P, _P, _I, _P, _SZ, _P]),
     "hb_kmeans_inertia_blocks": (_I, []),
     "hb_kmeans_inertia": (_I, [_P, _I64, _I, _I, _P, _I, _P, _P, _P]),
     "hb_kmeans_scatter": (_I, [_P, _I64, _I, _I, _P, _P, _P, _P, _P]),

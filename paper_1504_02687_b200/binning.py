@@ -37,6 +37,7 @@ __all__ = ["CRITERIA", "Clustering", "edge_features", "bin_by_orientation", "kme
 CRITERIA = ("none", "orientation", "origin", "destination", "od", "length", "file")
 
 _MAX_LLOYD_ITER = 100  # binning.py:31
+_CHECK_EVERY = 8       # Lloyd steps per host check for live restarts
 
 
 @dataclass
@@ -123,33 +124,20 @@ def _kmeans_device(df: _DeviceFeatures, k: int, restarts: int,
     dev = df.t.device
     cent = torch.from_numpy(np.ascontiguousarray(unique_rows[picks])).to(dev)  # (R, k, d)
     assign = torch.full((restarts, n), -1, dtype=torch.int8, device=dev)
-    flags = torch.zeros(2 * restarts, dtype=torch.int32, device=dev)  # changed | empty
-    changed, empty = flags[:restarts], flags[restarts:]
-    active = np.ones(restarts, dtype=bool)
+    # restart bookkeeping on the device (hb_kmeans_lloyd): [live | changed | empty]
+    flags = torch.zeros(3 * restarts, dtype=torch.int32, device=dev)
+    flags[:restarts] = 1
+    wsb = int(N.lib().hb_kmeans_reseed_workspace_bytes(n, restarts))
+    ws = torch.empty(max(wsb, 8), dtype=torch.uint8, device=dev)
     s = stream_ptr()
-    for _ in range(_MAX_LLOYD_ITER):
-        idx = np.flatnonzero(active).astype(np.int32)
-        if idx.size == 0:
+    done = 0
+    while done < _MAX_LLOYD_ITER:  # one host check per _CHECK_EVERY iterations
+        step = min(_CHECK_EVERY, _MAX_LLOYD_ITER - done)
+        N.call("hb_kmeans_lloyd", ptr(df.t), n, d, k, ptr(cent), restarts, ptr(assign),
+               ptr(flags), step, ptr(ws), ws.numel(), s)
+        done += step
+        if not bool(flags[:restarts].any()):
             break
-        flags.zero_()
-        idx_t = torch.from_numpy(idx).to(dev)
-        N.call("hb_kmeans_assign", ptr(df.t), n, d, k, ptr(cent), ptr(idx_t), int(idx.size),
-               ptr(assign), ptr(changed), s)
-        ch = changed.cpu().numpy()[idx] != 0
-        active[idx] = ch
-        upd = idx[ch]
-        if upd.size == 0:
-            continue
-        upd_t = torch.from_numpy(upd).to(dev)
-        N.call("hb_kmeans_update", ptr(df.t), n, d, k, ptr(cent), ptr(upd_t), int(upd.size),
-               ptr(assign), ptr(empty), s)
-        rs = upd[empty.cpu().numpy()[upd] != 0]
-        if rs.size:
-            rs_t = torch.from_numpy(rs).to(dev)
-            wsb = int(N.lib().hb_kmeans_reseed_workspace_bytes(n, int(rs.size)))
-            ws = torch.empty(max(wsb, 8), dtype=torch.uint8, device=dev)
-            N.call("hb_kmeans_reseed", ptr(df.t), n, d, k, ptr(cent), ptr(rs_t), int(rs.size),
-                   ptr(assign), ptr(ws), ws.numel(), s)
     nb = int(N.lib().hb_kmeans_inertia_blocks())
     part = torch.empty((restarts, nb), dtype=torch.float64, device=dev)
     N.call("hb_kmeans_inertia", ptr(df.t), n, d, k, ptr(cent), restarts, ptr(assign),

@@ -53,9 +53,11 @@ __device__ __forceinline__ double km_norm(const double *f, const double *c, int 
 __global__ void __launch_bounds__(256)
 km_assign_kernel(const double *__restrict__ f, int64_t n, int d, int k,
                  const double *__restrict__ cent, const int32_t *__restrict__ active,
-                 int8_t *__restrict__ assign, int32_t *__restrict__ changed) {
+                 int8_t *__restrict__ assign, int32_t *__restrict__ changed,
+                 const int32_t *__restrict__ live) {
     __shared__ double s_c[kKmMaxK * kKmMaxD];
-    const int r = active[blockIdx.y];
+    const int r = active ? active[blockIdx.y] : (int)blockIdx.y;
+    if (live && !live[r]) return;  // (device-driven loop: converged restart)
     for (int t = threadIdx.x; t < k * d; t += blockDim.x) s_c[t] = cent[(int64_t)r * k * d + t];
     __syncthreads();
     const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
@@ -89,7 +91,8 @@ constexpr int kUpdWin = kUpdTile / 32;
 __global__ void __launch_bounds__(kUpdBlock)
 km_update_kernel(const double *__restrict__ f, int64_t n, int d, int k,
                  double *__restrict__ cent, const int32_t *__restrict__ upd,
-                 const int8_t *__restrict__ assign, int32_t *__restrict__ empty) {
+                 const int8_t *__restrict__ assign, int32_t *__restrict__ empty,
+                 const int32_t *__restrict__ live, const int32_t *__restrict__ changed) {
     __shared__ int8_t s_a[kUpdTile];
     __shared__ short s_list[kUpdTile];
     __shared__ double s_f[kUpdTile * kKmMaxD];
@@ -97,7 +100,8 @@ km_update_kernel(const double *__restrict__ f, int64_t n, int d, int k,
     __shared__ int s_base[kKmMaxK + 1];
     const unsigned full = 0xffffffffu;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    const int r = upd[blockIdx.x];
+    const int r = upd ? upd[blockIdx.x] : (int)blockIdx.x;
+    if (live && !(live[r] && changed[r])) return;
     const int8_t *a = assign + (int64_t)r * n;
     // thread t < k*d owns the chain of cluster t / d, column t % d
     const int my_c = threadIdx.x / d, my_j = threadIdx.x % d;
@@ -180,12 +184,14 @@ constexpr int kReseedBlock = 1024;
 __global__ void __launch_bounds__(kReseedBlock)
 km_reseed_kernel(const double *__restrict__ f, int64_t n, int d, int k, double *__restrict__ cent,
                  const int32_t *__restrict__ rs, const int8_t *__restrict__ assign,
-                 double *__restrict__ dist) {
+                 double *__restrict__ dist, const int32_t *__restrict__ live,
+                 const int32_t *__restrict__ changed, const int32_t *__restrict__ empty) {
     __shared__ int s_cnt[kKmMaxK];
     __shared__ double s_c[kKmMaxK * kKmMaxD];
     __shared__ double s_bv[kReseedBlock / 32];
     __shared__ long long s_bi[kReseedBlock / 32];
-    const int r = rs[blockIdx.x];
+    const int r = rs ? rs[blockIdx.x] : (int)blockIdx.x;
+    if (live && !(live[r] && changed[r] && empty[r])) return;
     double *dr = dist + (int64_t)blockIdx.x * n;
     const int8_t *a = assign + (int64_t)r * n;
     for (int t = threadIdx.x; t < k; t += blockDim.x) s_cnt[t] = 0;
@@ -226,6 +232,18 @@ km_reseed_kernel(const double *__restrict__ f, int64_t n, int d, int k, double *
             dr[bi] = -__longlong_as_double(0x7ff0000000000000LL);
         }
         __syncthreads();
+    }
+}
+
+// end of a device-driven iteration: a restart stays live only if its
+// assignment changed (binning.py:117-118); the per-iteration flags reset
+__global__ void km_step_end_kernel(int restarts, int32_t *__restrict__ live,
+                                   int32_t *__restrict__ changed, int32_t *__restrict__ empty) {
+    const int r = blockIdx.x * blockDim.x + threadIdx.x;
+    if (r < restarts) {
+        live[r] = live[r] && changed[r];
+        changed[r] = 0;
+        empty[r] = 0;
     }
 }
 
@@ -309,7 +327,7 @@ int hb_kmeans_assign(const double *features, int64_t n, int d, int k, const doub
     if (n_active == 0) return HB_OK;
     dim3 g((unsigned)((n + 255) / 256), (unsigned)n_active);
     km_assign_kernel<<<g, 256, 0, km_stream(stream)>>>(features, n, d, k, cent, active, assign,
-                                                      changed);
+                                                      changed, nullptr);
     return check_launch("hb_kmeans_assign");
 }
 
@@ -321,7 +339,7 @@ int hb_kmeans_update(const double *features, int64_t n, int d, int k, double *ce
         return set_error(HB_EINVAL, "hb_kmeans_update: bad arguments");
     if (n_upd == 0) return HB_OK;
     km_update_kernel<<<n_upd, kUpdBlock, 0, km_stream(stream)>>>(features, n, d, k, cent, upd,
-                                                               assign, empty);
+                                                               assign, empty, nullptr, nullptr);
     return check_launch("hb_kmeans_update");
 }
 
@@ -339,8 +357,37 @@ int hb_kmeans_reseed(const double *features, int64_t n, int d, int k, double *ce
     if (workspace_bytes < hb_kmeans_reseed_workspace_bytes(n, n_rs))
         return set_error(HB_EINVAL, "hb_kmeans_reseed: workspace too small");
     km_reseed_kernel<<<n_rs, kReseedBlock, 0, km_stream(stream)>>>(
-        features, n, d, k, cent, rs, assign, reinterpret_cast<double *>(workspace));
+        features, n, d, k, cent, rs, assign, reinterpret_cast<double *>(workspace), nullptr,
+        nullptr, nullptr);
     return check_launch("hb_kmeans_reseed");
+}
+
+// `iterations` Lloyd steps of every restart with the restart bookkeeping on
+// the device: flags = [live (restarts) | changed | empty] int32, live = 1 to
+// start; a restart whose assignment stopped changing stays out.  The
+// workspace holds restarts * n float64 re-seed distances.
+int hb_kmeans_lloyd(const double *features, int64_t n, int d, int k, double *cent, int restarts,
+                    int8_t *assign, int32_t *flags, int iterations, void *workspace,
+                    size_t workspace_bytes, void *stream) {
+    if (!km_shape_ok(n, d, k) || restarts < 1 || restarts > 65535 || iterations < 0 ||
+        !features || !cent || !assign || !flags || !workspace)
+        return set_error(HB_EINVAL, "hb_kmeans_lloyd: bad arguments");
+    if (workspace_bytes < hb_kmeans_reseed_workspace_bytes(n, restarts))
+        return set_error(HB_EINVAL, "hb_kmeans_lloyd: workspace too small");
+    cudaStream_t st = km_stream(stream);
+    int32_t *live = flags, *changed = flags + restarts, *empty = flags + 2 * restarts;
+    dim3 g((unsigned)((n + 255) / 256), (unsigned)restarts);
+    for (int it = 0; it < iterations; ++it) {
+        km_assign_kernel<<<g, 256, 0, st>>>(features, n, d, k, cent, nullptr, assign, changed,
+                                            live);
+        km_update_kernel<<<restarts, kUpdBlock, 0, st>>>(features, n, d, k, cent, nullptr, assign,
+                                                         empty, live, changed);
+        km_reseed_kernel<<<restarts, kReseedBlock, 0, st>>>(
+            features, n, d, k, cent, nullptr, assign, reinterpret_cast<double *>(workspace), live,
+            changed, empty);
+        km_step_end_kernel<<<(restarts + 255) / 256, 256, 0, st>>>(restarts, live, changed, empty);
+    }
+    return check_launch("hb_kmeans_lloyd", 4 * iterations);
 }
 
 int hb_kmeans_inertia_blocks(void) { return 64; }

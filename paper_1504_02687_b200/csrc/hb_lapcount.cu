@@ -86,6 +86,10 @@ constexpr int kGroup = 32 * kRun;     // points per warp per group
 constexpr int kRowPad = kRun + 1;     // odd row stride: column walks are conflict-free
 static_assert(kRun >= 2 && kRun <= 32, "run length");
 
+#ifndef HB_LC_CPASYNC
+#define HB_LC_CPASYNC 1
+#endif
+
 #ifndef HB_LC_MINB
 #define HB_LC_MINB 4
 #endif
@@ -308,7 +312,17 @@ __global__ void __launch_bounds__(kLCBlock, ADV ? 3 : HB_LC_MINB) lapcount_kerne
         const int n = (int)(P1 - base < kGroup ? P1 - base : kGroup);
         const double2 *pin = p.pin + base;
         // ---- stage the group coalesced: point i -> row i / kRun, column i % kRun
+#if HB_LC_CPASYNC
+        // global -> shared without a register round trip: all of the group's
+        // loads are in flight at once (the starts scan below overlaps them)
+        for (int i = lane; i < n; i += 32) {
+            const unsigned sa = (unsigned)__cvta_generic_to_shared(&row_pt[i / kRun][i % kRun]);
+            asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(sa), "l"(pin + i));
+        }
+        asm volatile("cp.async.commit_group;\n" ::: "memory");
+#else
         for (int i = lane; i < n; i += 32) row_pt[i / kRun][i % kRun] = pin[i];
+#endif
         double2 next_first = make_double2(0.0, 0.0);  // original point base + kGroup
         if (lane == 31 && base + kGroup < P1) next_first = pin[kGroup];
 
@@ -358,6 +372,9 @@ __global__ void __launch_bounds__(kLCBlock, ADV ? 3 : HB_LC_MINB) lapcount_kerne
         int64_t e_cur = e_g + excl + ((lane > 0 && (mask & 1u)) ? 1 : 0);
         const int64_t e_first = e_cur;
         const unsigned prev_mask = __shfl_up_sync(full, mask, 1);
+#if HB_LC_CPASYNC
+        asm volatile("cp.async.wait_group 0;\n" ::: "memory");
+#endif
         __syncwarp();
         if (ADV) {
             // _kernels.advect (in place) on points base+1 .. base+kGroup; point

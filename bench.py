@@ -4,6 +4,7 @@ sample-point updates/s = sum_i N_i / T, and ms per bundling iteration).
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--config 4]
     python bench.py --impl reference ...        # the CPU reference arm
+    python bench.py --dist ...                  # collective path at N=1 (1-rank NCCL)
 
 A *step* bundles the whole synthetic graph from its straight initial
 polylines through all ``config.iterations`` iterations (the reference's
@@ -12,16 +13,24 @@ timed loop, bundler.py:351-376): the step first restores the sampled points
 the timed region starts; the ~2 GB point arrays of config 4 exceed the
 126 MB L2, so no L2 flush is needed between steps.
 
-N > 1 (torchrun, one process per GPU, NCCL): edges are sharded by initial
-point count, the int32 histogram is all-reduced every iteration, the same
-total work is split over N GPUs ("strong" scaling), time = max over ranks.
+N > 1: one process per GPU over NCCL -- under torchrun, or launched by this
+script itself when ``--gpus N`` is given without torchrun.  Edges are
+sharded by initial point count, the int32 histogram is all-reduced every
+iteration, the same total work is split over N GPUs ("strong" scaling),
+time = max over ranks.
+
+``--impl reference`` times the reference's CPU path (the oracle port of the
+numba kernels, every host thread) on the same workload and the same
+``config`` object, one step = the whole loop; under torchrun only rank 0
+runs it.
 
 Extra keys: ``e2e`` (same metric through the public ``bundle()`` with host
 numpy inputs and the world-coordinate polylines copied back every step),
 ``roofline`` (dominant kernel, CUDA events over the timed region),
 ``cpu_baseline`` (the oracle port on this host's cores, bounded sample),
 ``clocks`` (nvidia-smi sampled during the timed region), ``gpu_launches``
-(kernels our library launched inside the timed region, hb_launch_count).
+(kernels our library launched inside the timed region, hb_launch_count),
+``run`` (how it ran: backend, histogram path, splat path).
 """
 
 from __future__ import annotations
@@ -42,7 +51,8 @@ sys.path.insert(0, ROOT)
 
 def parse_args():
     ap = argparse.ArgumentParser()
-    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--gpus", type=int, default=1,
+                    help="GPUs (ranks); without torchrun the script launches N ranks itself")
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--config", type=int, default=4, choices=[1, 2, 3, 4, 5])
@@ -53,8 +63,29 @@ def parse_args():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--e2e-steps", type=int, default=None)
     ap.add_argument("--cpu-iterations", type=int, default=2,
-                    help="iterations of the workload timed for cpu_baseline")
+                    help="iterations of the workload timed for our line's cpu_baseline")
+    ap.add_argument("--ref-iterations", type=int, default=None,
+                    help="--impl reference: iterations per step (default: all of the "
+                         "workload's, i.e. the same work as our arm)")
+    ap.add_argument("--dist", action="store_true",
+                    help="run the collective path even at N=1 (1-rank NCCL group: the "
+                         "histogram all-reduce, status agreement and gather execute)")
     return ap.parse_args()
+
+
+def launch_ranks(n: int) -> int:
+    """`--gpus N` without torchrun: run this script under
+    torch.distributed.run with N ranks (one per GPU) and return its exit
+    code (rank 0 prints the JSON line)."""
+    import socket
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+           f"--nproc-per-node={n}", "--master-addr=127.0.0.1", f"--master-port={port}",
+           os.path.abspath(__file__), *sys.argv[1:]]
+    return subprocess.call(cmd)
 
 
 def host_cores() -> int:
@@ -128,8 +159,12 @@ def algorithmic_bytes(name: str, n_prev: int, n_cur: int, n_edges: int, cells: i
         return 32 * n_cur + 4 * n_cur + 16 * n_edges
     if name == "hb_advect_laplacian":   # Laplacian (+ fused next resample count)
         return 32 * n_cur + 16 * n_edges + 4 * cells
-    if name == "hb_resample_emit":      # resample emit + fused splat
+    if name in ("hb_resample_emit", "hb_resample_emit_cap"):  # resample emit + fused splat
         return 16 * n_prev + 16 * n_cur + 40 * n_edges + 4 * cells
+    if name == "hb_exact_check":
+        return 4 * cells
+    if name == "hb_accumulate_ordered":  # hits -> sort -> fold (ordered path)
+        return 16 * n_cur + 16 * n_edges + 4 * cells
     if name == "hb_resample_count":
         return 16 * n_prev + 8 * n_edges
     if name == "hb_splat":
@@ -197,35 +232,51 @@ def cpu_reference_sample(w, iterations: int, workers: int):
     return pts / run.bundling_seconds, run, wall
 
 
+def workload_config(w, grid, points_per_step: int) -> dict:
+    """The ``config`` object both arms print: what the workload IS (graph,
+    grid, parameters and the sum of N_i per step -- identical in both arms,
+    the results being bit-identical), nothing about how it was run."""
+    cfg = w.config
+    return {"workload": w.name, "edges": int(w.graph.n_edges), "grid": [int(x) for x in grid],
+            "iterations": int(cfg.iterations), "points_per_step": int(points_per_step),
+            "delta": cfg.delta, "sigma": cfg.sigma, "lambda": cfg.lambda_,
+            "l2": "inputs > L2 (point arrays >> 126 MB), no flush"}
+
+
 def run_reference_arm(args, rank, world):
-    """--impl reference: rank 0 times the oracle port of the reference's CPU
-    path (oracle/hb_oracle.c driven exactly like _parallel.py) on all host
-    threads; a step = the first `--cpu-iterations` iterations of the
-    workload (sampling excluded, like the reference's own timer)."""
+    """--impl reference: rank 0 times the reference's CPU path -- the oracle
+    port (oracle/hb_oracle.c, the numba kernels restated in C, driven like
+    _parallel.py on every host thread) -- on the same workload, metric and
+    config as our arm: one step = the whole bundling loop, all iterations
+    (sampling excluded, like the reference's own timer).  Warm-up steps run
+    one iteration each (the C port has no JIT or cache to warm)."""
     if rank != 0:
         return
     from paper_1504_02687_b200.workloads import workload
     w = workload(args.config, scale=args.scale)
     cores = host_cores()
-    iters = max(1, args.cpu_iterations)
+    iters = args.ref_iterations or w.config.iterations
+    for _ in range(args.warmup):
+        cpu_reference_sample(w, 1, cores)
     vals, secs = [], []
-    for s in range(args.warmup + args.steps):
+    for _ in range(args.steps):
         v, run, _ = cpu_reference_sample(w, iters, cores)
-        if s >= args.warmup:
-            vals.append(v)
-            secs.append(run.bundling_seconds)
-    value = statistics.mean(vals)
+        vals.append(v)
+        secs.append(run.bundling_seconds)
     n_pts = sum(m.n_points for m in run.metrics)
+    value = n_pts * len(secs) / sum(secs)
     sample = (f"{w.name}: iterations 0-{iters - 1} of {w.config.iterations}, all "
-              f"{w.graph.n_edges} edges, {n_pts} point updates per step")
+              f"{w.graph.n_edges} edges, {n_pts} point updates per step, oracle port "
+              f"(oracle/hb_oracle.c) on {cores} threads")
     line = {
         "impl": "reference", "metric": "sample-point updates/sec", "value": value,
         "unit": "points/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": 1e3 * statistics.mean(secs), "higher_is_better": True,
         "ms_per_iteration": 1e3 * statistics.mean(secs) / iters,
+        "scaling": "strong", "vs_baseline": None,
         "dtype": "f64", "data": "synthetic",
-        "config": {"workload": w.name, "iterations_timed": iters,
-                   "grid": [int(w.matrix.shape[0]), *map(int, run.field.shape[1:])]},
+        "config": workload_config(w, (int(w.matrix.shape[0]), *map(int, run.field.shape[1:])),
+                                  n_pts),
         "cpu_baseline": {"value": value, "unit": "points/s", "cores": cores, "kind": "port",
                          "sample": sample},
         "e2e": {"value": value, "unit": "points/s", "h2d_bytes_per_step": 0,
@@ -240,9 +291,13 @@ def run_reference_arm(args, rank, world):
 
 def main():
     args = parse_args()
+    if "WORLD_SIZE" not in os.environ and args.gpus > 1:
+        sys.exit(launch_ranks(args.gpus))
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world != args.gpus:
+        sys.exit(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={world}")
     if args.impl == "reference":
         run_reference_arm(args, rank, world)
         return
@@ -261,30 +316,37 @@ def main():
     device_index = 0 if os.environ.get("HB_BENCH_ONE_DEVICE") == "1" else local
     torch.cuda.set_device(device_index)
     group = None
-    if world > 1:
+    if world > 1 or args.dist:
         os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+        if world == 1:  # --dist at N=1: a 1-rank group, collective path forced
+            os.environ.setdefault("MASTER_PORT", "29531")
+            os.environ.setdefault("RANK", "0")
+            os.environ["HB_FORCE_DIST"] = "1"
         backend = os.environ.get("HB_DIST_BACKEND", "nccl")
         if backend == "nccl":
-            dist.init_process_group("nccl", device_id=torch.device("cuda", device_index))
+            dist.init_process_group("nccl", device_id=torch.device("cuda", device_index),
+                                    world_size=world, rank=rank)
         else:
-            dist.init_process_group(backend)
+            dist.init_process_group(backend, world_size=world, rank=rank)
+    dist_on = dist.is_available() and dist.is_initialized()
+    backend_name = dist.get_backend() if dist_on else None
 
     def barrier():
-        if world > 1:
+        if dist_on:
             dist.barrier()
 
     def coll_device():
         return "cuda" if dist.get_backend() == "nccl" else "cpu"
 
     def max_over_ranks(x: float) -> float:
-        if world == 1:
+        if not dist_on:
             return x
         t = torch.tensor([x], dtype=torch.float64, device=coll_device())
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         return float(t.item())
 
     def sum_over_ranks(x: int) -> int:
-        if world == 1:
+        if not dist_on:
             return x
         t = torch.tensor([x], dtype=torch.int64, device=coll_device())
         dist.all_reduce(t)
@@ -369,26 +431,26 @@ def main():
                          f"updates, oracle port (oracle/hb_oracle.c) on {cores} threads"}
 
     if rank == 0:
+        par = f"edge-shard x{world}"
+        if dist_on:
+            par += f" + {backend_name} int32 histogram allreduce"
         line = {
             "metric": "sample-point updates/sec", "value": value, "unit": "points/s",
             "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
             "ms_per_step": ms_step, "ms_per_iteration": ms_step / n_it,
             "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
             "dtype": "f64", "data": "synthetic",
-            "config": {"workload": w.name, "edges": int(w.graph.n_edges),
-                       "grid": [eng.nbins, eng.nv, eng.nu], "iterations": n_it,
-                       "points_per_step": pts_per_step * world if world == 1 else total_pts // args.steps,
-                       "delta": cfg.delta, "sigma": cfg.sigma, "lambda": cfg.lambda_,
-                       "parallelism": f"edge-shard x{world}" + (" + nccl int32 allreduce"
-                                                                 if world > 1 else ""),
-                       "l2": "inputs > L2 (point arrays >> 126 MB), no flush",
-                       "splat": {1: "segment-key table", 0: "tile records", -1: "direct"}[eng.tile_mode],
-                       "segment_key_ratio": [round(x, 4) for x in eng.key_ratio]},
+            "config": workload_config(w, (eng.nbins, eng.nv, eng.nu), total_pts // args.steps),
+            "run": {"parallelism": par, "backend": backend_name,
+                    "histogram_path": eng.wkind,
+                    "splat": {1: "segment-key table", 0: "tile records",
+                              -1: "direct"}[eng.tile_mode],
+                    "segment_key_ratio": [round(x, 4) for x in eng.key_ratio]},
             "roofline": roof, "cpu_baseline": cpu, "clocks": clk, "e2e": e2e,
             "gpu_launches": launches,
         }
         print(json.dumps(line), flush=True)
-    if world > 1:
+    if dist_on:
         dist.destroy_process_group()
 
 

@@ -44,6 +44,7 @@ extern "C" {
 /* status-flag bits written by device kernels (caller-owned int32) */
 #define HB_STATUS_OUT_OF_BOUNDS 1 /* raster.py:57-67 "sample out of bounds" */
 #define HB_STATUS_CAPACITY 4      /* a resample did not fit the output buffer */
+#define HB_STATUS_INEXACT 8       /* integer fast path no longer equals float32 sums */
 
 /* Tile-binned splatting state (all pointers caller-owned device memory).
  * The grid of every layer is cut into tile x tile cells; a segment is binned
@@ -154,14 +155,6 @@ HB_API int hb_splat(const double *pts, const int64_t *starts, int64_t n_edges,
  * into counts but records each tile's demand in tiles->fill (census for the
  * next hb_tiles_plan); with rec != NULL segments are binned and the caller
  * finishes with hb_tiles_flush.  hb_resample_emit takes the same argument. */
-
-/* Same rasterisation with float32 weights (non-integer edge weights):
- * hist[group[e]] += weight[e] with float atomics (order-dependent in the
- * last bits, like the reference across worker counts, raster.py:76-78). */
-HB_API int hb_splat_f32(const double *pts, const int64_t *starts, int64_t n_edges,
-                 int64_t n_pts, const int32_t *group, const float *weight,
-                 float *hist, int nbins, int nv, int nu, int32_t *status,
-                 void *stream);
 
 /* Workspace for hb_smooth: bytes of float64 tables + float32 staging. */
 HB_API size_t hb_smooth_workspace_bytes(int nbins, int nv, int nu);
@@ -365,6 +358,43 @@ HB_API int hb_kmeans_inertia(const double *features, int64_t n, int d, int k,
 HB_API int hb_kmeans_scatter(const double *features, int64_t n, int d, int k,
                              const double *centroids, const int8_t *assign, double *scatter,
                              int64_t *counts, void *stream);
+
+/* ---- bounds, exactness guard, ordered accumulation (raster.py:57-94) ----
+ * _check_bounds (raster.py:57-67): out4 = {xmin, ymin, xmax, ymax} of the
+ * n_pts points; scratch32 is 32 bytes of device scratch. */
+HB_API int hb_point_span(const double *pts, int64_t n_pts, void *scratch32, double *out4,
+                         void *stream);
+/* Guard of the integer fast path (per-group int32 counts mixed once): sets
+ * HB_STATUS_INEXACT when some cell has sum_b |M[l,b]| * counts[b] >= limit
+ * for a layer l (limit = 2^24 x the power-of-two quantum of every layer
+ * weight: beyond it the reference's float32 sums round), or a negative
+ * count.  abs_matrix: (B,B) float64 |M|, NULL = identity. */
+HB_API int hb_exact_check(const int32_t *counts, const double *abs_matrix, int nbins, int nv,
+                          int nu, double limit, int32_t *status, void *stream);
+/* Hit offsets of _kernels.accumulate (_kernels.py:46-77) in the reference's
+ * order: hoff[p] = number of cell increments of all segments before point
+ * p (n_pts + 1 int64; hoff[n_pts] = the total).  Workspace:
+ * hb_hits_workspace_bytes(n_pts). */
+HB_API size_t hb_hits_workspace_bytes(int64_t n_pts);
+HB_API int hb_hits_count(const double *pts, const int64_t *starts, int64_t n_edges,
+                         int64_t n_pts, int64_t *hoff, void *workspace, size_t workspace_bytes,
+                         void *stream);
+/* The reference's float32 histogram (raster.py:70-94) bit for bit for any
+ * layer weights: edges cut into `nparts` (= workers) partition_ranges
+ * (_parallel.py:20-28, over edges_total global edges, this shard's first
+ * global edge = edge_base), every cell of every partition folded in
+ * (edge, segment, step) order with layer_w[e,l] = fl32(w[e]) * M[l, g[e]]
+ * (bundler.py:345-346), partitions summed left to right.  w32 (NULL = 1)
+ * and groups (NULL = 0) are indexed by GLOBAL edge; matrix (B,B) float32,
+ * NULL = identity.  out: (B,V,U) float32.  Workspace:
+ * hb_ordered_workspace_bytes(n_hits, nv, nu, nparts), n_hits = hoff[n_pts]. */
+HB_API size_t hb_ordered_workspace_bytes(int64_t n_hits, int nv, int nu, int nparts);
+HB_API int hb_accumulate_ordered(const double *pts, const int64_t *starts, int64_t n_edges,
+                                 const int64_t *hoff, int64_t n_pts, int64_t n_hits, int nparts,
+                                 int64_t edge_base, int64_t edges_total, const float *w32,
+                                 const int32_t *groups, const float *matrix, int nbins, int nv,
+                                 int nu, float *out, int32_t *status, void *workspace,
+                                 size_t workspace_bytes, void *stream);
 
 /* ---- rendering (render.py:158-179) ----
  * Stroke width of every segment of every polyline (segments of edge e are

@@ -18,7 +18,7 @@ LIB_DIR = os.path.join(_PKG, "_lib")
 LIB_PATH = os.path.join(LIB_DIR, "libhb_b200.so")
 INCLUDE = os.path.join(os.path.dirname(_PKG), "include")
 
-SOURCES = ["hb_api.cu", "hb_polyline.cu", "hb_field.cu", "hb_advect.cu", "hb_advect_flat.cu", "hb_lapcount.cu", "hb_splat.cu", "hb_binning.cu", "hb_render.cu"]
+SOURCES = ["hb_api.cu", "hb_polyline.cu", "hb_field.cu", "hb_advect.cu", "hb_advect_flat.cu", "hb_lapcount.cu", "hb_splat.cu", "hb_binning.cu", "hb_render.cu", "hb_ordered.cu"]
 
 NVCC_FLAGS = [
     "-gencode", "arch=compute_100a,code=sm_100a",
@@ -104,7 +104,6 @@ SIGNATURES = {
     "hb_segtab_geometry": (_I, [_I, _I, _I, _D, _P, _P]),
     "hb_segtab_expand": (_I, [_P, _P, _I, _I, _P, _P]),
     "hb_splat": (_I, [_P, _P, _I64, _I64, _P, _P, _P, _I, _I, _I, _P, _P, _P]),
-    "hb_splat_f32": (_I, [_P, _P, _I64, _I64, _P, _P, _P, _I, _I, _I, _P, _P]),
     "hb_smooth_workspace_bytes": (_SZ, [_I, _I, _I]),
     "hb_smooth": (_I, [_P, _P, _P, _I, _I, _I, _P, _I, _P, _P, _SZ, _P, _P]),
     "hb_mix_layers": (_I, [_P, _P, _P, _I, _I, _I, _P, _P]),
@@ -128,6 +127,13 @@ SIGNATURES = {
                                   _P, _P, _P]),
     "hb_clamp_starts": (_I, [_P, _I64, _I64, _P, _P]),
     "hb_probe": (_I, [_P, _I, _I, _P, _I64, _P, _P, _P]),
+    "hb_point_span": (_I, [_P, _I64, _P, _P, _P]),
+    "hb_exact_check": (_I, [_P, _P, _I, _I, _I, _D, _P, _P]),
+    "hb_hits_workspace_bytes": (_SZ, [_I64]),
+    "hb_hits_count": (_I, [_P, _P, _I64, _I64, _P, _P, _SZ, _P]),
+    "hb_ordered_workspace_bytes": (_SZ, [_I64, _I, _I, _I]),
+    "hb_accumulate_ordered": (_I, [_P, _P, _I64, _P, _I64, _I64, _I, _I64, _I64, _P, _P, _P,
+                                   _I, _I, _I, _P, _P, _P, _SZ, _P]),
 }
 
 class HbTiles(ctypes.Structure):

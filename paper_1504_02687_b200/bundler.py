@@ -25,8 +25,8 @@ import torch
 
 from . import _native as N
 from . import dist as D
-from .engine import (MIN_STEP, BundleEngine, download, download_pinned, ptr, stream_ptr,
-                     upload, weight_plan)
+from .engine import (MIN_STEP, BundleEngine, download, download_pinned, ordered_plan, ptr,
+                     sample_counts, stream_ptr, upload, weight_plan)
 from .model import (BundleConfig, DensityField, Graph, GridTransform, SampledEdge,
                     interaction_matrix, make_transform)
 
@@ -58,9 +58,10 @@ class PackedPolylines(Sequence):
     results do not create 20M Python objects up front.
     """
 
-    def __init__(self, world: np.ndarray, starts: np.ndarray):
+    def __init__(self, world: np.ndarray, starts: np.ndarray, edge_base: int = 0):
         self.world = world
         self.starts = starts
+        self.edge_base = int(edge_base)  # global index of the first edge held
 
     def __len__(self) -> int:
         return self.starts.shape[0] - 1
@@ -73,7 +74,7 @@ class PackedPolylines(Sequence):
             i += n
         if not 0 <= i < n:
             raise IndexError(i)
-        return SampledEdge(i, self.world[self.starts[i]:self.starts[i + 1]])
+        return SampledEdge(self.edge_base + i, self.world[self.starts[i]:self.starts[i + 1]])
 
 
 @dataclass
@@ -93,12 +94,18 @@ def _resolve(graph, config, bins, matrix):
     bins_arr = graph.bins if bins is None else np.ascontiguousarray(bins, dtype=np.int64)
     if bins_arr.shape[0] != graph.n_edges:
         raise ValueError("bins length does not match edge count")
+    # (the reference's numpy indexing would wrap a negative bin; the device
+    # layer offsets must not, so the Graph rule, model.py:138, applies here)
+    if graph.n_edges and int(bins_arr.min()) < 0:
+        raise ValueError("edge bins must be nonnegative")
     nbins = int(bins_arr.max()) + 1 if graph.n_edges else 1
     if matrix is None:
         matrix = interaction_matrix(nbins, cfg.alpha)
     matrix = np.asarray(matrix, dtype=np.float32)
     if matrix.shape[0] < nbins:
         raise ValueError(f"interaction matrix smaller than bin count {nbins}")
+    if matrix.ndim != 2 or matrix.shape[0] != matrix.shape[1]:
+        raise ValueError("interaction matrix must be square")
     return cfg, bins_arr, matrix
 
 
@@ -126,21 +133,47 @@ class _Run:
 
 def prepare_engine(graph: Graph, config: BundleConfig | None = None, *, bins=None,
                    matrix=None, _fixed_step: bool = False, group=None,
-                   capacity_factor: float = 2.0):
+                   capacity_factor: float = 2.0, workers: int = 1, ordered: bool = False,
+                   sync_free: bool = True):
     """Validate, transform, shard and sample (everything the reference does
     before its timed loop, bundler.py:325-346) and return
-    ``(engine, transform, edge_lo, edge_hi)`` ready for ``engine.run()``."""
+    ``(engine, transform, edge_lo, edge_hi)`` ready for ``engine.run()``.
+    ``ordered`` forces the reference-order histogram path; ``sync_free=False``
+    reads each iteration's point total on the host (no capacity retries, so
+    the engine can be stepped and inspected iteration by iteration)."""
     cfg, bins_arr, matrix = _resolve(graph, config, bins, matrix)
-    return _setup(graph, cfg, bins_arr, matrix, _fixed_step, group, capacity_factor)
+    return _setup(graph, cfg, bins_arr, matrix, _fixed_step, group, capacity_factor,
+                  workers=workers, force_ordered=ordered, sync_free=sync_free)
 
 
-def _setup(graph, cfg, bins_arr, matrix, fixed_step, group, capacity_factor):
+def _plan(graph, cfg, matrix, transform, force_ordered=False):
+    """The histogram path for the WHOLE graph (every rank decides alike)."""
+    if force_ordered:
+        return ordered_plan(graph.weights)
+    n0 = 0
+    if graph.n_edges and not np.all(np.asarray(graph.weights, np.float32) == 1.0):
+        pos = graph.positions
+        n0 = int(sample_counts(transform.world_to_grid(pos[graph.sources]),
+                               transform.world_to_grid(pos[graph.targets]), cfg.delta).sum())
+    return weight_plan(graph.weights, matrix, n0)
+
+
+def _setup(graph, cfg, bins_arr, matrix, fixed_step, group, capacity_factor, *,
+           workers=1, force_ordered=False, sync_free=True):
     transform = make_transform(graph.positions, cfg.grid_size, cfg.padding_cells)
     rank, world = D.rank_world(group)
-    reduce_hist = (lambda h: D.all_reduce_sum(h, group)) if world > 1 else None
+    multi = D.distributed(group)
+    reduce_hist = (lambda h: D.all_reduce_sum(h, group)) if multi else None
+    reduce_flags = (lambda t: D.all_reduce_max(t, group)) if multi else None
+    plan = _plan(graph, cfg, matrix, transform, force_ordered)
+    if world > 1 and plan.kind == "ordered":
+        raise NotImplementedError(
+            "the reference-order histogram (non-dyadic interaction matrix or fractional "
+            "weights) runs on one GPU; shard only exact-weight graphs")
     common = dict(fixed_step=fixed_step, reduce_hist=reduce_hist,
-                  capacity_factor=capacity_factor)
-    if world == 1 and cfg.directed_offset_fraction == 0:
+                  capacity_factor=capacity_factor, workers=workers,
+                  reduce_flags=reduce_flags, sync_free=sync_free)
+    if not multi and cfg.directed_offset_fraction == 0:
         # per-edge preparation on the device: the host uploads node positions
         # and endpoint indices once, the kernel computes the grid endpoints and
         # the reference's point counts, CUB scans them into `starts`
@@ -160,7 +193,7 @@ def _setup(graph, cfg, bins_arr, matrix, fixed_step, group, capacity_factor):
                float(transform.origin[0]), float(transform.origin[1]),
                float(transform.cell_size), float(cfg.delta), ptr(src), ptr(dst), ptr(counts), s)
         N.call("hb_scan_counts", ptr(counts), E, ptr(starts), ptr(ws), ws.numel(), s)
-        eng = BundleEngine(src, dst, bins_arr, weight_plan(graph.weights), matrix,
+        eng = BundleEngine(src, dst, bins_arr, plan, matrix,
                            transform.shape, cfg, starts=starts, **common)
         eng.node_arrays = (node_pos, srcs, tgts)
         return eng, transform, 0, E
@@ -169,7 +202,6 @@ def _setup(graph, cfg, bins_arr, matrix, fixed_step, group, capacity_factor):
     dst_all = transform.world_to_grid(pos[graph.targets])
     lo, hi = 0, graph.n_edges
     if world > 1:
-        from .engine import sample_counts
         counts = sample_counts(src_all, dst_all, cfg.delta)
         lo, hi = D.shard_edges(counts, world)[rank]
     src = np.ascontiguousarray(src_all[lo:hi])
@@ -178,17 +210,20 @@ def _setup(graph, cfg, bins_arr, matrix, fixed_step, group, capacity_factor):
     if cfg.directed_offset_fraction > 0:
         od = _offset_vectors(src, dst, cfg.directed_offset_fraction
                              * max(transform.width, transform.height))
-    eng = BundleEngine(src, dst, bins_arr[lo:hi], weight_plan(graph.weights[lo:hi]),
+    eng = BundleEngine(src, dst, bins_arr[lo:hi], plan.slice(lo, hi),
                        matrix, transform.shape, cfg, offset_disp=od, **common)
     eng.node_arrays = None
     return eng, transform, lo, hi
 
 
 def _run_engine(graph, cfg, bins_arr, matrix, fixed_step, on_iteration, group=None,
-                capacity_factor=2.0):
+                capacity_factor=2.0, workers=1):
     t0 = time.perf_counter()
+    # a per-iteration callback reads the metrics every iteration anyway, so
+    # the run is synchronous (no capacity retry can replay callbacks)
     eng, transform, lo, hi = _setup(graph, cfg, bins_arr, matrix, fixed_step, group,
-                                    capacity_factor)
+                                    capacity_factor, workers=workers,
+                                    sync_free=on_iteration is None)
     if on_iteration is None:
         eng.run()
     else:
@@ -223,19 +258,24 @@ def bundle(graph: Graph, config: BundleConfig | None = None, *,
            _fixed_step: bool = False, group=None) -> BundleResult:
     """Run the full bundling pipeline on the GPU (reference ``bundler.py:311-380``).
 
-    Same signature and result as the reference. ``workers`` is accepted and
-    ignored (parallelism is the device's; with ``torch.distributed``
-    initialised, edges are sharded across ranks and every rank returns the
-    full result). ``graph`` may be a reference ``histobundle.model.Graph``.
+    Same signature and result as the reference. Parallelism is the device's;
+    ``workers`` keeps its reference meaning only where it changes results:
+    the number of edge partitions whose float32 histograms the reference
+    sums in order (``raster.py:85-94``), which matters for inexact layer
+    weights (repulsive matrices, fractional weights) and is reproduced
+    exactly. With ``torch.distributed`` initialised, edges are sharded
+    across ranks; rank 0 returns the full result and every other rank its
+    own edge shard (``sampled_edges.edge_base`` = its first edge).
+    ``graph`` may be a reference ``histobundle.model.Graph``.
     """
-    del workers
     cfg, bins_arr, matrix = _resolve(graph, config, bins, matrix)
-    if (on_iteration is None and D.rank_world(group)[1] == 1
+    if (on_iteration is None and not D.distributed(group)
             and os.environ.get("HB_STREAM_OUT", "1") != "0"):
         # one GPU: the last iteration streams its polylines to the host while
         # the remaining edge chunks are still being advected
         t0 = time.perf_counter()
-        eng, tr, _, _ = _setup(graph, cfg, bins_arr, matrix, _fixed_step, group, 2.0)
+        eng, tr, _, _ = _setup(graph, cfg, bins_arr, matrix, _fixed_step, group, 2.0,
+                               workers=workers)
         if eng.node_arrays is not None:
             world, recs = eng.run_streamed(tr.origin, tr.cell_size, *eng.node_arrays)
             starts = download(eng.starts)
@@ -246,7 +286,8 @@ def bundle(graph: Graph, config: BundleConfig | None = None, *,
         recs = eng.run()
         run = _Run(eng, tr, 0, graph.n_edges, recs, time.perf_counter() - t0)
     else:
-        run = _run_engine(graph, cfg, bins_arr, matrix, _fixed_step, on_iteration, group)
+        run = _run_engine(graph, cfg, bins_arr, matrix, _fixed_step, on_iteration, group,
+                          workers=workers)
     eng, tr = run.engine, run.transform
     if eng.node_arrays is not None:
         world_dev = eng.world_points_nodes(tr.origin, tr.cell_size, *eng.node_arrays)
@@ -255,25 +296,31 @@ def bundle(graph: Graph, config: BundleConfig | None = None, *,
         src_w = pos[graph.sources[run.edge_lo:run.edge_hi]]
         dst_w = pos[graph.targets[run.edge_lo:run.edge_hi]]
         world_dev = eng.world_points(tr.origin, tr.cell_size, src_w, dst_w)
-    if D.rank_world(group)[1] == 1:
+    edge_base = 0
+    if not D.distributed(group):
         world, starts = download_pinned(world_dev), download(eng.starts)
     else:
-        world, starts = D.gather_polylines(world_dev, eng.starts, group)
+        got = D.gather_polylines(world_dev, eng.starts, group)
+        if got is None:  # not rank 0: this rank's own shard
+            world, starts = download_pinned(world_dev), download(eng.starts)
+            edge_base = run.edge_lo
+        else:
+            world, starts = got
     field = DensityField(tr, download(eng.field))
     metrics = _metrics(run.records, group)
-    return BundleResult(graph, PackedPolylines(world, starts), field, metrics,
+    return BundleResult(graph, PackedPolylines(world, starts, edge_base), field, metrics,
                         sum(m.seconds for m in metrics))
 
 
 def bundle_packed(graph: Graph, config: BundleConfig | None = None, *, bins=None,
                   matrix=None, _fixed_step: bool = False, group=None,
-                  capacity_factor: float = 2.0):
+                  capacity_factor: float = 2.0, workers: int = 1):
     """Like :func:`bundle` but keeps the result on the device: returns
     ``(engine, transform, metrics)`` with the shard's packed grid-space
     points in ``engine.packed_points()`` (no host copies, no gathers)."""
     cfg, bins_arr, matrix = _resolve(graph, config, bins, matrix)
     run = _run_engine(graph, cfg, bins_arr, matrix, _fixed_step, None, group,
-                      capacity_factor)
+                      capacity_factor, workers=workers)
     return run.engine, run.transform, _metrics(run.records, group)
 
 

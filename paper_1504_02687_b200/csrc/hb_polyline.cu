@@ -159,15 +159,11 @@ splat_kernel(const double2 *__restrict__ pts, const int64_t *__restrict__ starts
 }
 
 // ---------------------------------------------------------------------------
-// resample_emit (_kernels.py:235-272) + accumulate of the new polylines,
-// warp per edge.  pos[j] (from the count pass) is the output index of kept
-// point j (-1 if merged).  A kept point x whose previous kept point is a
-// (pieces = pos[x] - pos[a]) owns outputs pos[a]+1 .. pos[x]: k/pieces
-// interpolants a + (k/pieces)(x - a), then x itself.  Work is balanced over
-// OUTPUT points: in each round lane t produces output m = base + t, finds
-// its owner lane by a 5-step shuffle search over the kept lanes' output
-// positions, writes it (coalesced) and rasterises the segment ending at it.
-// Chunks where every point is kept with one piece skip the search.
+// resample_emit (_kernels.py:235-272) + accumulate of the new polylines.
+// pos[j] (from the count pass) is the output index of kept point j (-1 if
+// merged).  A kept point x whose previous kept point is a (pieces = pos[x] -
+// pos[a]) owns outputs pos[a]+1 .. pos[x]: k/pieces interpolants
+// a + (k/pieces)(x - a), then x itself.
 __device__ __forceinline__ double2 interp_piece(double2 a, double2 x, int k, int pieces) {
     if (k == pieces) return x;
     if (k == 0) return a;
@@ -188,332 +184,6 @@ __device__ __forceinline__ double2 interp_piece(double2 a, double2 x, int k, int
 #define HB_ST_STREAM(p, v) (*(p) = (v))
 #endif
 
-#ifndef HB_EMIT_MINB
-#define HB_EMIT_MINB 3
-#endif
-
-__global__ void __launch_bounds__(kStreamBlock, HB_EMIT_MINB)
-emit_kernel(const double2 *__restrict__ pts, const int64_t *__restrict__ starts,
-            int64_t n_edges, const int32_t *__restrict__ pos,
-            const int64_t *__restrict__ new_starts, double2 *__restrict__ out,
-            const int32_t *__restrict__ group, const int32_t *__restrict__ weight,
-            int32_t *__restrict__ hist, int64_t plane, int nv, int nu,
-            int32_t *__restrict__ status, const __grid_constant__ hb_tiles tl, int use_tiles,
-            int64_t out_cap) {
-    const hb_tiles *tiles = use_tiles ? &tl : nullptr;
-    const unsigned full = 0xffffffffu;
-    const int lane = threadIdx.x & 31;
-    // the output total is only known on the device: a resample that would
-    // not fit the caller's buffer writes nothing and raises a status bit
-    if (new_starts[n_edges] > out_cap) {
-        if (blockIdx.x == 0 && threadIdx.x == 0 && status) atomicOr(status, HB_STATUS_CAPACITY);
-        return;
-    }
-    const unsigned below_mask = (1u << lane) - 1u;
-    const int64_t nwarps = (int64_t)gridDim.x * (kStreamBlock / 32);
-    int64_t e = ((int64_t)blockIdx.x * kStreamBlock + threadIdx.x) / 32;
-    // next edge's bounds are fetched one edge ahead, its first chunk one
-    // chunk ahead, so a warp always has a load in flight while it computes
-    int64_t s_nx = 0, t_nx = 0;
-    if (e < n_edges) { s_nx = starts[e]; t_nx = starts[e + 1]; }
-    for (; e < n_edges; e += nwarps) {
-        const int64_t s = s_nx;
-        const int n = (int)(t_nx - s);
-        if (e + nwarps < n_edges) { s_nx = starts[e + nwarps]; t_nx = starts[e + nwarps + 1]; }
-        double2 *o = out + new_starts[e];
-        const bool splat = hist != nullptr;
-        const int grp = splat && group ? group[e] : 0;
-        const int32_t w = weight ? weight[e] : 1;
-        // carry: last kept point so far and its output index (none yet)
-        double2 a = make_double2(0.0, 0.0);
-        int apos = -1;
-        int pj_nx = lane < n ? HB_LD_STREAM(pos + s + lane) : -1;
-        double2 x_nx = lane < n ? HB_LD_STREAM(pts + s + lane) : make_double2(0.0, 0.0);
-        for (int c0 = 0; c0 < n; c0 += kWarp) {
-            // local point 0 has pos 0: it is output 0 and the first `a`
-            const int j = c0 + lane;
-            const bool valid = j < n;
-            const int pj = pj_nx;
-            const double2 x = x_nx;
-            if (j + kWarp < n) {
-                pj_nx = HB_LD_STREAM(pos + s + j + kWarp);
-                x_nx = HB_LD_STREAM(pts + s + j + kWarp);
-            } else {
-                pj_nx = -1;  // past the end of the edge
-            }
-            const bool kept = pj >= 0;
-            const unsigned km = __ballot_sync(full, kept);
-            if (km == 0) continue;
-            const unsigned below = km & below_mask;
-            const int src = below ? 31 - __clz(below) : lane;
-            const double px = __shfl_sync(full, x.x, src);
-            const double py = __shfl_sync(full, x.y, src);
-            const int ppos = __shfl_sync(full, pj, src);
-            // previous kept point of this lane (valid for kept lanes)
-            const double2 pa2 = below ? make_double2(px, py) : a;
-            const int pa = below ? ppos : apos;
-            const int lk = 31 - __clz(km);
-            const int last_pos = __shfl_sync(full, pj, lk);
-            const bool simple = __all_sync(full, !valid || (kept && pj - pa == 1));
-            if (simple) {
-                // every valid lane is kept with one piece: output pj is x itself
-                if (valid) HB_ST_STREAM(o + pj, x);
-                if (splat)
-                    bin_or_splat<int32_t>(valid && pj >= 1, pa2.x, pa2.y, x.x, x.y,
-                                          pj == 1 ? 0 : 1, w, grp, hist, plane, nv, nu, status,
-                                          tiles);
-            } else {
-                // key: output index of the nearest kept point at or below this lane
-                const int key = kept ? pj : pa;
-                // segment m-1 -> m starts at output m-1: the previous lane's
-                // point (bit-identical to re-interpolating piece k-1), the
-                // previous round's lane 31, or at the chunk start output apos,
-                // the carried kept point a
-                double2 qprev = a;
-                for (int m = apos + 1 + lane; m - lane <= last_pos; m += kWarp) {
-                    int lo = 0;
-#pragma unroll
-                    for (int step = 16; step; step >>= 1) {
-                        const int probe = __shfl_sync(full, key, lo + step - 1);
-                        if (probe < m) lo += step;
-                    }
-                    const int owner = lo > 31 ? 31 : lo;
-                    const double ox = __shfl_sync(full, x.x, owner);
-                    const double oy = __shfl_sync(full, x.y, owner);
-                    const double oax = __shfl_sync(full, pa2.x, owner);
-                    const double oay = __shfl_sync(full, pa2.y, owner);
-                    const int opj = __shfl_sync(full, pj, owner);
-                    const int opa = __shfl_sync(full, pa, owner);
-                    const bool here = m <= last_pos;
-                    double2 q = make_double2(0.0, 0.0);
-                    if (here) {
-                        const int pieces = opj - opa, k = m - opa;
-                        q = interp_piece(make_double2(oax, oay), make_double2(ox, oy), k, pieces);
-                        HB_ST_STREAM(o + m, q);
-                    }
-                    if (splat) {
-                        double q0x = __shfl_up_sync(full, q.x, 1), q0y = __shfl_up_sync(full, q.y, 1);
-                        if (lane == 0) { q0x = qprev.x; q0y = qprev.y; }
-                        qprev = make_double2(__shfl_sync(full, q.x, 31), __shfl_sync(full, q.y, 31));
-                        bin_or_splat<int32_t>(here && m >= 1, q0x, q0y, q.x, q.y,
-                                              m == 1 ? 0 : 1, w, grp, hist, plane, nv, nu, status,
-                                              tiles);
-                    }
-                }
-            }
-            a.x = __shfl_sync(full, x.x, lk);
-            a.y = __shfl_sync(full, x.y, lk);
-            apos = last_pos;
-        }
-    }
-}
-
-// ---------------------------------------------------------------------------
-// Flat, output-tiled emit: the same outputs and splat as emit_kernel, but a
-// warp works on tiles of 32 consecutive GLOBAL outputs instead of one edge at
-// a time, so every lane has an output (short edges and ragged chunk ends
-// left a third of the lanes idle) and no owner needs a shuffle search.
-//
-// Kept inputs j (pos[j] >= 0) have global output indices G(j) =
-// new_starts[e(j)] + pos[j], strictly increasing in j.  Output m is the kept
-// input with G == m, or lies between the last kept input with G < m and the
-// first with G > m -- both of m's own edge, because an edge's first and last
-// inputs are always kept (pos 0 and count-1) -- at piece m - G(prev) of
-// G(next) - G(prev) (interp_piece, bit-identical to emit_kernel's).  Per
-// tile the warp scans its current 32-input chunk (advancing while no kept
-// input reaches the tile's last output), drops the tile's kept inputs into a
-// 33-slot shared table by G - m0 (slot 32: the first kept input past the
-// tile), and each lane finds its neighbours with two bit scans of the
-// occupancy mask.  Segment m-1 -> m (splat) starts at the previous lane's
-// output; lane 0 carries the previous tile's lane 31, so each warp first
-// recomputes the tile before its range without writing anything.
-struct EmitSlots {
-    double x[33], y[33];
-    long long g[33];    // G of the kept input in the slot
-    long long nsb[33];  // new_starts of its edge
-    int e[33];
-};
-
-#ifndef HB_EMIT_FLAT_MINB
-#define HB_EMIT_FLAT_MINB 4
-#endif
-__global__ void __launch_bounds__(kStreamBlock, HB_EMIT_FLAT_MINB)
-emit_flat_kernel(const double2 *__restrict__ pts, const int64_t *__restrict__ starts,
-                 int64_t n_edges, const int32_t *__restrict__ pos,
-                 const int64_t *__restrict__ new_starts, double2 *__restrict__ out,
-                 const int32_t *__restrict__ group, const int32_t *__restrict__ weight,
-                 int32_t *__restrict__ hist, int64_t plane, int nv, int nu,
-                 int32_t *__restrict__ status, const __grid_constant__ hb_tiles tl, int use_tiles,
-                 int64_t out_cap) {
-    __shared__ EmitSlots s_slots[kStreamBlock / 32];
-    const hb_tiles *tiles = use_tiles ? &tl : nullptr;
-    const unsigned full = 0xffffffffu;
-    const int lane = threadIdx.x & 31;
-    if (new_starts[n_edges] > out_cap) {
-        if (blockIdx.x == 0 && threadIdx.x == 0 && status) atomicOr(status, HB_STATUS_CAPACITY);
-        return;
-    }
-    EmitSlots &S = s_slots[threadIdx.x >> 5];
-    const int64_t M_lo = new_starts[0], M_hi = new_starts[n_edges];
-    const int64_t J_hi = starts[n_edges];
-    const int64_t n_tiles = M_hi > M_lo ? (M_hi - M_lo + 31) >> 5 : 0;
-    const int64_t gw = ((int64_t)blockIdx.x * kStreamBlock + threadIdx.x) >> 5;
-    const int64_t nw = (int64_t)gridDim.x * (kStreamBlock / 32);
-    const int64_t per = (n_tiles + nw - 1) / nw;
-    const int64_t t_beg = gw * per;
-    const int64_t t_end = t_beg + per < n_tiles ? t_beg + per : n_tiles;
-    if (t_beg >= t_end) return;  // (warp-uniform)
-    const bool splat = hist != nullptr;
-    const int64_t t0 = t_beg > 0 ? t_beg - 1 : t_beg;  // one dry tile for the carry
-    const int64_t m_first = M_lo + t0 * 32;
-
-    // edge of output m_first: the last e with new_starts[e] <= m_first
-    int64_t e_cur = 0;
-    if (lane == 0) {
-        int64_t lo = 0, hi = n_edges - 1;
-        while (lo < hi) {
-            const int64_t mid = (lo + hi + 1) >> 1;
-            if (new_starts[mid] <= m_first) lo = mid; else hi = mid - 1;
-        }
-        e_cur = lo;
-    }
-    e_cur = __shfl_sync(full, e_cur, 0);
-    // input cursor: a kept input of that edge with output index < m_first's
-    // (the edge's first input, moved forward by a 32-way search on pos)
-    int64_t jc = starts[e_cur];
-    {
-        const int64_t lm = m_first - new_starts[e_cur];
-        int64_t hi = starts[e_cur + 1];
-        for (int it = 0; it < 6 && lm > 0 && hi - jc > 64; ++it) {
-            const int64_t step = (hi - jc + 31) / 32;
-            const int64_t j = jc + lane * step;
-            const int pj = j < hi ? pos[j] : -1;
-            const unsigned ok = __ballot_sync(full, pj >= 0 && pj < lm);  // bit 0: jc itself
-            const unsigned past = __ballot_sync(full, pj >= lm);
-            const int L = 31 - __clz(ok);
-            const unsigned after = L == 31 ? 0u : (past & (0xfffffffeu << L));
-            if (after) hi = jc + (int64_t)(__ffs(after) - 1) * step;
-            jc += (int64_t)L * step;
-            if (L == 0 && !after) break;  // a long run of dropped inputs: scan it
-        }
-    }
-
-    // current input chunk [jc, jc + 32): point, edge, G (-1: dropped / none)
-    // (measured: issuing the next chunk's loads one chunk ahead costs more in
-    // registers / occupancy than it hides, 5.88 -> 6.06 ms on config 4)
-    double2 x = make_double2(0.0, 0.0);
-    int64_t G = -1, nsb = 0;
-    int ej = 0;
-    int64_t e_next = e_cur;
-    auto load_chunk = [&]() {
-        const int64_t j = jc + lane;
-        const bool in = j < J_hi;
-        x = in ? HB_LD_STREAM(pts + j) : make_double2(0.0, 0.0);
-        const int pj = in ? HB_LD_STREAM(pos + j) : -1;
-        // edges starting in (jc, jc + 31] (every edge has >= 1 input)
-        const int64_t ek = e_cur + 1 + lane;
-        const int64_t sv = ek <= n_edges ? starts[ek] : INT64_MAX;
-        const int64_t rel = sv - jc;  // >= 1
-        const unsigned smask = __reduce_or_sync(full, rel <= 31 ? (1u << rel) : 0u);
-        int64_t e = e_cur + __popc(smask & (0xffffffffu >> (31 - lane)));
-        if (e > n_edges - 1) e = n_edges - 1;
-        ej = (int)e;
-        nsb = new_starts[e];
-        G = pj >= 0 ? nsb + pj : -1;
-        e_next = e_cur + __popc(__ballot_sync(full, rel <= 32));
-    };
-    load_chunk();
-
-    double2 cq = make_double2(0.0, 0.0);      // output m0 - 1 (previous tile's lane 31)
-    double cpx = 0.0, cpy = 0.0;               // last kept input with G < m0 ...
-    int64_t cpg = 0;                           // ... and its G
-    for (int64_t tt = t0; tt < t_end; ++tt) {
-        const bool dry = tt < t_beg;
-        const int64_t m0 = M_lo + tt * 32;
-        const int64_t m_last = m0 + 31 < M_hi - 1 ? m0 + 31 : M_hi - 1;
-        unsigned W = 0;
-        for (;;) {
-            const bool kept = G >= 0;
-            const bool inw = kept && G >= m0 && G <= m0 + 31;
-            if (inw) {
-                const int sl = (int)(G - m0);
-                S.x[sl] = x.x; S.y[sl] = x.y; S.g[sl] = G; S.nsb[sl] = nsb; S.e[sl] = ej;
-            }
-            W |= __reduce_or_sync(full, inw ? (1u << (int)(G - m0)) : 0u);
-            const unsigned below = __ballot_sync(full, kept && G < m0);
-            if (below) {
-                const int L = 31 - __clz(below);
-                cpx = __shfl_sync(full, x.x, L);
-                cpy = __shfl_sync(full, x.y, L);
-                cpg = __shfl_sync(full, G, L);
-            }
-            const unsigned beyond = __ballot_sync(full, kept && G > m0 + 31);
-            if (beyond && lane == __ffs(beyond) - 1) {
-                S.x[32] = x.x; S.y[32] = x.y; S.g[32] = G; S.nsb[32] = nsb; S.e[32] = ej;
-            }
-            if (__any_sync(full, kept && G >= m_last)) {
-                break;
-            }
-            if (jc + 32 >= J_hi) break;  // (only for inconsistent, over-capacity inputs)
-            jc += 32;
-            e_cur = e_next;
-            load_chunk();
-        }
-        __syncwarp();
-        const int64_t m = m0 + lane;
-        const bool valid = m <= m_last;
-        double2 q = make_double2(0.0, 0.0);
-        int64_t mb = 0;  // new_starts of m's edge
-        int me = 0;      // m's edge
-        if ((W >> lane) & 1u) {
-            q = make_double2(S.x[lane], S.y[lane]);
-            mb = S.nsb[lane];
-            me = S.e[lane];
-        } else if (valid) {
-            const unsigned above = lane == 31 ? 0u : (W & (0xfffffffeu << lane));
-            const int os = above ? __ffs(above) - 1 : 32;
-            const unsigned lo = W & ((1u << lane) - 1u);
-            double2 a;
-            int64_t ag;
-            if (lo) {
-                const int ps = 31 - __clz(lo);
-                a = make_double2(S.x[ps], S.y[ps]);
-                ag = S.g[ps];
-            } else {
-                a = make_double2(cpx, cpy);
-                ag = cpg;
-            }
-            const int64_t og = S.g[os];
-            q = interp_piece(a, make_double2(S.x[os], S.y[os]), (int)(m - ag), (int)(og - ag));
-            mb = S.nsb[os];
-            me = S.e[os];
-        }
-        if (!dry && valid) HB_ST_STREAM(out + m, q);
-        if (splat) {
-            double q0x = __shfl_up_sync(full, q.x, 1), q0y = __shfl_up_sync(full, q.y, 1);
-            if (lane == 0) { q0x = cq.x; q0y = cq.y; }
-            cq = make_double2(__shfl_sync(full, q.x, 31), __shfl_sync(full, q.y, 31));
-            const int64_t lm = m - mb;
-            const bool seg = !dry && valid && lm >= 1;
-            // (clamped: after a capacity clamp, empty edges can leave stale slots)
-            me = me < 0 ? 0 : (me > (int)n_edges - 1 ? (int)n_edges - 1 : me);
-            const int grp = seg && group ? group[me] : 0;
-            const int32_t w = seg && weight ? weight[me] : 1;
-            bin_or_splat<int32_t>(seg, q0x, q0y, q.x, q.y, lm == 1 ? 0 : 1, w, grp, hist, plane,
-                                  nv, nu, status, tiles);
-        }
-        // the tile's last kept input is the next tile's predecessor unless
-        // the chunk scan finds a later one
-        if (W) {
-            const int ls = 31 - __clz(W);
-            cpx = S.x[ls];
-            cpy = S.y[ls];
-            cpg = S.g[ls];
-        }
-        __syncwarp();
-    }
-}
-
 // ---------------------------------------------------------------------------
 // Ring emit: input-major, each input read once.  A warp owns an edge-aligned
 // range of whole polylines (balanced by input points, like the Laplacian +
@@ -527,10 +197,8 @@ emit_flat_kernel(const double2 *__restrict__ pts, const int64_t *__restrict__ st
 // The previous output of a tile's lane 0 is carried in registers.  Output
 // indices inside the range are 32-bit (a range holds < 2^31 outputs).
 //
-// Compared with the output-tiled emit_flat_kernel, no chunk is scanned
-// twice and no slot table is rebuilt per tile: ~2x fewer instructions per
-// output (that kernel issues ~560 warp instructions per 32 outputs at 73 %
-// issue utilisation).
+// (An output-tiled variant, which rescanned chunks and rebuilt a slot table
+// per 32 outputs, issued ~2x the instructions per output; removed.)
 constexpr int kRing = 128;  // slots per warp (power of two)
 struct EmitRing {
     double2 q[kRing];
@@ -861,20 +529,6 @@ int hb_splat(const double *pts, const int64_t *starts, int64_t n_edges, int64_t 
     return check_launch("hb_splat");
 }
 
-int hb_splat_f32(const double *pts, const int64_t *starts, int64_t n_edges, int64_t n_pts,
-                 const int32_t *group, const float *weight, float *hist, int nbins, int nv,
-                 int nu, int32_t *status, void *stream) {
-    if (n_edges < 0 || n_pts < 0 || nbins < 1 || nv < 1 || nu < 1 || nv > kMaxDim || nu > kMaxDim || !hist || !status ||
-        (n_edges > 0 && (!pts || !starts || !group)))
-        return set_error(HB_EINVAL, "hb_splat_f32: bad arguments");
-    if (n_edges == 0 || n_pts == 0) return HB_OK;
-    splat_kernel<float><<<persistent_grid(splat_kernel<float>, n_edges), kStreamBlock, 0,
-                          as_stream(stream)>>>(
-        reinterpret_cast<const double2 *>(pts), starts, n_edges, group, weight, hist,
-        (int64_t)nv * nu, nv, nu, status, hb_tiles{}, 0);
-    return check_launch("hb_splat_f32");
-}
-
 int hb_resample_count(const double *pts, const int64_t *starts, int64_t n_edges,
                       double delta, int64_t *counts, int32_t *pos, void *stream) {
     if (n_edges < 0 || !(delta > 0) || (n_edges > 0 && (!pts || !starts || !counts || !pos)))
@@ -926,9 +580,6 @@ int hb_resample_emit_cap(const double *pts, const int64_t *starts, int64_t n_edg
         (counts && (nv < 1 || nu < 1 || nv > kMaxDim || nu > kMaxDim)))
         return set_error(HB_EINVAL, "hb_resample_emit: bad arguments");
     if (n_edges == 0 || n_pts == 0) return HB_OK;
-#if defined(HB_EMIT_PER_EDGE)
-    emit_kernel<<<persistent_grid(emit_kernel, n_edges), kStreamBlock, 0, as_stream(stream)>>>(
-#elif !defined(HB_EMIT_FLAT)
     static void *work_of[64] = {};  // the counter's address per device
     int dev = 0;
     if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64)
@@ -940,12 +591,6 @@ int hb_resample_emit_cap(const double *pts, const int64_t *starts, int64_t n_edg
         return check_launch("hb_resample_emit(memset)", 0);
     emit_ring_kernel<<<persistent_grid(emit_ring_kernel, (n_pts + 31) / 32), kStreamBlock, 0,
                        as_stream(stream)>>>(
-#else
-    // work items: output tiles (the output total is on the device; the input
-    // count bounds it well enough for the grid size)
-    emit_flat_kernel<<<persistent_grid(emit_flat_kernel, (n_pts + 31) / 32), kStreamBlock, 0,
-                       as_stream(stream)>>>(
-#endif
         reinterpret_cast<const double2 *>(pts), starts, n_edges, pos, new_starts,
         reinterpret_cast<double2 *>(out), group, weight, counts, (int64_t)nv * nu, nv, nu,
         status, tiles ? *tiles : hb_tiles{}, (counts && tiles) ? 1 : 0, out_capacity);

@@ -8,25 +8,36 @@ initial point count, splats it into a local int32 group histogram, and one
 all-reduce per iteration sums the histograms; integer sums are associative,
 so every rank then holds the bit-exact global histogram and smooths it
 redundantly. Metrics are summed at the end; polylines are
-gathered to every rank only when the caller materialises them.
+gathered to rank 0 only when the caller materialises them.
 
 Everything here also runs on CPU tensors with the gloo backend (tests).
 """
 
 from __future__ import annotations
 
+import os
+
 import numpy as np
 import torch
 import torch.distributed as dist
 
-__all__ = ["rank_world", "shard_edges", "all_reduce_sum", "sum_host_arrays",
-           "gather_polylines"]
+__all__ = ["rank_world", "distributed", "shard_edges", "all_reduce_sum", "all_reduce_max",
+           "sum_host_arrays", "gather_polylines"]
 
 
 def rank_world(group=None) -> tuple[int, int]:
     if not (dist.is_available() and dist.is_initialized()):
         return 0, 1
     return dist.get_rank(group), dist.get_world_size(group)
+
+
+def distributed(group=None) -> bool:
+    """Whether the collective path runs: more than one rank, or a 1-rank
+    process group with HB_FORCE_DIST=1 (so the NCCL branch is exercised on a
+    single GPU: an all-reduce over one rank is the identity)."""
+    if not (dist.is_available() and dist.is_initialized()):
+        return False
+    return dist.get_world_size(group) > 1 or os.environ.get("HB_FORCE_DIST") == "1"
 
 
 def shard_edges(point_counts: np.ndarray, world: int) -> list[tuple[int, int]]:
@@ -59,6 +70,15 @@ def all_reduce_sum(t: torch.Tensor, group=None) -> torch.Tensor:
     return t
 
 
+def all_reduce_max(t: torch.Tensor, group=None) -> torch.Tensor:
+    """Element-wise maximum of a small host tensor over ranks (status words,
+    bounds spans): every rank gets the same value and takes the same branch."""
+    dev = _backend_device(group)
+    d = t.to(dev)
+    dist.all_reduce(d, op=dist.ReduceOp.MAX, group=group)
+    return d.cpu()
+
+
 def _backend_device(group=None) -> torch.device:
     backend = dist.get_backend(group)
     if backend == "nccl":
@@ -68,8 +88,7 @@ def _backend_device(group=None) -> torch.device:
 
 def sum_host_arrays(arrays: list[np.ndarray], group=None) -> list[np.ndarray]:
     """Element-wise sum of small host arrays over ranks (one collective)."""
-    _, world = rank_world(group)
-    if world == 1:
+    if not distributed(group):
         return arrays
     dev = _backend_device(group)
     out = []
@@ -80,32 +99,37 @@ def sum_host_arrays(arrays: list[np.ndarray], group=None) -> list[np.ndarray]:
     return out
 
 
-def gather_polylines(points: torch.Tensor, starts: torch.Tensor, group=None):
-    """All ranks' packed polylines concatenated in rank order (= edge order).
-
-    Returns host numpy ``(world_points (N,2) f64, starts (E+1) i64)``."""
-    _, world = rank_world(group)
-    if world == 1:
+def gather_polylines(points: torch.Tensor, starts: torch.Tensor, group=None, root: int = 0):
+    """Every rank's packed polylines concatenated in rank order (= edge
+    order) on ``root`` only: the point counts are all-gathered
+    (one tiny collective), then each rank sends its exact-size arrays to the
+    root point to point.  Returns host numpy ``(world_points (N,2) f64,
+    starts (E+1) i64)`` on the root and ``None`` elsewhere."""
+    rank, world = rank_world(group)
+    if not distributed(group):
         return points.cpu().numpy(), starts.cpu().numpy()
     dev = _backend_device(group)
-    pts = points.to(dev)
-    st = starts.to(dev)
-    sizes = torch.tensor([pts.shape[0], st.shape[0] - 1], dtype=torch.int64, device=dev)
+    sizes = torch.tensor([points.shape[0], starts.shape[0] - 1], dtype=torch.int64, device=dev)
     all_sizes = [torch.empty_like(sizes) for _ in range(world)]
     dist.all_gather(all_sizes, sizes, group=group)
     all_sizes = [tuple(int(v) for v in s.cpu()) for s in all_sizes]
-    max_n = max(s[0] for s in all_sizes)
-    max_e = max(s[1] for s in all_sizes)
-    pad_p = torch.zeros((max_n, 2), dtype=pts.dtype, device=dev)
-    pad_p[: pts.shape[0]] = pts
-    pad_s = torch.zeros(max_e + 1, dtype=st.dtype, device=dev)
-    pad_s[: st.shape[0]] = st
-    gp = [torch.empty_like(pad_p) for _ in range(world)]
-    gs = [torch.empty_like(pad_s) for _ in range(world)]
-    dist.all_gather(gp, pad_p, group=group)
-    dist.all_gather(gs, pad_s, group=group)
+    groot = root if group is None else dist.get_global_rank(group, root)
+    if rank != root:
+        if all_sizes[rank][0]:
+            dist.send(points.contiguous().to(dev), dst=groot, group=group)
+        dist.send(starts.contiguous().to(dev), dst=groot, group=group)
+        return None
     pieces, st_pieces, base = [], [np.zeros(1, dtype=np.int64)], 0
-    for (n, e), p, s in zip(all_sizes, gp, gs):
+    for r, (n, e) in enumerate(all_sizes):
+        if r == root:
+            p, s = points.to(dev), starts.to(dev)
+        else:
+            src = r if group is None else dist.get_global_rank(group, r)
+            p = torch.empty((n, 2), dtype=points.dtype, device=dev)
+            if n:
+                dist.recv(p, src=src, group=group)
+            s = torch.empty(e + 1, dtype=starts.dtype, device=dev)
+            dist.recv(s, src=src, group=group)
         pieces.append(p[:n].cpu().numpy())
         st_pieces.append(s[1: e + 1].cpu().numpy() + base)
         base += n

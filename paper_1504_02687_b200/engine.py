@@ -33,7 +33,8 @@ import torch
 from . import _native as N
 from .model import BundleConfig
 
-__all__ = ["BundleEngine", "box_widths", "sample_counts", "IterationRecord"]
+__all__ = ["BundleEngine", "box_widths", "sample_counts", "IterationRecord", "WeightPlan",
+           "weight_plan", "ordered_plan", "CapacityExceeded", "InexactHistogram"]
 
 MIN_STEP = 0.25  # bundler.py:48
 
@@ -120,22 +121,111 @@ class IterationRecord:
     seconds: float = 0.0
 
 
+class InexactHistogram(RuntimeError):
+    """The integer fast path stopped equalling the reference's float32 sums
+    (a cell's layer sum outgrew 2^24 quanta); the run is redone ordered."""
+
+
 @dataclass
 class WeightPlan:
-    """How edge weights reach the histogram."""
+    """How edge weights reach the histogram.
 
-    kind: str                      # "unit" | "int" | "float"
+    The reference adds ``layer_w[e, l] = fl32(w_e) * M[l, b_e]`` into float32
+    buffers one hit at a time (``bundler.py:345-346``, ``raster.py:70-94``).
+
+    * ``"unit"`` / ``"int"``: every layer weight is an exact float32 multiple
+      of ``quantum``, so while each cell's partial sums stay below
+      ``limit = 2^24 * quantum`` the float32 sums are exact and order-free:
+      per-group int32 counts mixed once (``hb_smooth``) equal them bit for bit.
+      ``hb_exact_check`` guards the limit every iteration.
+    * ``"ordered"``: anything else (repulsive -alpha/(B-1) matrices, fractional
+      weights): the reference's own summation order, ``hb_accumulate_ordered``.
+
+    Decided once from the WHOLE graph, so every rank of a sharded run takes
+    the same path (``slice`` gives a rank its edges' arrays).
+    """
+
+    kind: str                      # "unit" | "int" | "ordered"
     int_w: np.ndarray | None = None
     f32_w: np.ndarray | None = None
+    quantum: float = 1.0
+    abs_matrix: np.ndarray | None = None   # (B,B) float64 |M|; None = identity
+
+    @property
+    def limit(self) -> float:
+        return float(2 ** 24) * self.quantum
+
+    def slice(self, lo: int, hi: int) -> "WeightPlan":
+        return WeightPlan(self.kind,
+                          None if self.int_w is None else self.int_w[lo:hi],
+                          None if self.f32_w is None else self.f32_w[lo:hi],
+                          self.quantum, self.abs_matrix)
 
 
-def weight_plan(weights: np.ndarray) -> WeightPlan:
-    w32 = weights.astype(np.float32)
-    if np.all(w32 == 1.0):
-        return WeightPlan("unit")
-    if np.all(np.floor(w32) == w32) and np.all(np.abs(w32) < 2**24):
-        return WeightPlan("int", int_w=w32.astype(np.int32))
-    return WeightPlan("float", f32_w=w32)
+
+def ordered_plan(weights: np.ndarray) -> WeightPlan:
+    """The reference's summation order whatever the weights."""
+    w32 = np.asarray(weights).astype(np.float32)
+    return WeightPlan("ordered", f32_w=None if np.all(w32 == 1.0) else w32)
+
+
+def _lowest_bit(x: np.ndarray) -> float:
+    """Largest power of two dividing every non-zero entry of ``x`` (floats)."""
+    x = np.abs(np.asarray(x, dtype=np.float64))
+    x = x[x > 0]
+    if x.size == 0:
+        return 1.0
+    m, e = np.frexp(x)                      # x = m * 2^e, m in [0.5, 1)
+    mi = (m * 2.0 ** 53).astype(np.int64)   # exact integer significand
+    low = mi & -mi                          # lowest set bit of the significand
+    tz = np.log2(low.astype(np.float64)).astype(np.int64)
+    return float(2.0 ** int((e - 53 + tz).min()))
+
+
+def _sig_bits(x: np.ndarray) -> int:
+    """Most significand bits any non-zero entry of ``x`` needs."""
+    x = np.abs(np.asarray(x, dtype=np.float64))
+    x = x[x > 0]
+    if x.size == 0:
+        return 1
+    m, _ = np.frexp(x)
+    mi = (m * 2.0 ** 53).astype(np.int64)
+    low = mi & -mi
+    return int((53 - np.log2(low.astype(np.float64)).astype(np.int64)).max())
+
+
+def weight_plan(weights: np.ndarray, matrix: np.ndarray | None = None,
+                n_points: int = 0) -> WeightPlan:
+    """Pick the histogram path for the whole graph (see :class:`WeightPlan`).
+
+    ``n_points`` (initial sample points) bounds the hits per cell for the
+    int32 overflow check of non-unit integer weights (the buffers hold at
+    most ~4x that many points)."""
+    w32 = np.asarray(weights).astype(np.float32)
+    mat = (np.eye(1, dtype=np.float32) if matrix is None
+           else np.ascontiguousarray(matrix, dtype=np.float32))
+    nb = mat.shape[0]
+    identity = np.array_equal(mat, np.eye(nb, dtype=np.float32))
+    absm = None if identity else np.abs(mat.astype(np.float64))
+    ordered = ordered_plan(w32)
+    if w32.size and (not np.all(np.isfinite(w32)) or np.any(w32 < 0)):
+        return ordered
+    unit = bool(np.all(w32 == 1.0))
+    if not unit and not (np.all(np.floor(w32) == w32) and np.all(w32 < 2 ** 24)):
+        return ordered
+    wmax = float(w32.max()) if w32.size else 1.0
+    # every product fl32(w * M[l,b]) exact: the weights' bit span plus the
+    # matrix entries' significand bits fit float32's 24
+    qw = 1.0 if unit else _lowest_bit(w32)
+    span_w = 1 if unit else int(math.floor(math.log2(max(wmax, qw) / qw))) + 1
+    if span_w + _sig_bits(mat) > 24:
+        return ordered
+    if not unit and wmax * (4.0 * n_points + (1 << 20)) >= 2.0 ** 31:
+        return ordered  # int32 counts could wrap
+    q = qw * _lowest_bit(mat)
+    if unit:
+        return WeightPlan("unit", quantum=q, abs_matrix=absm)
+    return WeightPlan("int", int_w=w32.astype(np.int32), quantum=q, abs_matrix=absm)
 
 
 class BundleEngine:
@@ -145,7 +235,12 @@ class BundleEngine:
     ``transform.world_to_grid`` of the node positions), ``groups`` its bins.
     ``reduce_hist`` (optional) is called with the int32/float32 group
     histogram tensor after the splat; the distributed driver passes an
-    all-reduce here.
+    all-reduce here.  ``reduce_flags`` (optional) takes a small int64
+    tensor and returns its element-wise maximum over ranks, so every rank
+    takes the same decision on the run's status (bounds, capacity retry,
+    exactness) and raises together.  ``workers`` is the reference's
+    partition count (``_parallel.partition_ranges``): it only changes results
+    on the ordered path, exactly as it does in the reference.
     """
 
     def __init__(self, src: np.ndarray, dst: np.ndarray, groups: np.ndarray,
@@ -153,7 +248,8 @@ class BundleEngine:
                  cfg: BundleConfig, *, fixed_step: bool = False,
                  offset_disp: np.ndarray | None = None, device=None,
                  reduce_hist=None, capacity_factor: float = 2.0,
-                 starts: torch.Tensor | None = None):
+                 starts: torch.Tensor | None = None, workers: int = 1,
+                 reduce_flags=None, sync_free: bool = True):
         N.lib()  # fail loudly if the native library is missing
         if not torch.cuda.is_available():
             raise N.NativeError("paper_1504_02687_b200 needs a CUDA device (sm_100a); "
@@ -162,6 +258,7 @@ class BundleEngine:
         self.cfg = cfg
         self.fixed_step = bool(fixed_step)
         self.reduce_hist = reduce_hist
+        self.reduce_flags = reduce_flags
         self.nv, self.nu = int(shape[0]), int(shape[1])
         self.matrix = np.ascontiguousarray(matrix, dtype=np.float32)
         self.nbins = int(self.matrix.shape[0])
@@ -190,12 +287,20 @@ class BundleEngine:
         self.starts_alt = torch.empty_like(self.starts)
         self.ecounts = torch.empty(max(E, 1), dtype=torch.int64, device=dev)
         self.groups = upload(np.asarray(groups, dtype=np.int32), dev)
+        self.plan = weights
         self.wkind = weights.kind
         self.wint = upload(weights.int_w, dev) if weights.kind == "int" else None
-        self.wf32 = upload(weights.f32_w, dev) if weights.kind == "float" else None
+        self.wf32 = (upload(weights.f32_w, dev) if weights.kind == "ordered"
+                     and weights.f32_w is not None else None)
         mat_is_identity = np.array_equal(self.matrix, np.eye(B, dtype=np.float32))
         self.mat_dev = None if mat_is_identity else upload(self.matrix, dev)
-        hdtype = torch.float32 if self.wkind == "float" else torch.int32
+        self.absm_dev = (None if weights.abs_matrix is None
+                         else upload(np.ascontiguousarray(weights.abs_matrix, np.float64), dev))
+        self.nparts = max(1, min(int(workers), E)) if E else 1
+        self.hoff = None         # ordered path: hit offsets + workspaces
+        self.hits_ws = None
+        self.ord_ws = None
+        hdtype = torch.float32 if self.wkind == "ordered" else torch.int32
         self.hist = torch.empty((B, self.nv, self.nu), dtype=hdtype, device=dev)
         self.field = torch.empty((B, self.nv, self.nu), dtype=torch.float32, device=dev)
         # quad advection field (hb_grad_field), 48 B per cell, whenever memory
@@ -230,7 +335,7 @@ class BundleEngine:
         self.tile_mode = -1
         # HB_SPLAT_MODE=auto|table|tiles|direct forces a path (tests cover all three)
         smode = os.environ.get("HB_SPLAT_MODE", "auto")
-        if self.wkind != "float" and smode != "direct":
+        if self.wkind != "ordered" and smode != "direct":
             geo = N.HbTiles()
             ent = ctypes.c_int64(0)
             budget = min(8 << 30, torch.cuda.mem_get_info(dev)[0] // 8)
@@ -263,13 +368,22 @@ class BundleEngine:
         # kernels read it from `starts`, the emit checks it against the
         # buffer), so no host read separates the iterations.  The buffers get
         # headroom; a run that outgrows them is redone in the synchronous mode.
-        self.async_n = (self.tile_mode != 0 and self.wkind != "float"
+        self.async_n = (sync_free and self.tile_mode != 0 and self.wkind != "ordered"
                         and os.environ.get("HB_SYNC_FREE", "1") != "0")
         self._n_known = True
         self._init = None
         if self.async_n:
+            # headroom for the sync-free resample: the kernels index points in
+            # 32 bits (< 2^31) and the buffers must fit the device; without
+            # room for 4x growth the run is synchronous instead
             f = float(os.environ.get("HB_ASYNC_CAP_FACTOR", "4"))  # (tests shrink it)
-            self._ensure_capacity(int(f * self.n_pts) + (1 << 20 if f >= 1 else 0))
+            want = int(f * self.n_pts) + (1 << 20 if f >= 1 else 0)
+            free = torch.cuda.mem_get_info(dev)[0]
+            extra = max(want - self.cap, 0) * (2 * 16 + 4) * 5 // 4
+            if want * 5 // 4 >= (1 << 31) - 1 or extra > free * 0.6:
+                self.async_n = False
+            else:
+                self._ensure_capacity(want)
         self.lap_passes = int(cfg.laplacian_passes)
         # one-pass advect + Laplacian + count (hb_advect_laplacian_count):
         # bit-identical, measured slower (config 4: 9.23 ms vs 5.29 + 2.41 ms)
@@ -295,6 +409,11 @@ class BundleEngine:
         if offset_disp is not None:
             od = upload(offset_disp, dev)
             N.call("hb_offset", ptr(self.pts), ptr(self.starts), E, ptr(od), s)
+        # _check_bounds (raster.py:57-67) of the first accumulate.  Later
+        # iterations cannot leave the grid: advection clamps moved points to
+        # [1, dim-2] and resampling / Laplacian smoothing only form convex
+        # combinations, so the kernels' cell checks are a backstop.
+        self._raise_if_out_of_bounds()
         self.iteration = 0
         self._tab_on = True       # segment-key table in use for the next emit
         self._tab_segments = 0    # segments the last table pass saw
@@ -335,10 +454,8 @@ class BundleEngine:
         """Straight splat of the current points (iteration 0 / float weights);
         with tiles it also takes the per-tile census for the next plan."""
         E, B, nv, nu = self.n_edges, self.nbins, self.nv, self.nu
-        if self.wkind == "float":
-            self._k("hb_splat_f32", ptr(self.pts), ptr(self.starts), E, self.n_pts,
-                    ptr(self.groups), ptr(self.wf32), ptr(self.hist), B, nv, nu,
-                    ptr(self.status), s)
+        if self.wkind == "ordered":
+            self._accumulate_ordered(s)
             return
         # Straight initial polylines have no duplicate segments, so the key
         # table would only add its expansion: splat directly (tile mode still
@@ -349,6 +466,29 @@ class BundleEngine:
             sink = ctypes.byref(self.tiles_census)
         self._k("hb_splat", ptr(self.pts), ptr(self.starts), E, self.n_pts, ptr(self.groups),
                 ptr(self.wint), ptr(self.hist), B, nv, nu, ptr(self.status), sink, s)
+
+    def _accumulate_ordered(self, s) -> None:
+        """The reference's float32 histogram in its own summation order
+        (raster.py:70-94): hit offsets, one host read of the hit total to
+        size the workspace, then records -> stable sort by cell -> fold."""
+        E, B, nv, nu = self.n_edges, self.nbins, self.nv, self.nu
+        n = self.n_pts
+        if self.hoff is None or self.hoff.numel() < n + 1:
+            self.hoff = torch.empty(int((n + 1) * 1.25) + 1024, dtype=torch.int64, device=self.dev)
+        hb = int(N.lib().hb_hits_workspace_bytes(n))
+        if self.hits_ws is None or self.hits_ws.numel() < hb:
+            self.hits_ws = torch.empty(int(hb * 1.25) + 4096, dtype=torch.uint8, device=self.dev)
+        self._k("hb_hits_count", ptr(self.pts), ptr(self.starts), E, n, ptr(self.hoff),
+                ptr(self.hits_ws), self.hits_ws.numel(), s)
+        n_hits = int(download(self.hoff[n:n + 1])[0])
+        ob = int(N.lib().hb_ordered_workspace_bytes(n_hits, nv, nu, self.nparts))
+        if self.ord_ws is None or self.ord_ws.numel() < ob:
+            self.ord_ws = None
+            self.ord_ws = torch.empty(int(ob * 1.25) + 4096, dtype=torch.uint8, device=self.dev)
+        self._k("hb_accumulate_ordered", ptr(self.pts), ptr(self.starts), E, ptr(self.hoff), n,
+                n_hits, self.nparts, 0, E, ptr(self.wf32), self._emit_groups(),
+                ptr(self.mat_dev), B, nv, nu, ptr(self.hist), ptr(self.status),
+                ptr(self.ord_ws), self.ord_ws.numel(), s)
 
     def _ensure_records(self, n: int) -> None:
         if n <= self.t_rec.numel():
@@ -384,7 +524,7 @@ class BundleEngine:
             # resample (bundler.py:353-354): the counts/codes came out of the
             # previous iteration's fused advect pass; scan, size, then emit
             # fused with the splat (:355-356)
-            fused = self.wkind != "float"
+            fused = self.wkind != "ordered"
             tiles = None
             if fused and self.tile_mode == 0:
                 self._k("hb_tiles_plan", ctypes.byref(self.tiles), ptr(self.t_total), s)
@@ -460,11 +600,7 @@ class BundleEngine:
         s = stream_ptr()
         E, B, nv, nu = self.n_edges, self.nbins, self.nv, self.nu
         ev0 = self._ev_open
-        is_int = self.wkind != "float"
-        self._k("hb_smooth", ptr(self.hist) if is_int else None,
-                None if is_int else ptr(self.hist), ptr(self.mat_dev), B, nv, nu,
-                self.radii.data_ptr(), int(self.radii.numel()), ptr(self.field),
-                ptr(self.smooth_ws), self.smooth_ws.numel(), ptr(self.peak), s)
+        self._smooth(s)
         h_i = cfg.lambda_ ** i * cfg.h_max  # bundler.py:360, Python float power
         # advect -> Laplacian (-> next iteration's resample count), in place
         last = i == self.iters - 1
@@ -533,18 +669,17 @@ class BundleEngine:
             self.run()
             return download_pinned(self.world_points_nodes(origin, cell, node_pos, sources,
                                                            targets)), self.records
-        if self.async_n and self._init is None and self.iteration == 0:
+        if self._retryable() and self._init is None and self.iteration == 0:
             self.keep_initial_state()
         try:
             while self.iteration < self.iters - 1:
                 self.step()
             out = self._last_iteration_streamed(origin, cell, node_pos, sources, targets, chunks)
             return out, self.finish_metrics()
-        except CapacityExceeded as ex:
-            self.status.zero_()
-            self.async_n = False
-            self.reset()
-            self._ensure_capacity(int(ex.needed * 1.25))
+        except (CapacityExceeded, InexactHistogram) as ex:
+            if self._init is None:
+                raise
+            self._retry(ex)
             return self.run_streamed(origin, cell, node_pos, sources, targets, chunks)
 
     def _last_iteration_streamed(self, origin, cell, node_pos, sources, targets, chunks):
@@ -552,11 +687,7 @@ class BundleEngine:
         self.step_splat()
         i, cfg = self.iteration, self.cfg
         ev0 = self._ev_open
-        is_int = self.wkind != "float"
-        self._k("hb_smooth", ptr(self.hist) if is_int else None,
-                None if is_int else ptr(self.hist), ptr(self.mat_dev), B, nv, nu,
-                self.radii.data_ptr(), int(self.radii.numel()), ptr(self.field),
-                ptr(self.smooth_ws), self.smooth_ws.numel(), ptr(self.peak), s)
+        self._smooth(s)
         if self.gfield is not None:
             self._k("hb_grad_field", ptr(self.field), B, nv, nu, ptr(self.gfield), s)
         h_i = cfg.lambda_ ** i * cfg.h_max
@@ -591,6 +722,21 @@ class BundleEngine:
         world.record_stream(copy)
         return host.numpy()
 
+    def _smooth(self, s) -> None:
+        """Exactness guard of the integer path (the global histogram), then
+        mix + 3 box passes + layer peaks."""
+        B, nv, nu = self.nbins, self.nv, self.nu
+        if self.wkind == "ordered":  # layer weights already applied, float32
+            self._k("hb_smooth", None, ptr(self.hist), None, B, nv, nu,
+                    self.radii.data_ptr(), int(self.radii.numel()), ptr(self.field),
+                    ptr(self.smooth_ws), self.smooth_ws.numel(), ptr(self.peak), s)
+            return
+        self._k("hb_exact_check", ptr(self.hist), ptr(self.absm_dev), B, nv, nu,
+                float(self.plan.limit), ptr(self.status), s)
+        self._k("hb_smooth", ptr(self.hist), None, ptr(self.mat_dev), B, nv, nu,
+                self.radii.data_ptr(), int(self.radii.numel()), ptr(self.field),
+                ptr(self.smooth_ws), self.smooth_ws.numel(), ptr(self.peak), s)
+
     def _close_iteration(self, ev0, h_i: float) -> IterationRecord:
         ev1 = torch.cuda.Event(enable_timing=True)
         ev1.record()
@@ -610,6 +756,7 @@ class BundleEngine:
         """Back to iteration 0 on the remembered initial points (device copies
         only, stream-ordered, no host sync)."""
         pts0, starts0, n0 = self._init
+        self._cb_seen = -1
         self._ensure_capacity(n0)
         self.pts[:n0].copy_(pts0)
         self.starts.copy_(starts0)
@@ -625,14 +772,66 @@ class BundleEngine:
         self.m_ntot.zero_()
         self.status.zero_()
 
+    def _reduce_max(self, vals: list) -> list:
+        """Element-wise maximum over ranks (identity on one rank)."""
+        if self.reduce_flags is None:
+            return vals
+        t = torch.tensor(vals, dtype=torch.float64)
+        return [float(v) for v in self.reduce_flags(t)]
+
+    def _raise_if_out_of_bounds(self) -> None:
+        """The reference's bounds check on the current points, with its
+        message (raster.py:57-67); the span is taken over all ranks."""
+        n = self.sync_count()
+        if self.n_edges == 0 or n == 0:
+            span = [math.inf, math.inf, -math.inf, -math.inf]
+        else:
+            scratch = torch.empty(4, dtype=torch.int64, device=self.dev)
+            out = torch.empty(4, dtype=torch.float64, device=self.dev)
+            N.call("hb_point_span", ptr(self.pts), n, ptr(scratch), ptr(out), stream_ptr())
+            span = [float(v) for v in download(out)]
+        xmin, ymin, nxmax, nymax = self._reduce_max(
+            [-span[0], -span[1], span[2], span[3]])
+        xmin, ymin, xmax, ymax = -xmin, -ymin, nxmax, nymax
+        if not math.isfinite(xmin):
+            return  # no points anywhere
+        width, height = self.nu, self.nv
+        if xmin <= -0.5 or ymin <= -0.5 or xmax >= width - 0.5 or ymax >= height - 0.5:
+            raise ValueError(
+                f"sample out of bounds: points span ({xmin:.3f}, {ymin:.3f}) to "
+                f"({xmax:.3f}, {ymax:.3f}) on a {width}x{height} grid")
+
+    def _switch_to_ordered(self) -> None:
+        """Leave the integer path for the reference's summation order."""
+        p = self.plan
+        w = None if p.kind == "unit" else p.int_w.astype(np.float32)
+        self.plan = WeightPlan("ordered", f32_w=w)
+        self.wkind = "ordered"
+        self.wint = None
+        self.wf32 = None if w is None else upload(w, self.dev)
+        self.hist = torch.empty((self.nbins, self.nv, self.nu), dtype=torch.float32,
+                                device=self.dev)
+        self.tiles, self.tile_mode = None, -1
+        self.t_tab = self.t_rec = None
+        self.async_n = False
+
     def finish_metrics(self) -> list[IterationRecord]:
-        """Synchronise once and fill moved/disp/used/seconds of all records."""
+        """Synchronise once and fill moved/disp/used/seconds of all records.
+
+        The status word is agreed over ranks first, so a retry (capacity,
+        exactness) or a bounds error happens on every rank together."""
         torch.cuda.current_stream().synchronize()
         st = int(download(self.status)[0])
-        if st & 4:
-            raise CapacityExceeded(int(download(self.m_ntot).max()))
-        if st & 1:
+        oob, cap, inexact = self._reduce_max([st & 1, st & 4, st & 8])
+        if oob:
+            self._raise_if_out_of_bounds()
             raise ValueError("sample out of bounds: a polyline point left the grid")
+        if cap:
+            raise CapacityExceeded(int(download(self.m_ntot).max()))
+        if inexact:
+            raise InexactHistogram(
+                "a histogram cell outgrew 2^24 weight quanta: the reference's float32 "
+                "sums round there")
         if any(r.n_points < 0 for r in self.records):
             ntot = download(self.m_ntot)
             for r in self.records:
@@ -649,24 +848,49 @@ class BundleEngine:
             r.seconds = a.elapsed_time(b) / 1e3
         return self.records
 
+    def _retryable(self) -> bool:
+        return self.async_n or self.wkind != "ordered"
+
+    def _retry(self, ex) -> None:
+        """Back to iteration 0 for a synchronous (capacity) or ordered
+        (exactness) rerun; every rank gets here together."""
+        seen = getattr(self, "_cb_seen", -1)
+        self.status.zero_()
+        if isinstance(ex, CapacityExceeded):
+            # stay sync-free with room for what the run needed (the next
+            # reset()+run() reuses it); after repeated overflows, or beyond
+            # the 32-bit point index, run synchronously instead
+            self._cap_retries = getattr(self, "_cap_retries", 0) + 1
+            want = int(ex.needed * 1.25) + (1 << 20)
+            if self._cap_retries > 2 or want * 5 // 4 >= (1 << 31) - 1:
+                self.async_n = False
+                want = int(ex.needed * 1.25)
+            self.reset()
+            self._ensure_capacity(want)
+        else:
+            self._switch_to_ordered()
+            self.reset()
+        self._cb_seen = seen
+
     def run(self, on_iteration=None) -> list[IterationRecord]:
-        if self.async_n and self._init is None and self.iteration == 0:
-            self.keep_initial_state()  # for the (rare) capacity retry
+        """All remaining iterations.  ``on_iteration(engine)`` runs after each
+        one; after a retry it is called again only for iterations it has not
+        seen (the rerun reproduces the earlier ones exactly)."""
+        if self._retryable() and self._init is None and self.iteration == 0:
+            self.keep_initial_state()  # for the (rare) capacity / exactness retry
         start = self.iteration
+        seen = getattr(self, "_cb_seen", -1)
         try:
             while self.iteration < self.iters:
                 self.step()
-                if on_iteration is not None:
+                if on_iteration is not None and self.iteration - 1 > seen:
                     on_iteration(self)
+                    seen = self._cb_seen = self.iteration - 1
             return self.finish_metrics()
-        except CapacityExceeded as ex:
+        except (CapacityExceeded, InexactHistogram) as ex:
             if start != 0 or self._init is None:
                 raise
-            # outgrew the headroom: redo the run synchronously with room to spare
-            self.status.zero_()
-            self.async_n = False
-            self.reset()
-            self._ensure_capacity(int(ex.needed * 1.25))
+            self._retry(ex)
             return self.run(on_iteration)
 
     # ------------------------------------------------------------------

@@ -61,11 +61,33 @@ def _pack_world(sampled: Sequence[SampledEdge], transform: GridTransform):
     return transform.world_to_grid(pts), starts
 
 
+def _accumulate_ordered(dpts, dst, E, n, grp, w32, mat, nb, nv, nu, workers, status):
+    """The reference's float32 fold order (raster.py:85-94) on the device."""
+    dev = dpts.device
+    s = stream_ptr()
+    hoff = torch.empty(n + 1, dtype=torch.int64, device=dev)
+    hws = torch.empty(int(N.lib().hb_hits_workspace_bytes(n)), dtype=torch.uint8, device=dev)
+    N.call("hb_hits_count", ptr(dpts), ptr(dst), E, n, ptr(hoff), ptr(hws), hws.numel(), s)
+    n_hits = int(hoff[n].item())
+    parts = max(1, min(int(workers), E)) if E else 1
+    ows = torch.empty(int(N.lib().hb_ordered_workspace_bytes(n_hits, nv, nu, parts)),
+                      dtype=torch.uint8, device=dev)
+    out = torch.empty((nb, nv, nu), dtype=torch.float32, device=dev)
+    N.call("hb_accumulate_ordered", ptr(dpts), ptr(dst), E, ptr(hoff), n, n_hits, parts, 0, E,
+           ptr(w32), ptr(grp) if nb > 1 else None, ptr(mat), nb, nv, nu, ptr(out), ptr(status),
+           ptr(ows), ows.numel(), s)
+    return out
+
+
 def accumulate_edges(sampled: Sequence[SampledEdge], graph: Graph, matrix: np.ndarray,
                      transform: GridTransform, workers: int = 1) -> DensityField:
-    """Raw multi-layer histogram H (raster.py:108-130) on the device:
-    per-group counts by DDA splat, then H[l] = sum_b M[l,b] C[b]."""
-    del workers
+    """Raw multi-layer histogram H (raster.py:108-130) on the device.
+
+    Exact layer weights: per-group int32 counts by DDA splat, then
+    H[l] = sum_b M[l,b] C[b] in one rounding (guarded by hb_exact_check).
+    Otherwise, or when the guard trips: the reference's own float32
+    summation order over ``workers`` edge partitions (hb_accumulate_ordered),
+    so H equals the reference bit for bit for the same ``workers``."""
     matrix = np.asarray(matrix, dtype=np.float32)
     nb = matrix.shape[0]
     if matrix.shape != (nb, nb):
@@ -84,27 +106,32 @@ def accumulate_edges(sampled: Sequence[SampledEdge], graph: Graph, matrix: np.nd
                 f"sample out of bounds: points span ({xmin:.3f}, {ymin:.3f}) to "
                 f"({xmax:.3f}, {ymax:.3f}) on a {nu}x{nv} grid")
     dev = _dev()
-    plan = weight_plan(graph.weights[edge_idx])
+    E, n = len(sampled), pts.shape[0]
+    weights = graph.weights[edge_idx]
+    plan = weight_plan(weights, matrix, n)
     grp = torch.from_numpy(graph.bins[edge_idx].astype(np.int32)).to(dev)
     dpts = torch.from_numpy(np.ascontiguousarray(pts)).to(dev)
     dst = torch.from_numpy(starts).to(dev)
     status = torch.zeros(1, dtype=torch.int32, device=dev)
-    mat = torch.from_numpy(matrix.copy()).to(dev)
-    out = torch.empty((nb, nv, nu), dtype=torch.float32, device=dev)
+    identity = np.array_equal(matrix, np.eye(nb, dtype=np.float32))
+    mat = None if identity else torch.from_numpy(matrix.copy()).to(dev)
     s = stream_ptr()
-    E, n = len(sampled), pts.shape[0]
-    if plan.kind == "float":
-        hist = torch.zeros((nb, nv, nu), dtype=torch.float32, device=dev)
-        w = torch.from_numpy(plan.f32_w).to(dev)
-        N.call("hb_splat_f32", ptr(dpts), ptr(dst), E, n, ptr(grp), ptr(w), ptr(hist), nb, nv,
-               nu, ptr(status), s)
-        N.call("hb_mix_layers", None, ptr(hist), ptr(mat), nb, nv, nu, ptr(out), s)
-    else:
+    if plan.kind != "ordered":
         hist = torch.zeros((nb, nv, nu), dtype=torch.int32, device=dev)
         w = None if plan.kind == "unit" else torch.from_numpy(plan.int_w).to(dev)
         N.call("hb_splat", ptr(dpts), ptr(dst), E, n, ptr(grp), ptr(w), ptr(hist), nb, nv, nu,
                ptr(status), None, s)
-        N.call("hb_mix_layers", ptr(hist), None, ptr(mat), nb, nv, nu, ptr(out), s)
+        absm = (None if plan.abs_matrix is None
+                else torch.from_numpy(np.ascontiguousarray(plan.abs_matrix)).to(dev))
+        N.call("hb_exact_check", ptr(hist), ptr(absm), nb, nv, nu, float(plan.limit),
+               ptr(status), s)
+        if not int(status.item()) & 8:
+            out = torch.empty((nb, nv, nu), dtype=torch.float32, device=dev)
+            N.call("hb_mix_layers", ptr(hist), None, ptr(mat), nb, nv, nu, ptr(out), s)
+            return DensityField(transform, out.cpu().numpy())
+    w32 = weights.astype(np.float32)
+    wd = None if np.all(w32 == 1.0) else torch.from_numpy(w32).to(dev)
+    out = _accumulate_ordered(dpts, dst, E, n, grp, wd, mat, nb, nv, nu, workers, status)
     return DensityField(transform, out.cpu().numpy())
 
 

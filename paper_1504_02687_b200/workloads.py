@@ -17,11 +17,11 @@ from dataclasses import dataclass
 
 import numpy as np
 
-from .model import BundleConfig, Graph, make_transform
+from .model import BundleConfig, Graph, interaction_matrix, make_transform
 
 __all__ = ["Workload", "workload", "uniform_graph", "mixture_graph",
            "powerlaw_mixture_graph", "stress_graph", "mean_edge_cells",
-           "WORKLOAD_NAMES"]
+           "random_graph", "table1_workload", "WORKLOAD_NAMES"]
 
 WORKLOAD_NAMES = {
     1: "cfg1-uniform-2k-256",
@@ -30,6 +30,41 @@ WORKLOAD_NAMES = {
     4: "cfg4-powerlaw-2m-1024",
     5: "cfg5-stress-20m-4x2048",
 }
+
+
+def random_graph(n_edges: int, samples_per_edge: float = 24.0, delta: float = 3.0,
+                 grid_size: int = 800, padding_cells: int = 41, seed: int = 0,
+                 world: float = 1000.0) -> Graph:
+    """The reference's scalability graph (``cli.py:142-163``, the paper's
+    Table 1 "random" row): uniform sources in a ``world`` square, targets at
+    a uniform angle and a length ~U(0.5, 1.5) x the mean that gives about
+    ``samples_per_edge`` initial samples, clipped to the square.  The same
+    seeded numpy draws in the same order, so the arrays equal the
+    reference's (tests/golden/make_golden_r2.py checks the digests)."""
+    rng = np.random.default_rng(seed)
+    cell = world / (grid_size - 2 * padding_cells - 1)
+    mean_len = max(samples_per_edge - 1.5, 0.7) * delta * cell
+    src = rng.uniform(0.0, world, size=(n_edges, 2))
+    angle = rng.uniform(0.0, 2.0 * math.pi, size=n_edges)
+    length = rng.uniform(0.5, 1.5, size=n_edges) * mean_len
+    dst = src + np.stack([np.cos(angle), np.sin(angle)], axis=1) * length[:, None]
+    np.clip(dst, 0.0, world, out=dst)
+    positions = np.concatenate([src, dst], axis=0)
+    return Graph(positions, np.arange(n_edges, dtype=np.int64),
+                 np.arange(n_edges, 2 * n_edges, dtype=np.int64))
+
+
+def table1_workload(n_edges: int = 200_000, nbins: int = 1, seed: int = 0,
+                    iterations: int = 10) -> Workload:
+    """``cli.bench`` (``cli.py:166-192``) for one (size, B) pair: default
+    BundleConfig, bins = arange % B, ``interaction_matrix(B, alpha)`` -- the
+    reference's repulsive model, non-dyadic for B = 4 / 16."""
+    cfg = BundleConfig(iterations=iterations, random_seed=seed)
+    g = random_graph(n_edges, 24.0, cfg.delta, cfg.grid_size, cfg.padding_cells, seed)
+    bins = np.arange(n_edges, dtype=np.int64) % nbins
+    mat = interaction_matrix(nbins, cfg.alpha)
+    g = Graph(g.positions, g.sources, g.targets, None, bins)
+    return Workload(f"table1-random-{n_edges // 1000}k-b{nbins}", g, cfg, bins, mat)
 
 
 @dataclass

@@ -56,9 +56,13 @@ def _worker(rank, world, port, outdir):
         D.all_reduce_sum(t)
         moved, disp = D.sum_host_arrays([np.array([rank + 1], dtype=np.int64),
                                          np.array([0.5 * (rank + 1)])])
-        wp, ws = D.gather_polylines(torch.from_numpy(pts), torch.from_numpy(starts))
+        got = D.gather_polylines(torch.from_numpy(pts), torch.from_numpy(starts))
+        # the status / span agreement used by the engine: max over ranks
+        mx = D.all_reduce_max(torch.tensor([float(rank), -float(rank), 4.0 * (rank == 1)],
+                                           dtype=torch.float64))
+        wp, ws = got if got is not None else (np.zeros((0, 2)), np.zeros(0, np.int64))
         np.savez(os.path.join(outdir, f"r{rank}.npz"), hist=t.numpy(), moved=moved, disp=disp,
-                 wp=wp, ws=ws, lo=lo, hi=hi)
+                 wp=wp, ws=ws, lo=lo, hi=hi, gathered=got is not None, mx=mx.numpy())
     finally:
         dist.destroy_process_group()
 
@@ -80,6 +84,9 @@ def test_two_rank_gloo_histogram_and_gather(tmp_path):
     for k in range(world):
         assert np.array_equal(r[k]["hist"], full)          # bit-exact global histogram
         assert int(r[k]["moved"][0]) == 3 and float(r[k]["disp"][0]) == 1.5
-        assert np.array_equal(r[k]["wp"], pts)              # gathered in edge order
-        assert np.array_equal(r[k]["ws"], starts)
+        assert list(r[k]["mx"]) == [1.0, 0.0, 4.0]
+    # polylines gathered to rank 0 only, in edge order
+    assert bool(r[0]["gathered"]) and not bool(r[1]["gathered"])
+    assert np.array_equal(r[0]["wp"], pts)
+    assert np.array_equal(r[0]["ws"], starts)
     assert r[0]["hi"] == r[1]["lo"] and r[1]["hi"] == g.n_edges

@@ -40,7 +40,7 @@ def _emulated(w, shards):
     dst = tr.world_to_grid(g.positions[g.targets])
     parts = shard_edges(sample_counts(src, dst, cfg.delta), shards)
     engs = [BundleEngine(np.ascontiguousarray(src[lo:hi]), np.ascontiguousarray(dst[lo:hi]),
-                         w.bins[lo:hi], weight_plan(g.weights[lo:hi]), w.matrix, tr.shape, cfg)
+                         w.bins[lo:hi], weight_plan(g.weights, w.matrix).slice(lo, hi), w.matrix, tr.shape, cfg)
             for lo, hi in parts]
     for _ in range(cfg.iterations):
         for e in engs:
@@ -101,6 +101,7 @@ def _rank_main(rank, world, port, outdir):
         res = Bm.bundle(w.graph, w.config, bins=w.bins, matrix=w.matrix)
         np.savez(os.path.join(outdir, f"r{rank}.npz"), world=res.sampled_edges.world,
                  starts=res.sampled_edges.starts, field=res.density.values,
+                 edge_base=res.sampled_edges.edge_base, n_edges=len(res.sampled_edges),
                  moved=np.array([m.moved_points for m in res.metrics]),
                  used=np.array([m.used_cells for m in res.metrics]),
                  disp=np.array([m.mean_displacement for m in res.metrics]))
@@ -115,10 +116,18 @@ def test_two_processes_gloo_bundle_matches_single(tmp_path):
                        join=True, start_method="spawn")
     w = workload(1, scale=0.5)
     ref = B.bundle(w.graph, w.config, bins=w.bins, matrix=w.matrix)
+    rs = ref.sampled_edges.starts
     for r in range(world):
         got = np.load(tmp_path / f"r{r}.npz")
-        assert np.array_equal(got["world"], ref.sampled_edges.world)
-        assert np.array_equal(got["starts"], ref.sampled_edges.starts)
+        if r == 0:  # rank 0 holds the gathered result
+            assert int(got["edge_base"]) == 0
+            assert np.array_equal(got["world"], ref.sampled_edges.world)
+            assert np.array_equal(got["starts"], rs)
+        else:       # other ranks: their own edge shard
+            lo, n = int(got["edge_base"]), int(got["n_edges"])
+            assert lo > 0 and lo + n == w.graph.n_edges
+            assert np.array_equal(got["starts"], rs[lo:lo + n + 1] - rs[lo])
+            assert np.array_equal(got["world"], ref.sampled_edges.world[rs[lo]:rs[lo + n]])
         assert np.array_equal(got["field"], ref.density.values)
         assert got["moved"].tolist() == [m.moved_points for m in ref.metrics]
         assert got["used"].tolist() == [m.used_cells for m in ref.metrics]

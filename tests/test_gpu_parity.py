@@ -12,6 +12,7 @@ import numpy as np
 import pytest
 
 from conftest import GOLDEN
+from golden_check import check_golden
 from hb_hash import digest
 
 torch = pytest.importorskip("torch")
@@ -325,21 +326,12 @@ def _golden(name):
 
 
 def _check_run(k, scale=1.0, golden=None):
+    """Config k against its reference golden: per-iteration raw histogram,
+    smoothed field, N_i and metrics; final points / starts; and bundle()'s
+    world polylines (golden_check.check_golden)."""
     w = workload(k, scale=scale)
     g = _golden(golden or f"cfg{k}.json")
-    eng, tr, metrics = B.bundle_packed(w.graph, w.config, bins=w.bins, matrix=w.matrix)
-    pts, starts = eng.packed_points()
-    assert digest(pts.cpu().numpy())["sha256"] == g["final_pts"]["sha256"]
-    assert digest(starts.cpu().numpy())["sha256"] == g["final_starts"]["sha256"]
-    assert digest(eng.field.cpu().numpy())["sha256"] == g["final_field"]["sha256"]
-    for m, gi in zip(metrics, g["iterations"]):
-        assert m.moved_points == gi["moved_points"]
-        assert m.used_cells == gi["used_cells"]
-        assert m.bandwidth == gi["bandwidth"]
-        np.testing.assert_allclose(m.mean_displacement, gi["mean_displacement"],
-                                   rtol=DISP_RTOL)
-    for r, gi in zip(eng.records, g["iterations"]):
-        assert r.n_points == gi["n_points"]
+    check_golden(w, g, workers=g.get("workers", 1), check_graph=False)
 
 
 def test_bundle_cfg1_mini_world_points_bit_exact():
@@ -658,15 +650,26 @@ def test_bundle_small_shapes_vs_oracle(name):
 
 def test_sync_free_capacity_overflow_retries_exactly(monkeypatch):
     """The sync-free loop keeps N_i on the device; when a resample outgrows
-    the buffers the run restarts synchronously -- same bits either way."""
+    the buffers the run is redone with room for it -- same bits either way,
+    and a following reset()+run() needs no retry."""
     w = workload(1, scale=0.5)
     cfg = w.config
-    ref = B.bundle(w.graph, cfg, bins=w.bins, matrix=w.matrix)
-    monkeypatch.setenv("HB_ASYNC_CAP_FACTOR", "1.0")  # no headroom: overflows at once
-    res = B.bundle(w.graph, cfg, bins=w.bins, matrix=w.matrix)
-    assert np.array_equal(res.sampled_edges.starts, ref.sampled_edges.starts)
-    assert np.array_equal(res.sampled_edges.world, ref.sampled_edges.world)
-    assert [m.moved_points for m in res.metrics] == [m.moved_points for m in ref.metrics]
     monkeypatch.setenv("HB_SYNC_FREE", "0")
-    res2 = B.bundle(w.graph, cfg, bins=w.bins, matrix=w.matrix)
-    assert np.array_equal(res2.sampled_edges.world, ref.sampled_edges.world)
+    ref, _, ref_m = B.bundle_packed(w.graph, cfg, bins=w.bins, matrix=w.matrix)
+    rp, rs = (t.cpu().numpy() for t in ref.packed_points())
+    monkeypatch.setenv("HB_SYNC_FREE", "1")
+    monkeypatch.setenv("HB_ASYNC_CAP_FACTOR", "0.5")  # below N_0 x growth: overflows
+    eng, _, metrics = B.bundle_packed(w.graph, cfg, bins=w.bins, matrix=w.matrix,
+                                      capacity_factor=1.0)
+    assert getattr(eng, "_cap_retries", 0) >= 1 and eng.async_n
+    pts, starts = (t.cpu().numpy() for t in eng.packed_points())
+    assert np.array_equal(starts, rs) and np.array_equal(pts, rp)
+    assert [m.moved_points for m in metrics] == [m.moved_points for m in ref_m]
+    retries = eng._cap_retries
+    eng.reset()
+    eng.run()
+    assert eng._cap_retries == retries
+    pts2 = eng.packed_points()[0].cpu().numpy()
+    assert np.array_equal(pts2, rp)
+    res = B.bundle(w.graph, cfg, bins=w.bins, matrix=w.matrix)
+    assert np.array_equal(res.sampled_edges.starts, rs)

@@ -39,7 +39,7 @@ def run(w, shards):
     dst = tr.world_to_grid(g.positions[g.targets])
     parts = shard_edges(sample_counts(src, dst, cfg.delta), shards)
     engs = [BundleEngine(np.ascontiguousarray(src[lo:hi]), np.ascontiguousarray(dst[lo:hi]),
-                         w.bins[lo:hi], weight_plan(g.weights[lo:hi]), w.matrix, tr.shape, cfg)
+                         w.bins[lo:hi], weight_plan(g.weights, w.matrix).slice(lo, hi), w.matrix, tr.shape, cfg)
             for lo, hi in parts]
     for e in engs:
         e.keep_initial_state()

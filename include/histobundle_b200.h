@@ -396,6 +396,26 @@ HB_API int hb_accumulate_ordered(const double *pts, const int64_t *starts, int64
                                  int nu, float *out, int32_t *status, void *workspace,
                                  size_t workspace_bytes, void *stream);
 
+/* The two halves of hb_accumulate_ordered, for edge shards on several GPUs
+ * (the records are exchanged by cell in between, so every cell's hits meet
+ * on one rank in global order):
+ * hb_hits_fill_sorted writes this shard's n_hits records (key = cell *
+ * nparts + partition of the global edge, val = global edge), stably sorted
+ * by key, into keys/vals; hb_ordered_fold folds records whose cells lie in
+ * [cell_base, cell_base + n_cells) into out (B, n_cells) float32 -- first
+ * stably sorting them by key when `sort` (rank-ordered concatenations). */
+HB_API size_t hb_hits_sorted_workspace_bytes(int64_t n_hits);
+HB_API int hb_hits_fill_sorted(const double *pts, const int64_t *starts, int64_t n_edges,
+                               const int64_t *hoff, int64_t n_hits, int nparts,
+                               int64_t edge_base, int64_t edges_total, int nv, int nu,
+                               uint32_t *keys, int32_t *vals, int32_t *status, void *workspace,
+                               size_t workspace_bytes, void *stream);
+HB_API size_t hb_ordered_fold_workspace_bytes(int64_t n_hits, int64_t n_cells);
+HB_API int hb_ordered_fold(uint32_t *keys, int32_t *vals, int64_t n_hits, int sort, int nparts,
+                           int64_t cell_base, int64_t n_cells, const float *w32,
+                           const int32_t *groups, const float *matrix, int nbins, float *out,
+                           void *workspace, size_t workspace_bytes, void *stream);
+
 /* ---- rendering (render.py:158-179) ----
  * Stroke width of every segment of every polyline (segments of edge e are
  * outputs starts[e]-e .. starts[e+1]-e-2): the mean of the layer's clamped

@@ -134,6 +134,12 @@ SIGNATURES = {
     "hb_ordered_workspace_bytes": (_SZ, [_I64, _I, _I, _I]),
     "hb_accumulate_ordered": (_I, [_P, _P, _I64, _P, _I64, _I64, _I, _I64, _I64, _P, _P, _P,
                                    _I, _I, _I, _P, _P, _P, _SZ, _P]),
+    "hb_hits_sorted_workspace_bytes": (_SZ, [_I64]),
+    "hb_hits_fill_sorted": (_I, [_P, _P, _I64, _P, _I64, _I, _I64, _I64, _I, _I, _P, _P, _P,
+                                 _P, _SZ, _P]),
+    "hb_ordered_fold_workspace_bytes": (_SZ, [_I64, _I64]),
+    "hb_ordered_fold": (_I, [_P, _P, _I64, _I, _I, _I64, _I64, _P, _P, _P, _I, _P, _P, _SZ,
+                             _P]),
 }
 
 class HbTiles(ctypes.Structure):

@@ -166,10 +166,6 @@ def _setup(graph, cfg, bins_arr, matrix, fixed_step, group, capacity_factor, *,
     reduce_hist = (lambda h: D.all_reduce_sum(h, group)) if multi else None
     reduce_flags = (lambda t: D.all_reduce_max(t, group)) if multi else None
     plan = _plan(graph, cfg, matrix, transform, force_ordered)
-    if world > 1 and plan.kind == "ordered":
-        raise NotImplementedError(
-            "the reference-order histogram (non-dyadic interaction matrix or fractional "
-            "weights) runs on one GPU; shard only exact-weight graphs")
     common = dict(fixed_step=fixed_step, reduce_hist=reduce_hist,
                   capacity_factor=capacity_factor, workers=workers,
                   reduce_flags=reduce_flags, sync_free=sync_free)
@@ -210,8 +206,12 @@ def _setup(graph, cfg, bins_arr, matrix, fixed_step, group, capacity_factor, *,
     if cfg.directed_offset_fraction > 0:
         od = _offset_vectors(src, dst, cfg.directed_offset_fraction
                              * max(transform.width, transform.height))
+    shard = None
+    if multi:
+        shard = dict(rank=rank, world=world, group=group, edge_base=lo,
+                     edges_total=graph.n_edges, weights=graph.weights, bins=bins_arr)
     eng = BundleEngine(src, dst, bins_arr[lo:hi], plan.slice(lo, hi),
-                       matrix, transform.shape, cfg, offset_disp=od, **common)
+                       matrix, transform.shape, cfg, offset_disp=od, shard=shard, **common)
     eng.node_arrays = None
     return eng, transform, lo, hi
 

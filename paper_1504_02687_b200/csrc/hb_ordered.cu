@@ -187,15 +187,16 @@ ordered_fold_kernel(const uint32_t *__restrict__ keys, const int32_t *__restrict
                     const uint32_t *__restrict__ run_cell, const int32_t *__restrict__ run_len,
                     const int64_t *__restrict__ run_off, const int *__restrict__ n_runs, int nparts,
                     const float *__restrict__ w32, const int32_t *__restrict__ groups,
-                    const float *__restrict__ mat, int nb, int64_t plane,
+                    const float *__restrict__ mat, int nb, int64_t cell_base, int64_t n_cells,
                     float *__restrict__ out) {
     const unsigned full = 0xffffffffu;
     const int lane = threadIdx.x & 31;
     const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
     const int runs = *n_runs;
     for (int64_t r = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; r < runs; r += nw) {
-        const uint32_t cell = run_cell[r];
-        if (cell == 0xffffffffu || (int64_t)cell >= plane) continue;
+        const uint32_t cell_key = run_cell[r];
+        const int64_t cell = (int64_t)cell_key - cell_base;  // output column of this run
+        if (cell_key == 0xffffffffu || cell < 0 || cell >= n_cells) continue;
         const int64_t off = run_off[r], len = run_len[r];
         for (int l0 = 0; l0 < nb; l0 += 32) {
             const int l = l0 + lane;
@@ -232,53 +233,12 @@ ordered_fold_kernel(const uint32_t *__restrict__ keys, const int32_t *__restrict
                 }
             }
             if (curp >= 0) total = first ? acc : __fadd_rn(total, acc);
-            if (l < nb) out[(int64_t)l * plane + cell] = total;
+            if (l < nb) out[(int64_t)l * n_cells + cell] = total;
         }
     }
 }
 
-struct OrderedWs {
-    uint32_t *keys[2];
-    int32_t *vals[2];
-    uint32_t *run_cell;
-    int32_t *run_len;
-    int64_t *run_off;
-    int *n_runs;
-    void *tmp;
-    size_t tmp_bytes;
-};
-
 static size_t align_up(size_t x) { return (x + 255) & ~(size_t)255; }
-
-static size_t cub_tmp_bytes(int64_t n_hits, int64_t plane, int end_bit) {
-    size_t a = 0, b = 0, c = 0;
-    cub::DoubleBuffer<uint32_t> k(nullptr, nullptr);
-    cub::DoubleBuffer<int32_t> v(nullptr, nullptr);
-    cub::DeviceRadixSort::SortPairs(nullptr, a, k, v, (int)n_hits, 0, end_bit);
-    thrust::transform_iterator<CellOf, const uint32_t *> it(nullptr, CellOf{1});
-    cub::DeviceRunLengthEncode::Encode(nullptr, b, it, (uint32_t *)nullptr, (int32_t *)nullptr,
-                                       (int *)nullptr, (int)n_hits);
-    cub::DeviceScan::ExclusiveSum(nullptr, c, (const int32_t *)nullptr, (int64_t *)nullptr,
-                                  (int)(plane + 1));
-    return a > b ? (a > c ? a : c) : (b > c ? b : c);
-}
-
-static OrderedWs carve(void *ws, int64_t n_hits, int64_t plane, int end_bit) {
-    OrderedWs w{};
-    char *p = reinterpret_cast<char *>(ws);
-    const int64_t runs = (n_hits < plane + 1 ? n_hits : plane + 1) + 1;
-    w.keys[0] = reinterpret_cast<uint32_t *>(p); p += align_up(4 * n_hits);
-    w.keys[1] = reinterpret_cast<uint32_t *>(p); p += align_up(4 * n_hits);
-    w.vals[0] = reinterpret_cast<int32_t *>(p); p += align_up(4 * n_hits);
-    w.vals[1] = reinterpret_cast<int32_t *>(p); p += align_up(4 * n_hits);
-    w.run_cell = reinterpret_cast<uint32_t *>(p); p += align_up(4 * runs);
-    w.run_len = reinterpret_cast<int32_t *>(p); p += align_up(4 * runs);
-    w.run_off = reinterpret_cast<int64_t *>(p); p += align_up(8 * runs);
-    w.n_runs = reinterpret_cast<int *>(p); p += 256;
-    w.tmp = p;
-    w.tmp_bytes = cub_tmp_bytes(n_hits, plane, end_bit);
-    return w;
-}
 
 static int key_bits(int64_t plane, int nparts) {
     // valid keys are < maxkey; the sentinel 0xffffffff must sort after all
@@ -288,6 +248,92 @@ static int key_bits(int64_t plane, int nparts) {
     int bits = 1;
     while (bits < 32 && (1ull << bits) <= maxkey) ++bits;
     return bits;
+}
+
+static size_t sort_tmp_bytes(int64_t n) {
+    size_t a = 0;
+    cub::DoubleBuffer<uint32_t> k(nullptr, nullptr);
+    cub::DoubleBuffer<int32_t> v(nullptr, nullptr);
+    cub::DeviceRadixSort::SortPairs(nullptr, a, k, v, (int)n, 0, 32);
+    return align_up(a);
+}
+
+static size_t fold_tmp_bytes(int64_t n, int64_t runs) {
+    size_t b = 0, c = 0;
+    thrust::transform_iterator<CellOf, const uint32_t *> it(nullptr, CellOf{1});
+    cub::DeviceRunLengthEncode::Encode(nullptr, b, it, (uint32_t *)nullptr, (int32_t *)nullptr,
+                                       (int *)nullptr, (int)n);
+    cub::DeviceScan::ExclusiveSum(nullptr, c, (const int32_t *)nullptr, (int64_t *)nullptr,
+                                  (int)runs);
+    return align_up(b > c ? b : c);
+}
+
+// Stable sort of (key, val) pairs by key, in place (keys/vals on return),
+// with a scratch double buffer and CUB temp from `ws`.
+static int sort_pairs(uint32_t *keys, int32_t *vals, int64_t n, int end_bit, char *ws,
+                      cudaStream_t st) {
+    uint32_t *k2 = reinterpret_cast<uint32_t *>(ws); ws += align_up(4 * (size_t)n);
+    int32_t *v2 = reinterpret_cast<int32_t *>(ws); ws += align_up(4 * (size_t)n);
+    cub::DoubleBuffer<uint32_t> kb(keys, k2);
+    cub::DoubleBuffer<int32_t> vb(vals, v2);
+    size_t tb = sort_tmp_bytes(n);
+    if (cub::DeviceRadixSort::SortPairs(ws, tb, kb, vb, (int)n, 0, end_bit, st) != cudaSuccess)
+        return check_launch("hb_ordered(sort)", 0);
+    if (kb.Current() != keys &&
+        (cudaMemcpyAsync(keys, kb.Current(), 4 * (size_t)n, cudaMemcpyDeviceToDevice, st) !=
+             cudaSuccess ||
+         cudaMemcpyAsync(vals, vb.Current(), 4 * (size_t)n, cudaMemcpyDeviceToDevice, st) !=
+             cudaSuccess))
+        return check_launch("hb_ordered(sort copy)", 0);
+    return HB_OK;
+}
+static size_t sort_ws_bytes(int64_t n) { return 2 * align_up(4 * (size_t)n) + sort_tmp_bytes(n); }
+
+// Runs of equal cell over sorted records -> one warp per cell folds them.
+static int fold_sorted(const uint32_t *keys, const int32_t *vals, int64_t n, int nparts,
+                       int64_t cell_base, int64_t n_cells, const float *w32,
+                       const int32_t *groups, const float *matrix, int nbins, float *out,
+                       char *ws, cudaStream_t st) {
+    const int64_t runs_cap = n < n_cells + 1 ? n : n_cells + 1;  // + the sentinel run
+    uint32_t *run_cell = reinterpret_cast<uint32_t *>(ws); ws += align_up(4 * (size_t)(runs_cap + 1));
+    int32_t *run_len = reinterpret_cast<int32_t *>(ws); ws += align_up(4 * (size_t)(runs_cap + 1));
+    int64_t *run_off = reinterpret_cast<int64_t *>(ws); ws += align_up(8 * (size_t)(runs_cap + 1));
+    int *n_runs = reinterpret_cast<int *>(ws); ws += 256;
+    if (cudaMemsetAsync(run_len, 0, 4 * (size_t)(runs_cap + 1), st) != cudaSuccess)
+        return check_launch("hb_ordered(memset)", 0);
+    thrust::transform_iterator<CellOf, const uint32_t *> cells(keys, CellOf{(uint32_t)nparts});
+    size_t tb = fold_tmp_bytes(n, runs_cap + 1);
+    if (cub::DeviceRunLengthEncode::Encode(ws, tb, cells, run_cell, run_len, n_runs, (int)n,
+                                           st) != cudaSuccess)
+        return check_launch("hb_ordered(rle)", 0);
+    // run offsets: exclusive scan of the run lengths (entries past n_runs
+    // stay zero and are never read)
+    tb = fold_tmp_bytes(n, runs_cap + 1);
+    if (cub::DeviceScan::ExclusiveSum(ws, tb, run_len, run_off, (int)(runs_cap + 1), st) !=
+        cudaSuccess)
+        return check_launch("hb_ordered(scan)", 1);
+    const int64_t fold_warps = runs_cap < (int64_t)device_sm_count() * 64
+                                   ? runs_cap : (int64_t)device_sm_count() * 64;
+    ordered_fold_kernel<<<(unsigned)((fold_warps * 32 + 255) / 256), 256, 0, st>>>(
+        keys, vals, run_cell, run_len, run_off, n_runs, nparts, w32, groups, matrix, nbins,
+        cell_base, n_cells, out);
+    return check_launch("hb_ordered(fold)", 3);
+}
+static size_t fold_ws_bytes(int64_t n, int64_t n_cells) {
+    const int64_t runs_cap = (n < n_cells + 1 ? n : n_cells + 1) + 1;
+    return 2 * align_up(4 * (size_t)runs_cap) + align_up(8 * (size_t)runs_cap) + 256 +
+           fold_tmp_bytes(n, runs_cap);
+}
+
+static void fill_launch(const double *pts, const int64_t *starts, int64_t n_edges,
+                        const int64_t *hoff, int nparts, int64_t edge_base, int64_t edges_total,
+                        int nv, int nu, uint32_t *keys, int32_t *vals, int32_t *status,
+                        cudaStream_t st) {
+    const int64_t warps = n_edges < (int64_t)device_sm_count() * 64 ? n_edges
+                                                                 : (int64_t)device_sm_count() * 64;
+    hits_fill_kernel<<<(unsigned)((warps * 32 + 255) / 256), 256, 0, st>>>(
+        reinterpret_cast<const double2 *>(pts), starts, n_edges, hoff, nparts, edge_base,
+        edges_total, nv, nu, keys, vals, status);
 }
 
 }  // namespace hb
@@ -356,13 +402,21 @@ int hb_hits_count(const double *pts, const int64_t *starts, int64_t n_edges, int
     return check_launch("hb_hits_count", kernels + 1);
 }
 
+static bool ordered_args_ok(int64_t n_edges, int64_t n_hits, int nparts, int nv, int nu,
+                            int64_t edge_base, int64_t edges_total) {
+    const int64_t plane = (int64_t)nv * nu;
+    return n_edges >= 0 && n_hits >= 0 && n_hits < (1ll << 31) && nparts >= 1 && nv >= 1 &&
+           nu >= 1 && nv <= kMaxDim && nu <= kMaxDim && edge_base >= 0 &&
+           edges_total >= edge_base + n_edges && edges_total < (1ll << 31) &&
+           (uint64_t)plane * (uint64_t)nparts < 0xffffffffull;
+}
+
 size_t hb_ordered_workspace_bytes(int64_t n_hits, int nv, int nu, int nparts) {
     if (n_hits < 0 || nv < 1 || nu < 1 || nparts < 1) return 0;
     const int64_t plane = (int64_t)nv * nu;
-    const int64_t runs = (n_hits < plane + 1 ? n_hits : plane + 1) + 1;
-    return 4 * align_up(4 * (size_t)n_hits) + 2 * align_up(4 * (size_t)runs) +
-           align_up(8 * (size_t)runs) + 256 + cub_tmp_bytes(n_hits, plane, key_bits(plane, nparts)) +
-           256;
+    const size_t recs = 2 * align_up(4 * (size_t)n_hits);
+    const size_t a = sort_ws_bytes(n_hits), b = fold_ws_bytes(n_hits, plane);
+    return recs + (a > b ? a : b) + 256;
 }
 
 int hb_accumulate_ordered(const double *pts, const int64_t *starts, int64_t n_edges,
@@ -372,53 +426,70 @@ int hb_accumulate_ordered(const double *pts, const int64_t *starts, int64_t n_ed
                           float *out, int32_t *status, void *workspace, size_t workspace_bytes,
                           void *stream) {
     const int64_t plane = (int64_t)nv * nu;
-    if (n_edges < 0 || n_hits < 0 || n_hits >= (1ll << 31) || nparts < 1 || nbins < 1 ||
-        nv < 1 || nu < 1 || nv > kMaxDim || nu > kMaxDim || !out || !status ||
-        edge_base < 0 || edges_total < edge_base + n_edges || edges_total >= (1ll << 31) ||
-        (uint64_t)plane * (uint64_t)nparts >= 0xffffffffull ||
-        (n_edges > 0 && (!pts || !starts || !hoff)) || !workspace ||
-        workspace_bytes < hb_ordered_workspace_bytes(n_hits, nv, nu, nparts))
+    if (!ordered_args_ok(n_edges, n_hits, nparts, nv, nu, edge_base, edges_total) ||
+        nbins < 1 || !out || !status || (n_edges > 0 && (!pts || !starts || !hoff)) ||
+        !workspace || workspace_bytes < hb_ordered_workspace_bytes(n_hits, nv, nu, nparts))
         return set_error(HB_EINVAL, "hb_accumulate_ordered: bad arguments");
     (void)n_pts;
     cudaStream_t st = as_stream(stream);
     if (cudaMemsetAsync(out, 0, sizeof(float) * (size_t)nbins * plane, st) != cudaSuccess)
         return check_launch("hb_accumulate_ordered(memset)", 0);
     if (n_hits == 0 || n_edges == 0) return check_launch("hb_accumulate_ordered", 0);
-    const int end_bit = key_bits(plane, nparts);
-    OrderedWs w = carve(workspace, n_hits, plane, end_bit);
-    const int64_t warps = n_edges < (int64_t)device_sm_count() * 64 ? n_edges
-                                                                 : (int64_t)device_sm_count() * 64;
-    hits_fill_kernel<<<(unsigned)((warps * 32 + 255) / 256), 256, 0, st>>>(
-        reinterpret_cast<const double2 *>(pts), starts, n_edges, hoff, nparts, edge_base,
-        edges_total, nv, nu, w.keys[0], w.vals[0], status);
-    cub::DoubleBuffer<uint32_t> kb(w.keys[0], w.keys[1]);
-    cub::DoubleBuffer<int32_t> vb(w.vals[0], w.vals[1]);
-    size_t tb = w.tmp_bytes;
-    if (cub::DeviceRadixSort::SortPairs(w.tmp, tb, kb, vb, (int)n_hits, 0, end_bit, st) !=
-        cudaSuccess)
-        return check_launch("hb_accumulate_ordered(sort)", 1);
-    if (cudaMemsetAsync(w.run_len, 0, 4 * (size_t)(n_hits < plane + 1 ? n_hits : plane + 1), st) !=
-        cudaSuccess)
-        return check_launch("hb_accumulate_ordered(memset)", 1);
-    thrust::transform_iterator<CellOf, const uint32_t *> cells(kb.Current(),
-                                                              CellOf{(uint32_t)nparts});
-    tb = w.tmp_bytes;
-    if (cub::DeviceRunLengthEncode::Encode(w.tmp, tb, cells, w.run_cell, w.run_len, w.n_runs,
-                                           (int)n_hits, st) != cudaSuccess)
-        return check_launch("hb_accumulate_ordered(rle)", 2);
-    // run offsets: exclusive scan of the run lengths (only the first n_runs
-    // are meaningful; the rest of run_len is left as is and never read)
-    const int64_t runs_cap = (n_hits < plane + 1 ? n_hits : plane + 1);
-    tb = w.tmp_bytes;
-    if (cub::DeviceScan::ExclusiveSum(w.tmp, tb, w.run_len, w.run_off, (int)runs_cap, st) !=
-        cudaSuccess)
-        return check_launch("hb_accumulate_ordered(scan)", 3);
-    const int64_t fold_warps = runs_cap < (int64_t)device_sm_count() * 64
-                                   ? runs_cap : (int64_t)device_sm_count() * 64;
-    ordered_fold_kernel<<<(unsigned)((fold_warps * 32 + 255) / 256), 256, 0, st>>>(
-        kb.Current(), vb.Current(), w.run_cell, w.run_len, w.run_off, w.n_runs, nparts,
-        w32, groups, matrix, nbins, plane, out);
-    return check_launch("hb_accumulate_ordered", 5);
+    char *p = reinterpret_cast<char *>(workspace);
+    uint32_t *keys = reinterpret_cast<uint32_t *>(p); p += align_up(4 * (size_t)n_hits);
+    int32_t *vals = reinterpret_cast<int32_t *>(p); p += align_up(4 * (size_t)n_hits);
+    fill_launch(pts, starts, n_edges, hoff, nparts, edge_base, edges_total, nv, nu, keys, vals,
+                status, st);
+    int rc = check_launch("hb_accumulate_ordered(fill)");
+    if (rc) return rc;
+    if ((rc = sort_pairs(keys, vals, n_hits, key_bits(plane, nparts), p, st))) return rc;
+    return fold_sorted(keys, vals, n_hits, nparts, 0, plane, w32, groups, matrix, nbins, out, p,
+                       st);
+}
+
+size_t hb_hits_sorted_workspace_bytes(int64_t n_hits) { return sort_ws_bytes(n_hits) + 256; }
+
+int hb_hits_fill_sorted(const double *pts, const int64_t *starts, int64_t n_edges,
+                        const int64_t *hoff, int64_t n_hits, int nparts, int64_t edge_base,
+                        int64_t edges_total, int nv, int nu, uint32_t *keys, int32_t *vals,
+                        int32_t *status, void *workspace, size_t workspace_bytes, void *stream) {
+    if (!ordered_args_ok(n_edges, n_hits, nparts, nv, nu, edge_base, edges_total) || !status ||
+        (n_hits > 0 && (!keys || !vals)) || (n_edges > 0 && (!pts || !starts || !hoff)) ||
+        !workspace || workspace_bytes < hb_hits_sorted_workspace_bytes(n_hits))
+        return set_error(HB_EINVAL, "hb_hits_fill_sorted: bad arguments");
+    if (n_hits == 0 || n_edges == 0) return HB_OK;
+    cudaStream_t st = as_stream(stream);
+    fill_launch(pts, starts, n_edges, hoff, nparts, edge_base, edges_total, nv, nu, keys, vals,
+                status, st);
+    int rc = check_launch("hb_hits_fill_sorted(fill)");
+    if (rc) return rc;
+    return sort_pairs(keys, vals, n_hits, key_bits((int64_t)nv * nu, nparts),
+                      reinterpret_cast<char *>(workspace), st);
+}
+
+size_t hb_ordered_fold_workspace_bytes(int64_t n_hits, int64_t n_cells) {
+    const size_t a = sort_ws_bytes(n_hits), b = fold_ws_bytes(n_hits, n_cells);
+    return (a > b ? a : b) + 256;
+}
+
+int hb_ordered_fold(uint32_t *keys, int32_t *vals, int64_t n_hits, int sort, int nparts,
+                    int64_t cell_base, int64_t n_cells, const float *w32, const int32_t *groups,
+                    const float *matrix, int nbins, float *out, void *workspace,
+                    size_t workspace_bytes, void *stream) {
+    if (n_hits < 0 || n_hits >= (1ll << 31) || nparts < 1 || nbins < 1 || cell_base < 0 ||
+        n_cells < 1 || !out || (n_hits > 0 && (!keys || !vals)) || !workspace ||
+        workspace_bytes < hb_ordered_fold_workspace_bytes(n_hits, n_cells) ||
+        (uint64_t)(cell_base + n_cells) * (uint64_t)nparts >= 0xffffffffull)
+        return set_error(HB_EINVAL, "hb_ordered_fold: bad arguments");
+    cudaStream_t st = as_stream(stream);
+    if (cudaMemsetAsync(out, 0, sizeof(float) * (size_t)nbins * n_cells, st) != cudaSuccess)
+        return check_launch("hb_ordered_fold(memset)", 0);
+    if (n_hits == 0) return HB_OK;
+    char *p = reinterpret_cast<char *>(workspace);
+    int rc;
+    if (sort && (rc = sort_pairs(keys, vals, n_hits, 32, p, st))) return rc;
+    return fold_sorted(keys, vals, n_hits, nparts, cell_base, n_cells, w32, groups, matrix, nbins,
+                       out, p, st);
 }
 
 }  // extern "C"

@@ -22,7 +22,7 @@ import torch
 import torch.distributed as dist
 
 __all__ = ["rank_world", "distributed", "shard_edges", "all_reduce_sum", "all_reduce_max",
-           "sum_host_arrays", "gather_polylines"]
+           "all_to_all_var", "all_gather_columns", "sum_host_arrays", "gather_polylines"]
 
 
 def rank_world(group=None) -> tuple[int, int]:
@@ -77,6 +77,32 @@ def all_reduce_max(t: torch.Tensor, group=None) -> torch.Tensor:
     d = t.to(dev)
     dist.all_reduce(d, op=dist.ReduceOp.MAX, group=group)
     return d.cpu()
+
+
+def all_to_all_var(t: torch.Tensor, send_counts: list[int], group=None) -> torch.Tensor:
+    """Variable-size all-to-all of the rows of ``t`` (rank r gets the
+    ``send_counts[r]`` rows starting at ``sum(send_counts[:r])``).  The
+    received blocks are concatenated in sender-rank order."""
+    dev = _backend_device(group)
+    sc = torch.tensor(send_counts, dtype=torch.int64, device=dev)
+    rc = torch.empty_like(sc)
+    dist.all_to_all_single(rc, sc, group=group)
+    recv_counts = [int(v) for v in rc.cpu()]
+    src = t.to(dev)
+    out = torch.empty((sum(recv_counts),) + tuple(t.shape[1:]), dtype=t.dtype, device=dev)
+    dist.all_to_all_single(out, src, recv_counts, list(send_counts), group=group)
+    return out.to(t.device)
+
+
+def all_gather_columns(t: torch.Tensor, sizes: list[int], group=None) -> torch.Tensor:
+    """Concatenate every rank's (B, sizes[r]) block along dim 1, in rank order."""
+    dev = _backend_device(group)
+    width = max(sizes)
+    pad = torch.zeros((t.shape[0], width), dtype=t.dtype, device=dev)
+    pad[:, : t.shape[1]] = t.to(dev)
+    parts = [torch.empty_like(pad) for _ in sizes]
+    dist.all_gather(parts, pad, group=group)
+    return torch.cat([p[:, :n] for p, n in zip(parts, sizes)], dim=1).to(t.device)
 
 
 def _backend_device(group=None) -> torch.device:

@@ -240,7 +240,10 @@ class BundleEngine:
     takes the same decision on the run's status (bounds, capacity retry,
     exactness) and raises together.  ``workers`` is the reference's
     partition count (``_parallel.partition_ranges``): it only changes results
-    on the ordered path, exactly as it does in the reference.
+    on the ordered path, exactly as it does in the reference.  ``shard``
+    (multi-rank runs) describes this engine's place in the whole graph:
+    ``rank, world, group, edge_base, edges_total`` and the global
+    ``weights`` / ``bins`` arrays the ordered path indexes by global edge.
     """
 
     def __init__(self, src: np.ndarray, dst: np.ndarray, groups: np.ndarray,
@@ -249,7 +252,7 @@ class BundleEngine:
                  offset_disp: np.ndarray | None = None, device=None,
                  reduce_hist=None, capacity_factor: float = 2.0,
                  starts: torch.Tensor | None = None, workers: int = 1,
-                 reduce_flags=None, sync_free: bool = True):
+                 reduce_flags=None, sync_free: bool = True, shard: dict | None = None):
         N.lib()  # fail loudly if the native library is missing
         if not torch.cuda.is_available():
             raise N.NativeError("paper_1504_02687_b200 needs a CUDA device (sm_100a); "
@@ -296,7 +299,12 @@ class BundleEngine:
         self.mat_dev = None if mat_is_identity else upload(self.matrix, dev)
         self.absm_dev = (None if weights.abs_matrix is None
                          else upload(np.ascontiguousarray(weights.abs_matrix, np.float64), dev))
-        self.nparts = max(1, min(int(workers), E)) if E else 1
+        self.shard = shard
+        e_total = E if shard is None else int(shard["edges_total"])
+        self.nparts = max(1, min(int(workers), e_total)) if e_total else 1
+        self.ord_w32 = self.ord_groups = None  # global arrays (sharded ordered path)
+        if shard is not None and weights.kind == "ordered":
+            self._upload_global_arrays()
         self.hoff = None         # ordered path: hit offsets + workspaces
         self.hits_ws = None
         self.ord_ws = None
@@ -467,6 +475,21 @@ class BundleEngine:
         self._k("hb_splat", ptr(self.pts), ptr(self.starts), E, self.n_pts, ptr(self.groups),
                 ptr(self.wint), ptr(self.hist), B, nv, nu, ptr(self.status), sink, s)
 
+    def _upload_global_arrays(self) -> None:
+        sh = self.shard
+        w32 = np.asarray(sh["weights"]).astype(np.float32)
+        self.ord_w32 = None if np.all(w32 == 1.0) else upload(w32, self.dev)
+        self.ord_groups = (None if self.nbins == 1 else
+                           upload(np.asarray(sh["bins"], dtype=np.int32), self.dev))
+
+    def _ws(self, attr: str, nbytes: int) -> torch.Tensor:
+        t = getattr(self, attr, None)
+        if t is None or t.numel() < nbytes:
+            setattr(self, attr, None)
+            t = torch.empty(int(nbytes * 1.25) + 4096, dtype=torch.uint8, device=self.dev)
+            setattr(self, attr, t)
+        return t
+
     def _accumulate_ordered(self, s) -> None:
         """The reference's float32 histogram in its own summation order
         (raster.py:70-94): hit offsets, one host read of the hit total to
@@ -475,12 +498,13 @@ class BundleEngine:
         n = self.n_pts
         if self.hoff is None or self.hoff.numel() < n + 1:
             self.hoff = torch.empty(int((n + 1) * 1.25) + 1024, dtype=torch.int64, device=self.dev)
-        hb = int(N.lib().hb_hits_workspace_bytes(n))
-        if self.hits_ws is None or self.hits_ws.numel() < hb:
-            self.hits_ws = torch.empty(int(hb * 1.25) + 4096, dtype=torch.uint8, device=self.dev)
+        self.hits_ws = self._ws("hits_ws", int(N.lib().hb_hits_workspace_bytes(n)))
         self._k("hb_hits_count", ptr(self.pts), ptr(self.starts), E, n, ptr(self.hoff),
                 ptr(self.hits_ws), self.hits_ws.numel(), s)
         n_hits = int(download(self.hoff[n:n + 1])[0])
+        if self.shard is not None:
+            self._accumulate_ordered_sharded(n, n_hits, s)
+            return
         ob = int(N.lib().hb_ordered_workspace_bytes(n_hits, nv, nu, self.nparts))
         if self.ord_ws is None or self.ord_ws.numel() < ob:
             self.ord_ws = None
@@ -489,6 +513,42 @@ class BundleEngine:
                 n_hits, self.nparts, 0, E, ptr(self.wf32), self._emit_groups(),
                 ptr(self.mat_dev), B, nv, nu, ptr(self.hist), ptr(self.status),
                 ptr(self.ord_ws), self.ord_ws.numel(), s)
+
+    def _accumulate_ordered_sharded(self, n: int, n_hits: int, s) -> None:
+        """Ordered histogram of an edge-sharded run: every rank sorts its own
+        hit records by cell, the records travel to the rank owning their
+        cell slab (all-to-all; rank order = global edge order, so each
+        cell's hits arrive in the reference's order), each rank folds its
+        slab and the slabs are all-gathered -- identical to one GPU."""
+        from . import dist as D
+        sh = self.shard
+        rank, world, group = sh["rank"], sh["world"], sh["group"]
+        E, B, nv, nu, P = self.n_edges, self.nbins, self.nv, self.nu, self.nparts
+        plane = nv * nu
+        keys = torch.empty(max(n_hits, 1), dtype=torch.int32, device=self.dev)
+        vals = torch.empty(max(n_hits, 1), dtype=torch.int32, device=self.dev)
+        ws = self._ws("ord_ws", int(N.lib().hb_hits_sorted_workspace_bytes(n_hits)))
+        self._k("hb_hits_fill_sorted", ptr(self.pts), ptr(self.starts), E, ptr(self.hoff),
+                n_hits, P, int(sh["edge_base"]), int(sh["edges_total"]), nv, nu, ptr(keys),
+                ptr(vals), ptr(self.status), ptr(ws), ws.numel(), s)
+        k64 = keys[:n_hits].to(torch.int64) & 0xFFFFFFFF  # keys are uint32
+        bounds = torch.tensor([(r * plane // world) * P for r in range(world + 1)],
+                              dtype=torch.int64, device=self.dev)
+        cuts = torch.searchsorted(k64, bounds).cpu().tolist()  # out-of-grid keys sort last
+        counts = [cuts[r + 1] - cuts[r] for r in range(world)]
+        rk = D.all_to_all_var(keys[cuts[0]:cuts[-1]], counts, group)
+        rv = D.all_to_all_var(vals[cuts[0]:cuts[-1]], counts, group)
+        c0, c1 = rank * plane // world, (rank + 1) * plane // world
+        m = int(rk.shape[0])
+        slab = torch.empty((B, max(c1 - c0, 1)), dtype=torch.float32, device=self.dev)
+        fws = self._ws("fold_ws", int(N.lib().hb_ordered_fold_workspace_bytes(m, max(c1 - c0, 1))))
+        if c1 > c0:
+            self._k("hb_ordered_fold", ptr(rk), ptr(rv), m, 1, P, c0, c1 - c0,
+                    ptr(self.ord_w32), ptr(self.ord_groups), ptr(self.mat_dev), B, ptr(slab),
+                    ptr(fws), fws.numel(), s)
+        sizes = [(r + 1) * plane // world - r * plane // world for r in range(world)]
+        full = D.all_gather_columns(slab[:, : c1 - c0], sizes, group)
+        self.hist.view(B, plane).copy_(full)
 
     def _ensure_records(self, n: int) -> None:
         if n <= self.t_rec.numel():
@@ -501,7 +561,8 @@ class BundleEngine:
     def step(self) -> IterationRecord:
         """One bundling iteration (bundler.py:351-376) on the device."""
         self.step_splat()
-        if self.reduce_hist is not None:
+        if self.reduce_hist is not None and self.wkind != "ordered":
+            # (a sharded ordered histogram is already global: slabs all-gathered)
             self.reduce_hist(self.hist)
         return self.step_field()
 
@@ -811,6 +872,8 @@ class BundleEngine:
         self.wf32 = None if w is None else upload(w, self.dev)
         self.hist = torch.empty((self.nbins, self.nv, self.nu), dtype=torch.float32,
                                 device=self.dev)
+        if self.shard is not None:
+            self._upload_global_arrays()
         self.tiles, self.tile_mode = None, -1
         self.t_tab = self.t_rec = None
         self.async_n = False

@@ -90,3 +90,39 @@ def test_two_rank_gloo_histogram_and_gather(tmp_path):
     assert np.array_equal(r[0]["wp"], pts)
     assert np.array_equal(r[0]["ws"], starts)
     assert r[0]["hi"] == r[1]["lo"] and r[1]["hi"] == g.n_edges
+
+
+def _exchange_worker(rank, world, port, outdir):
+    import sys
+    sys.path.insert(0, ROOT)
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from paper_1504_02687_b200 import dist as D
+        # rank r sends (r, dest) tagged rows: dest d gets d + 1 rows from every rank
+        rows = [np.array([[rank, d]] * (d + 1), dtype=np.int32) for d in range(world)]
+        send = torch.from_numpy(np.concatenate(rows))
+        recv = D.all_to_all_var(send, [d + 1 for d in range(world)])
+        # column blocks of unequal width, gathered in rank order
+        block = torch.full((2, rank + 1), float(rank))
+        cols = D.all_gather_columns(block, [r + 1 for r in range(world)])
+        np.savez(os.path.join(outdir, f"x{rank}.npz"), recv=recv.numpy(), cols=cols.numpy())
+    finally:
+        dist.destroy_process_group()
+
+
+def test_exchange_helpers_gloo(tmp_path):
+    """The ordered path's record exchange (variable all-to-all, sender-rank
+    order) and slab all-gather over gloo, world size 3."""
+    world = 3
+    mp.start_processes(_exchange_worker, args=(world, _free_port(), str(tmp_path)),
+                       nprocs=world, join=True, start_method="spawn")
+    for r in range(world):
+        x = np.load(tmp_path / f"x{r}.npz")
+        want = np.concatenate([np.array([[s, r]] * (r + 1), dtype=np.int32)
+                               for s in range(world)])
+        assert np.array_equal(x["recv"], want)
+        cols = x["cols"]
+        assert cols.shape == (2, 6)
+        assert cols[0].tolist() == [0, 1, 1, 2, 2, 2]

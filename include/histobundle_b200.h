@@ -173,6 +173,20 @@ HB_API int hb_smooth(const int32_t *counts, const float *hist, const float *matr
               float *out, void *workspace, size_t workspace_bytes,
               float *layer_peak, void *stream);
 
+/* hb_smooth of integer group counts whose mixed sums are exact
+ * (H = scale * mix * G with an integer matrix `mix` (B,B) int32, NULL =
+ * identity, and scale = 2^k).  The first pass is computed from exact
+ * integer window sums -- the reference's float64 table is exact there, so
+ * its box sum is the true window sum (no sequential fold needed); later
+ * passes as in hb_smooth.  Also the exactness guard: HB_STATUS_INEXACT in
+ * *status (nullable) when a cell has sum_b |mix[l,b]| * G[b] >= limit or a
+ * negative count.  Needs radii[0] > 0 and nu <= 8192 (else use hb_smooth +
+ * hb_exact_check); same workspace as hb_smooth. */
+HB_API int hb_smooth_counts(const int32_t *counts, const int32_t *mix, double scale,
+                            double limit, int nbins, int nv, int nu, const int32_t *radii,
+                            int npasses, float *out, void *workspace, size_t workspace_bytes,
+                            float *layer_peak, int32_t *status, void *stream);
+
 /* The raw histogram H = M * G alone (raster.accumulate_edges, raster.py:108-130). */
 HB_API int hb_mix_layers(const int32_t *counts, const float *hist, const float *matrix,
                          int nbins, int nv, int nu, float *out, void *stream);

@@ -106,6 +106,7 @@ SIGNATURES = {
     "hb_splat": (_I, [_P, _P, _I64, _I64, _P, _P, _P, _I, _I, _I, _P, _P, _P]),
     "hb_smooth_workspace_bytes": (_SZ, [_I, _I, _I]),
     "hb_smooth": (_I, [_P, _P, _P, _I, _I, _I, _P, _I, _P, _P, _SZ, _P, _P]),
+    "hb_smooth_counts": (_I, [_P, _P, _D, _D, _I, _I, _I, _P, _I, _P, _P, _SZ, _P, _P, _P]),
     "hb_mix_layers": (_I, [_P, _P, _P, _I, _I, _I, _P, _P]),
     "hb_integral_image": (_I, [_P, _I, _I, _I, _P, _P]),
     "hb_used_cells": (_I, [_P, _P, _I, _I, _I, _D, _P, _P]),

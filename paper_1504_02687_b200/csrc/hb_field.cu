@@ -368,6 +368,285 @@ box_kernel(const double *__restrict__ table, int nv, int nu, int radius,
     if (peak) block_peak(peak + l, m);
 }
 
+// ---- exact integer first pass ----------------------------------------------
+// The first pass smooths H = M * G where G are integer group counts and every
+// partial sum is exact (the caller's guard: |H| < 2^24 quanta).  Its float64
+// integral table then holds exact multiples of the quantum (< 2^53 of them),
+// so the reference's box sum ((T11 - T01) - T10) + T00 is the EXACT window
+// sum -- computable in any order, with integers, and no float64 fold chain.
+//
+// box_int_kernel: one CTA per (TV x TU output tile, layer).  The input region
+// (tile + radius halo on every side; zero outside the grid) is staged in
+// shared memory (cp.async, or computed there as Hi = sum_b mix[l,b] * G[b]
+// for a mixing matrix), then
+//   vertical  : a thread per region column slides a (2r+1)-row window down
+//               the tile's rows -> W (int32, shared)
+//   horizontal: a thread per (row, 32-column chunk) slides a (2r+1)-column
+//               window along W (int64) and writes float32(S * scale / area)
+//               (the reference's quotient, box_quotient_f32).
+// The guard -- any cell with sum_b |mix[l,b]| * G[b] >= limit, or a negative
+// count -- sets HB_STATUS_INEXACT; each cell is checked by exactly one tile.
+constexpr int kBoxIntTU = 128;   // output columns per CTA
+constexpr int kBoxIntThreads = 256;
+constexpr int kBoxIntMaxSmem = 220 * 1024;
+#ifndef HB_BOX_INT_TILE_MAX_RADIUS
+#define HB_BOX_INT_TILE_MAX_RADIUS 32  // larger radii take the separable vwin/hwin pair
+#endif
+constexpr int kBoxIntTileMaxRadius = HB_BOX_INT_TILE_MAX_RADIUS;
+
+__host__ __device__ __forceinline__ int box_int_pitch(int radius) {
+    return (kBoxIntTU + 2 * radius) | 1;  // odd: conflict-free column walks
+}
+__host__ __device__ __forceinline__ size_t box_int_smem(int tv, int radius) {
+    const int pitch = box_int_pitch(radius);
+    return sizeof(int32_t) * ((size_t)(tv + 2 * radius) * pitch + (size_t)tv * pitch);
+}
+
+template <bool MIX>
+__global__ void __launch_bounds__(kBoxIntThreads)
+box_int_kernel(const int32_t *__restrict__ counts, const int32_t *__restrict__ mix, int nb,
+               int nv, int nu, int radius, int tv, double scale, double limit,
+               int32_t *__restrict__ status, float *__restrict__ out, float *__restrict__ peak) {
+    extern __shared__ int32_t sm[];
+    const int pitch = box_int_pitch(radius);
+    const int rows_in = tv + 2 * radius, cols_in = kBoxIntTU + 2 * radius;
+    int32_t *in = sm;                              // rows_in x pitch
+    int32_t *wv = sm + (size_t)rows_in * pitch;    // tv x pitch
+    const int u0 = blockIdx.x * kBoxIntTU, v0 = blockIdx.y * tv, l = blockIdx.z;
+    const int ub = u0 - radius, vb = v0 - radius;  // region origin (may be < 0)
+    const int64_t plane = (int64_t)nv * nu;
+    bool bad = false;
+    // 1. stage the region
+    const int n_in = rows_in * cols_in;
+    for (int k = threadIdx.x; k < n_in; k += kBoxIntThreads) {
+        const int rr = k / cols_in, cc = k - rr * cols_in;
+        const int v = vb + rr, u = ub + cc;
+        const bool inside = (unsigned)v < (unsigned)nv && (unsigned)u < (unsigned)nu;
+        const int64_t off = (int64_t)v * nu + u;
+        if (!MIX) {
+            const unsigned sa = (unsigned)__cvta_generic_to_shared(in + rr * pitch + cc);
+            asm volatile("cp.async.ca.shared.global [%0], [%1], 4, %2;\n" ::"r"(sa),
+                         "l"(inside ? counts + l * plane + off : counts), "r"(inside ? 4 : 0));
+        } else {
+            long long acc = 0;
+            double a = 0.0;
+            if (inside)
+                for (int b = 0; b < nb; ++b) {
+                    const int32_t c = __ldg(counts + b * plane + off);
+                    const int32_t m = __ldg(mix + l * nb + b);
+                    acc += (long long)m * c;
+                    a += fabs((double)m) * (double)c;
+                    bad |= c < 0;
+                }
+            // own cells only: the guard sees each cell once
+            if (rr >= radius && rr < radius + tv && cc >= radius && cc < radius + kBoxIntTU)
+                bad |= a >= limit;
+            in[rr * pitch + cc] = (int32_t)acc;
+        }
+    }
+    if (!MIX) {
+        asm volatile("cp.async.commit_group;\n" ::);
+        asm volatile("cp.async.wait_group 0;\n" ::);
+    }
+    __syncthreads();
+    // 2. vertical window sums of every region column for the tile's rows
+    for (int c = threadIdx.x; c < cols_in; c += kBoxIntThreads) {
+        if (!MIX && c >= radius && c < radius + kBoxIntTU)  // the guard on own cells
+            for (int t = 0; t < tv; ++t) {
+                const int32_t x = in[(t + radius) * pitch + c];
+                bad |= x < 0 || (double)x >= limit;
+            }
+        int32_t w = 0;
+        for (int rr = 0; rr <= 2 * radius; ++rr) w += in[rr * pitch + c];
+        wv[c] = w;
+        for (int t = 1; t < tv; ++t) {
+            w += in[(t + 2 * radius) * pitch + c] - in[(t - 1) * pitch + c];
+            wv[t * pitch + c] = w;
+        }
+    }
+    __syncthreads();
+    // 3. horizontal window sums along W, quotient, store
+    const double area = (double)((2 * radius + 1) * (2 * radius + 1));
+    const double inv_area = __drcp_rn(area);
+    float m = 0.0f;
+    const int chunks = kBoxIntTU / 32;
+    for (int job = threadIdx.x; job < tv * chunks; job += kBoxIntThreads) {
+        // warps walk 32 different rows of the same chunk (odd pitch: no conflicts)
+        const int t = (job / (32 * chunks)) * 32 + (job & 31);
+        const int ch = (job >> 5) % chunks;
+        if (t >= tv) continue;
+        const int v = v0 + t;
+        const int32_t *row = wv + t * pitch + ch * 32;  // region column of output ch*32 - r
+        long long w = 0;
+        for (int k = 0; k <= 2 * radius; ++k) w += row[k];
+        float vals[32];
+#pragma unroll
+        for (int j = 0; j < 32; ++j) {
+            if (j) w += (long long)row[j + 2 * radius] - row[j - 1];
+            const float val = box_quotient_f32(dmul((double)w, scale), area, inv_area);
+            vals[j] = val;
+            m = fmaxf(m, val > 0.0f ? val : 0.0f);
+        }
+        const int u = u0 + ch * 32;
+        if (v < nv) {
+            float *o = out + l * plane + (int64_t)v * nu + u;
+            if (u + 32 <= nu && (nu % 4) == 0) {
+#pragma unroll
+                for (int j = 0; j < 32; j += 4)
+                    *reinterpret_cast<float4 *>(o + j) =
+                        make_float4(vals[j], vals[j + 1], vals[j + 2], vals[j + 3]);
+            } else {
+#pragma unroll
+                for (int j = 0; j < 32; ++j)
+                    if (u + j < nu) o[j] = vals[j];
+            }
+        }
+    }
+    if (status && __any_sync(0xffffffffu, bad) && (threadIdx.x & 31) == 0)
+        atomicOr(status, HB_STATUS_INEXACT);
+    if (peak) block_peak(peak + l, m);
+}
+
+// Large radii: the tile's halo dominates (r = 50: a 64 x 128 tile stages
+// 164 x 228 cells in 209 KB, one CTA per SM), so the same exact sums are
+// taken separably through an int32 buffer in global memory (L2):
+//   vwin_int : a thread per column slides a (2r+1)-row window down kVwinRows
+//              rows (loads unrolled ahead, the outgoing row is an L1 hit)
+//   hwin_int : a CTA stages kHwinRows rows of W in shared memory (padded by
+//              one word per 32 so 32-column chunks hit distinct banks) and a
+//              thread per (row, 32-column chunk) slides the row window.
+constexpr int kVwinRows = 64;
+constexpr int kVwinThreads = 128;
+// Hi of one cell (MIX: sum_b mix[l,b] * G[b]; the guard's |.|-sum in `a`)
+template <bool MIX>
+__device__ __forceinline__ int32_t hi_cell(const int32_t *__restrict__ g, int64_t plane,
+                                           const int32_t *__restrict__ mixrow, int nb,
+                                           double &a, bool &neg) {
+    if (!MIX) return __ldg(g);
+    long long acc = 0;
+    for (int b = 0; b < nb; ++b) {
+        const int32_t c = __ldg(g + b * plane);
+        const int32_t m = __ldg(mixrow + b);
+        acc += (long long)m * c;
+        a += fabs((double)m) * (double)c;
+        neg |= c < 0;
+    }
+    return (int32_t)acc;
+}
+
+template <bool MIX>
+__global__ void __launch_bounds__(kVwinThreads)
+vwin_int_kernel(const int32_t *__restrict__ counts, const int32_t *__restrict__ mix, int nb,
+                int nv, int nu, int radius, double limit, int32_t *__restrict__ status,
+                int32_t *__restrict__ wout) {
+    const int u = blockIdx.x * kVwinThreads + threadIdx.x;
+    const int v0 = blockIdx.y * kVwinRows;
+    const int l = blockIdx.z;
+    const int64_t plane = (int64_t)nv * nu;
+    bool bad = false;
+    if (u < nu) {
+        const int v1 = min(v0 + kVwinRows, nv);
+        // groups of layer 0 at column u (MIX) or this layer's counts
+        const int32_t *col = counts + (MIX ? 0 : l * plane) + u;
+        const int32_t *mixrow = MIX ? mix + l * nb : nullptr;
+        double a = 0.0;
+        bool neg = false;
+        // the guard, on this thread's own cells (each cell once)
+        {
+            const int32_t *p = col + (int64_t)v0 * nu;
+            for (int v = v0; v < v1; ++v, p += nu) {
+                double av = 0.0;
+                const int32_t x = hi_cell<MIX>(p, plane, mixrow, nb, av, neg);
+                bad |= MIX ? av >= limit : (x < 0 || (double)x >= limit);
+            }
+            bad |= neg;
+        }
+        int32_t w = 0;
+        const int ra = max(v0 - radius, 0), rb = min(v0 + radius, nv - 1);
+        const int32_t *p = col + (int64_t)ra * nu;
+#pragma unroll 8
+        for (int v = ra; v <= rb; ++v, p += nu) w += hi_cell<MIX>(p, plane, mixrow, nb, a, neg);
+        int32_t *dst = wout + l * plane + (int64_t)v0 * nu + u;
+        *dst = w;
+        // slide: row v + radius enters, row v - radius - 1 leaves
+        const int32_t *pin = col + (int64_t)(v0 + 1 + radius) * nu;
+        const int32_t *pout = col + (int64_t)(v0 - radius) * nu;
+#pragma unroll 8
+        for (int v = v0 + 1; v < v1; ++v) {
+            dst += nu;
+            const int32_t xin = v + radius < nv ? hi_cell<MIX>(pin, plane, mixrow, nb, a, neg) : 0;
+            const int32_t xout = v - radius - 1 >= 0 ? hi_cell<MIX>(pout, plane, mixrow, nb, a, neg)
+                                                     : 0;
+            w += xin - xout;
+            *dst = w;
+            pin += nu;
+            pout += nu;
+        }
+    }
+    if (status && __any_sync(0xffffffffu, bad) && (threadIdx.x & 31) == 0)
+        atomicOr(status, HB_STATUS_INEXACT);
+}
+
+constexpr int kHwinRows = 4;
+constexpr int kHwinThreads = 256;
+__host__ __device__ __forceinline__ int hwin_pitch(int nu) {  // padded row length
+    return nu + (nu + 31) / 32 + 1;
+}
+__device__ __forceinline__ int hwin_ix(int j) { return j + (j >> 5); }
+
+__global__ void __launch_bounds__(kHwinThreads)
+hwin_int_kernel(const int32_t *__restrict__ win, int nv, int nu, int radius, double scale,
+                float *__restrict__ out, float *__restrict__ peak) {
+    extern __shared__ int32_t srow[];
+    const int pitch = hwin_pitch(nu);
+    const int vb = blockIdx.x * kHwinRows, l = blockIdx.y;
+    const int64_t plane = (int64_t)nv * nu;
+    const int nr = min(kHwinRows, nv - vb);
+    const int32_t *src = win + l * plane + (int64_t)vb * nu;
+    for (int t = 0; t < nr; ++t)
+        for (int j = threadIdx.x; j < nu; j += kHwinThreads)
+            srow[t * pitch + hwin_ix(j)] = __ldg(src + (int64_t)t * nu + j);
+    __syncthreads();
+    const double area = (double)((2 * radius + 1) * (2 * radius + 1));
+    const double inv_area = __drcp_rn(area);
+    const int chunks = (nu + 31) / 32;
+    float m = 0.0f;
+    for (int job = threadIdx.x; job < nr * chunks; job += kHwinThreads) {
+        const int t = job / chunks, ch = job - t * chunks;
+        const int32_t *row = srow + t * pitch;
+        const int u0 = ch * 32;
+        long long w = 0;  // (2r+1)^2 cells: may pass 2^31
+        {
+            const int ja = max(u0 - radius, 0), jb = min(u0 + radius, nu - 1);
+            for (int j = ja; j <= jb; ++j) w += row[hwin_ix(j)];
+        }
+        float *o = out + l * plane + (int64_t)(vb + t) * nu + u0;
+        const bool full = u0 + 32 <= nu && (nu % 4) == 0;
+        float4 q;
+#pragma unroll
+        for (int k = 0; k < 32; ++k) {
+            const int u = u0 + k;
+            if (k) {
+                const int jin = u + radius, jout = u - radius - 1;
+                w += (long long)(jin < nu ? row[hwin_ix(jin)] : 0) -
+                     (jout >= 0 ? row[hwin_ix(jout)] : 0);
+            }
+            const float val = box_quotient_f32(dmul((double)w, scale), area, inv_area);
+            m = fmaxf(m, (u < nu && val > 0.0f) ? val : 0.0f);
+            if ((k & 3) == 0) q.x = val;
+            else if ((k & 3) == 1) q.y = val;
+            else if ((k & 3) == 2) q.z = val;
+            else q.w = val;
+            if (full) {
+                if ((k & 3) == 3) *reinterpret_cast<float4 *>(o + k - 3) = q;
+            } else if (u < nu) {
+                o[k] = val;
+            }
+        }
+    }
+    if (peak) block_peak(peak + l, m);
+}
+
 // radius-0 pass (raster.py:157-158 returns a copy) and stand-alone layer
 // mixing (the raw histogram H of raster.accumulate_edges).
 template <typename T>
@@ -479,6 +758,17 @@ static unsigned col_fold_blocks(int nbins, int nu) {
 
 static inline cudaStream_t as_stream(void *s) { return reinterpret_cast<cudaStream_t>(s); }
 
+// One float box pass (raster.py:147-169) of every layer: column fold, row
+// fold (float64 table), 4-term box / area -> dst (+ layer peaks).
+static void float_box_pass(const float *fin, int nbins, int nv, int nu, int r, float *dst,
+                           double *table, float *pk, cudaStream_t st) {
+    col_fold_kernel<<<col_fold_blocks(nbins, nu), kColWarps * 32, 0, st>>>(fin, nbins, nv, nu,
+                                                                           table);
+    launch_row_fold(table, (int64_t)nbins * nv, nu, st);
+    dim3 gb((nu + kBoxBlock - 1) / kBoxBlock, (nv + kBoxRows - 1) / kBoxRows, nbins);
+    box_kernel<<<gb, kBoxBlock, 0, st>>>(table, nv, nu, r, dst, pk);
+}
+
 extern "C" {
 
 size_t hb_smooth_workspace_bytes(int nbins, int nv, int nu) {
@@ -534,14 +824,96 @@ int hb_smooth(const int32_t *counts, const float *hist, const float *matrix, int
                                                               nullptr);
                 fin = stage;
             }
-            col_fold_kernel<<<col_fold_blocks(nbins, nu), kColWarps * 32, 0, st>>>(fin, nbins, nv,
-                                                                                   nu, table);
-            const int64_t rows = (int64_t)nbins * nv;
-            launch_row_fold(table, rows, nu, st);
-            dim3 gb((nu + kBoxBlock - 1) / kBoxBlock, (nv + kBoxRows - 1) / kBoxRows, nbins);
-            box_kernel<<<gb, kBoxBlock, 0, st>>>(table, nv, nu, r, dst, pk);
+            float_box_pass(fin, nbins, nv, nu, r, dst, table, pk, st);
         }
         int rc = check_launch("hb_smooth", r == 0 ? 1 : (mix_first ? 4 : 3));
+        if (rc) return rc;
+        src = dst;
+    }
+    return HB_OK;
+}
+
+int hb_smooth_counts(const int32_t *counts, const int32_t *mix, double scale, double limit,
+                     int nbins, int nv, int nu, const int32_t *radii, int npasses, float *out,
+                     void *workspace, size_t workspace_bytes, float *layer_peak, int32_t *status,
+                     void *stream) {
+    if (!counts || nbins < 1 || nv < 1 || nu < 1 || nv > kMaxDim || nu > kMaxDim ||
+        npasses < 1 || !radii || !out || !(scale > 0.0))
+        return set_error(HB_EINVAL, "hb_smooth_counts: bad arguments");
+    int sexp = 0;
+    if (frexp(scale, &sexp) != 0.5) return set_error(HB_EINVAL, "hb_smooth_counts: scale must be 2^k");
+    if (!workspace || workspace_bytes < hb_smooth_workspace_bytes(nbins, nv, nu))
+        return set_error(HB_EINVAL, "hb_smooth_counts: workspace too small");
+    for (int p = 0; p < npasses; ++p)
+        if (radii[p] < 0) return set_error(HB_EINVAL, "radius must be >= 0");
+    if (radii[0] == 0) return set_error(HB_EINVAL, "hb_smooth_counts: first radius must be > 0");
+    cudaStream_t st = as_stream(stream);
+    const int64_t plane = (int64_t)nv * nu;
+    const size_t cells = (size_t)nbins * plane;
+    double *table = reinterpret_cast<double *>(workspace);
+    float *stage = reinterpret_cast<float *>(table + cells);
+    if (layer_peak && cudaMemsetAsync(layer_peak, 0, sizeof(float) * nbins, st) != cudaSuccess)
+        return check_launch("hb_smooth_counts(memset)", 0);
+    // pass 0: exact integer window sums in shared-memory tiles
+    {
+        float *dst = ((npasses - 1) % 2 == 0) ? out : stage;
+        float *pk = npasses == 1 ? layer_peak : nullptr;
+        const int r = radii[0];
+        int tv = 64;
+        while (tv > 8 && box_int_smem(tv, r) > (size_t)kBoxIntMaxSmem) tv >>= 1;
+        const size_t smem = box_int_smem(tv, r);
+        const bool sums_fit = (double)(2 * r + 1) * limit < 2147483647.0;
+        const size_t hsm = sizeof(int32_t) * (size_t)kHwinRows * hwin_pitch(nu);
+        if (sums_fit && r > kBoxIntTileMaxRadius && hsm <= (size_t)kBoxIntMaxSmem) {
+            if (cudaFuncSetAttribute(hwin_int_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     kBoxIntMaxSmem) != cudaSuccess)
+                return check_launch("hb_smooth_counts(smem)", 0);
+            int32_t *w = reinterpret_cast<int32_t *>(table);
+            dim3 gv((nu + kVwinThreads - 1) / kVwinThreads, (nv + kVwinRows - 1) / kVwinRows,
+                    nbins);
+            if (mix)
+                vwin_int_kernel<true><<<gv, kVwinThreads, 0, st>>>(counts, mix, nbins, nv, nu, r,
+                                                                  limit, status, w);
+            else
+                vwin_int_kernel<false><<<gv, kVwinThreads, 0, st>>>(counts, mix, nbins, nv, nu, r,
+                                                                   limit, status, w);
+            hwin_int_kernel<<<dim3((nv + kHwinRows - 1) / kHwinRows, nbins), kHwinThreads, hsm,
+                              st>>>(w, nv, nu, r, scale, dst, pk);
+            int rc = check_launch("hb_smooth_counts", 2);
+            if (rc) return rc;
+        } else if (sums_fit && smem <= (size_t)kBoxIntMaxSmem) {
+            if (cudaFuncSetAttribute(box_int_kernel<false>,
+                                     cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     kBoxIntMaxSmem) != cudaSuccess ||
+                cudaFuncSetAttribute(box_int_kernel<true>,
+                                     cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     kBoxIntMaxSmem) != cudaSuccess)
+                return check_launch("hb_smooth_counts(smem)", 0);
+            dim3 g((nu + kBoxIntTU - 1) / kBoxIntTU, (nv + tv - 1) / tv, nbins);
+            if (mix)
+                box_int_kernel<true><<<g, kBoxIntThreads, smem, st>>>(
+                    counts, mix, nbins, nv, nu, r, tv, scale, limit, status, dst, pk);
+            else
+                box_int_kernel<false><<<g, kBoxIntThreads, smem, st>>>(
+                    counts, mix, nbins, nv, nu, r, tv, scale, limit, status, dst, pk);
+            int rc = check_launch("hb_smooth_counts", 1);
+            if (rc) return rc;
+        } else {
+            return set_error(HB_EINVAL, "hb_smooth_counts: radius too large for the integer pass");
+        }
+    }
+    const float *src = ((npasses - 1) % 2 == 0) ? out : stage;
+    for (int p = 1; p < npasses; ++p) {
+        float *dst = ((npasses - 1 - p) % 2 == 0) ? out : stage;
+        float *pk = (p == npasses - 1) ? layer_peak : nullptr;
+        const int r = radii[p];
+        if (r == 0) {
+            dim3 g((unsigned)((plane + 255) / 256), nbins);
+            mix_pass_kernel<float><<<g, 256, 0, st>>>(src, nullptr, nbins, plane, dst, pk);
+        } else {
+            float_box_pass(src, nbins, nv, nu, r, dst, table, pk, st);
+        }
+        int rc = check_launch("hb_smooth_counts", r == 0 ? 1 : 3);
         if (rc) return rc;
         src = dst;
     }

@@ -63,6 +63,17 @@ def sample_counts(src: np.ndarray, dst: np.ndarray, delta: float) -> np.ndarray:
     return np.maximum(np.ceil(seg / delta).astype(np.int64), 1) + 1
 
 
+def smooth_counts_ok(radius: int, limit: float) -> bool:
+    """Whether hb_smooth_counts takes this first pass (mirrors its checks in
+    hb_field.cu: a shared-memory tile with >= 8 rows fits 220 KB, and the
+    int32 vertical window sums (2r+1) x limit cannot overflow)."""
+    if radius <= 0 or (2 * radius + 1) * limit >= 2 ** 31 - 1:
+        return False
+    pitch = (128 + 2 * radius) | 1
+    return (4 * ((8 + 2 * radius) * pitch + 8 * pitch) <= 220 * 1024
+            or radius > 32)  # (the separable pair: 4 padded rows of <= 8192 cells)
+
+
 def ptr(t) -> int | None:
     return None if t is None else t.data_ptr()
 
@@ -299,6 +310,22 @@ class BundleEngine:
         self.mat_dev = None if mat_is_identity else upload(self.matrix, dev)
         self.absm_dev = (None if weights.abs_matrix is None
                          else upload(np.ascontiguousarray(weights.abs_matrix, np.float64), dev))
+        # exact first smoothing pass from integer window sums (hb_smooth_counts):
+        # H = scale * mix * G with an integer matrix, scale = the matrix quantum
+        self.int_mix = None
+        self.int_scale = 1.0
+        self.smooth_int = (os.environ.get("HB_SMOOTH_INT", "1") != "0"
+                           and weights.kind != "ordered")
+        if self.smooth_int and not mat_is_identity:
+            qm = _lowest_bit(self.matrix)
+            mix = self.matrix.astype(np.float64) / qm
+            if np.all(np.abs(mix) < 2 ** 31) and np.all(mix == np.round(mix)):
+                self.int_mix = upload(mix.astype(np.int32), dev)
+                self.int_scale = qm
+            else:
+                self.smooth_int = False
+        self.smooth_int = self.smooth_int and smooth_counts_ok(
+            int(self.radii[0]), weights.limit / self.int_scale)
         self.shard = shard
         e_total = E if shard is None else int(shard["edges_total"])
         self.nparts = max(1, min(int(workers), e_total)) if e_total else 1
@@ -791,6 +818,14 @@ class BundleEngine:
             self._k("hb_smooth", None, ptr(self.hist), None, B, nv, nu,
                     self.radii.data_ptr(), int(self.radii.numel()), ptr(self.field),
                     ptr(self.smooth_ws), self.smooth_ws.numel(), ptr(self.peak), s)
+            return
+        if self.smooth_int:
+            # exact integer first pass + the guard in the same launch
+            self._k("hb_smooth_counts", ptr(self.hist), ptr(self.int_mix), self.int_scale,
+                    float(self.plan.limit / self.int_scale), B, nv, nu,
+                    self.radii.data_ptr(), int(self.radii.numel()), ptr(self.field),
+                    ptr(self.smooth_ws), self.smooth_ws.numel(), ptr(self.peak),
+                    ptr(self.status), s)
             return
         self._k("hb_exact_check", ptr(self.hist), ptr(self.absm_dev), B, nv, nu,
                 float(self.plan.limit), ptr(self.status), s)

@@ -673,3 +673,46 @@ def test_sync_free_capacity_overflow_retries_exactly(monkeypatch):
     assert np.array_equal(pts2, rp)
     res = B.bundle(w.graph, cfg, bins=w.bins, matrix=w.matrix)
     assert np.array_equal(res.sampled_edges.starts, rs)
+
+@pytest.mark.parametrize("limit", [2.0 ** 24, 2.0 ** 20])
+@pytest.mark.parametrize("mixed", [False, True])
+def test_smooth_counts_integer_first_pass_matches_float_path(limit, mixed):
+    """hb_smooth_counts (exact integer first pass) equals hb_smooth (the
+    reference's float64 integral-image folds) bit for bit, and the guard
+    flags a cell past the limit."""
+    rng = np.random.default_rng(5)
+    nb, nv, nu = 3, 131, 517
+    counts = (rng.poisson(3.0, size=(nb, nv, nu)) *
+              (rng.uniform(size=(nb, nv, nu)) < 0.5)).astype(np.int32)
+    counts[1, 60:70, 100:140] += 4000  # a bundle
+    mat = (np.eye(nb) + 0.5 * (1 - np.eye(nb))).astype(np.float32) if mixed else None
+    mix = (mat * 2).astype(np.int32) if mixed else None
+    scale = 0.5 if mixed else 1.0
+    for radii in ([15, 15, 16], [1, 0, 2], [40, 41, 41], [51, 51, 51]):
+        r = torch.tensor(radii, dtype=torch.int32)
+        ws = torch.empty(int(N.lib().hb_smooth_workspace_bytes(nb, nv, nu)), dtype=torch.uint8,
+                         device="cuda")
+        c = dev(counts)
+        ref = torch.empty((nb, nv, nu), dtype=torch.float32, device="cuda")
+        got = torch.empty_like(ref)
+        pk_ref = torch.zeros(nb, dtype=torch.float32, device="cuda")
+        pk = torch.zeros_like(pk_ref)
+        status = torch.zeros(1, dtype=torch.int32, device="cuda")
+        N.call("hb_smooth", ptr(c), None, ptr(dev(mat) if mixed else None), nb, nv, nu,
+               r.data_ptr(), 3, ptr(ref), ptr(ws), ws.numel(), ptr(pk_ref), stream_ptr())
+        N.call("hb_smooth_counts", ptr(c), ptr(dev(mix) if mixed else None), scale, limit, nb,
+               nv, nu, r.data_ptr(), 3, ptr(got), ptr(ws), ws.numel(), ptr(pk), ptr(status),
+               stream_ptr())
+        sync()
+        assert torch.equal(got, ref), radii
+        assert torch.equal(pk, pk_ref)
+        assert int(status.item()) == 0
+    r3 = torch.tensor([3, 3, 3], dtype=torch.int32)
+    with pytest.raises(N.NativeError):  # int32 window sums could overflow: refused
+        N.call("hb_smooth_counts", ptr(dev(counts)), None, 1.0, 2.0 ** 40, nb, nv, nu,
+               r3.data_ptr(), 3, ptr(got), ptr(ws), ws.numel(), None, None, stream_ptr())
+    status = torch.zeros(1, dtype=torch.int32, device="cuda")
+    N.call("hb_smooth_counts", ptr(dev(counts)), None, 1.0, 4000.0, nb, nv, nu,
+           r3.data_ptr(), 3, ptr(got), ptr(ws), ws.numel(), None, ptr(status), stream_ptr())
+    sync()
+    assert int(status.item()) & 8  # 4000+ counts reach the limit

@@ -1,15 +1,16 @@
-"""SVG rendering of a bundling result: the API of the reference's ``render.py``.
+"""SVG and PNG rendering of a bundling result: the API of the reference's ``render.py``.
 
 Mirrors ``/root/reference/pkg/src/histobundle/render.py`` (``ColorScheme``,
-``RenderOptions``, ``color_for_bin``, ``width_for_segment``, ``render_svg``;
-same arguments and the same SVG text, checked byte for byte against
+``RenderOptions``, ``color_for_bin``, ``width_for_segment``, ``render_svg``,
+``render_png``; same arguments and the same SVG text / image bytes, checked byte for byte against
 fixtures made by the reference, tests/golden/make_render_golden.py).  The
 per-segment stroke widths -- a clamped bilinear density sample at both ends
 of every segment -- are computed on the device (``hb_segment_widths``);
 colours, alpha and the text are host work, as in the reference.
 
-``render_png`` draws with PIL's rasteriser, which is not installed in this
-image, so its output cannot be pinned here; it raises.
+``render_png`` computes the same device widths and draws every edge with
+PIL's rasteriser (the reference's), compositing the per-edge tiles in edge
+order: byte-identical images (tests/golden/make_render_golden.py).
 """
 
 from __future__ import annotations
@@ -244,6 +245,74 @@ def render_svg(result, scheme: ColorScheme | None = None,
 
 def render_png(result, scheme: ColorScheme | None = None, options: RenderOptions | None = None,
                size: tuple[int, int] | None = None):
-    """Raster backend of render.py:263-335 (PIL's line and ellipse drawing)."""
-    raise NotImplementedError("render_png composites with PIL's rasteriser, which is not "
-                              "available here; use render_svg")
+    """Raster image with source-over alpha accumulation (render.py:263-335).
+
+    Every polyline's segment widths come from one device call (as in
+    :func:`render_svg`); each edge is then drawn on its own transparent tile
+    with PIL's line and disc rasteriser -- the reference's, so the pixels are
+    the same -- and composited onto the canvas in edge order, so overlapping
+    edges darken each other while one edge's own overlaps do not accumulate.
+    Returns a PIL RGBA image."""
+    from PIL import Image, ImageDraw
+
+    scheme = scheme or ColorScheme()
+    opts = options or RenderOptions()
+    graph, field = result.graph, result.density
+    tr = field.transform
+    x0, y0, w, h = tr.world_bounds()
+    if size is None:
+        size = (tr.width, tr.height)
+    width_px, height_px = int(size[0]), int(size[1])
+    if width_px <= 0 or height_px <= 0:
+        raise ValueError("image dimensions must be positive")
+    alpha = opts.resolve_alpha(graph.n_edges)
+    px_per_cell = width_px / tr.width
+    flow = scheme.kind == "flow-blue-red"
+    bg = (0, 0, 0, 0)
+    if opts.background:
+        r, g, b = _hex_to_unit(opts.background)
+        bg = (int(r * 255), int(g * 255), int(b * 255), 255)
+    canvas = Image.new("RGBA", (width_px, height_px), bg)
+    edges = list(result.sampled_edges)
+    if not edges:
+        return canvas
+    counts = np.array([len(se) for se in edges], dtype=np.int64)
+    starts = np.concatenate([[0], np.cumsum(counts)])
+    grid = tr.world_to_grid(np.concatenate([se.points for se in edges]))
+    layers = np.array([int(graph.bins[se.edge_index]) for se in edges], dtype=np.int32)
+    seg_w = _DeviceWidths(field).widths(grid, starts, layers, opts.width_min, opts.width_max,
+                                        opts.log_widths)
+    seg_off = starts[:-1] - np.arange(len(edges))
+    a8 = int(round(alpha * 255))
+    for k, se in enumerate(edges):
+        b = int(layers[k])
+        px = (se.points[:, 0] - x0) / w * width_px
+        py = (1.0 - (se.points[:, 1] - y0) / h) * height_px
+        widths_px = np.maximum(seg_w[seg_off[k]:seg_off[k] + len(se) - 1] * px_per_cell, 1.0)
+        margin = int(math.ceil(widths_px.max() / 2)) + 2
+        tx0 = max(int(math.floor(px.min())) - margin, 0)
+        ty0 = max(int(math.floor(py.min())) - margin, 0)
+        tx1 = min(int(math.ceil(px.max())) + margin, width_px)
+        ty1 = min(int(math.ceil(py.max())) + margin, height_px)
+        if tx1 <= tx0 or ty1 <= ty0:
+            continue
+        tile = Image.new("RGBA", (tx1 - tx0, ty1 - ty0), (0, 0, 0, 0))
+        draw = ImageDraw.Draw(tile)
+        if not flow:
+            rgba = color_for_bin(scheme, b, field.bin_count)
+            fill = (int(rgba[0] * 255), int(rgba[1] * 255), int(rgba[2] * 255), a8)
+        arc = _arc_fraction(se.points) if flow else None
+        for j in range(len(se) - 1):
+            if flow:
+                r, g, bb = _flow_color(0.5 * (arc[j] + arc[j + 1]))
+                fill = (int(r * 255), int(g * 255), int(bb * 255), a8)
+            lw = int(round(widths_px[j]))
+            draw.line([(px[j] - tx0, py[j] - ty0), (px[j + 1] - tx0, py[j + 1] - ty0)],
+                      fill=fill, width=max(lw, 1))
+            if lw > 2:  # round joins and caps
+                rr = lw / 2.0
+                for q in (j, j + 1):
+                    draw.ellipse([px[q] - tx0 - rr, py[q] - ty0 - rr,
+                                  px[q] - tx0 + rr, py[q] - ty0 + rr], fill=fill)
+        canvas.alpha_composite(tile, (tx0, ty0))
+    return canvas

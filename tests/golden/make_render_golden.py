@@ -1,10 +1,9 @@
-"""SVG rendering fixtures made by running the REFERENCE (render.py) here.
+"""SVG and PNG rendering fixtures made by running the REFERENCE (render.py) here.
 
     python tests/golden/make_render_golden.py
 
-render.py imports PIL at module level for its raster backend; PIL is not
-installed in this image, so a stub module stands in for the import (render_svg
-and the width helpers never touch it).  The bundling result comes from the
+PNG cases use the reference's render_png (pillow 12.2, recorded); the raw
+RGBA bytes are hashed.  The bundling result comes from the
 reference's own bundle() on a 100-edge config-1 graph (seed 0) -- the device
 path reproduces it bit for bit, so both renderers see the same input.
 Writes tests/golden/render.npz: per option set, the sha256 and length of the
@@ -16,7 +15,6 @@ from __future__ import annotations
 import hashlib
 import os
 import sys
-import types
 
 import numpy as np
 
@@ -24,12 +22,6 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 REPO = os.path.dirname(os.path.dirname(HERE))
 sys.path.insert(0, "/root/reference/pkg/src")
 sys.path.insert(0, REPO)
-
-if "PIL" not in sys.modules:  # render_svg does not use PIL
-    pil = types.ModuleType("PIL")
-    pil.Image = types.ModuleType("PIL.Image")
-    pil.ImageDraw = types.ModuleType("PIL.ImageDraw")
-    sys.modules.update({"PIL": pil, "PIL.Image": pil.Image, "PIL.ImageDraw": pil.ImageDraw})
 
 from histobundle import bundler as RB  # noqa: E402
 from histobundle import model as RM  # noqa: E402
@@ -46,6 +38,16 @@ CASES = [
     ("flow", "flow-blue-red", {"width_min": 0.5, "width_max": 3.0}, 1),
     ("logw", "nominal", {"log_widths": True}, 1),
 ]
+
+
+# render_png cases: (name, scheme kind, RenderOptions kwargs, bins per edge)
+PNG_CASES = [
+    ("default", "nominal", {}, 1),
+    ("modal", "modal-hue", {"alpha": 0.3}, 3),
+    ("flow_wide", "flow-blue-red", {"width_min": 0.5, "width_max": 6.0, "background": None}, 1),
+    ("sequential_big", "sequential", {"width_min": 1.0, "width_max": 9.0}, 3),
+]
+PNG_SIZES = {"sequential_big": (600, 420), "flow_wide": (333, 250)}
 
 
 def graph_for(bins_n):
@@ -71,6 +73,15 @@ def main():
         out[f"{name}_len"] = np.array(len(svg))
         if name == "default":
             out["default_svg"] = np.array(svg)
+    import PIL
+    out["pillow"] = np.array(PIL.__version__)
+    for name, kind, opts, bins_n in PNG_CASES:
+        img = RR.render_png(results[bins_n], RR.ColorScheme(kind=kind), RR.RenderOptions(**opts),
+                            size=PNG_SIZES.get(name))
+        raw = img.tobytes()
+        out[f"png_{name}_sha"] = np.array(hashlib.sha256(raw).hexdigest())
+        out[f"png_{name}_size"] = np.array(img.size)
+        out[f"png_{name}_mode"] = np.array(img.mode)
     res = results[1]
     peaks = RR._layer_peaks(res.density)
     ws = []

@@ -98,3 +98,55 @@ def test_width_for_segment_matches_reference():
     got = [[PR.width_for_segment(res.density, 0, a, b, 0.6, 4.0, lg) for a, b in G["wfs_probes"]]
            for lg in (False, True)]
     assert np.array_equal(np.array(got), G["wfs"])
+
+
+PNG_CASES = {  # must match make_render_golden.PNG_CASES / PNG_SIZES
+    "default": ("nominal", {}, 1, None),
+    "modal": ("modal-hue", {"alpha": 0.3}, 3, None),
+    "flow_wide": ("flow-blue-red", {"width_min": 0.5, "width_max": 6.0, "background": None}, 1,
+                  (333, 250)),
+    "sequential_big": ("sequential", {"width_min": 1.0, "width_max": 9.0}, 3, (600, 420)),
+}
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("name", list(PNG_CASES))
+def test_render_png_matches_reference(name):
+    """render_png (render.py:263-335): device stroke widths, per-edge tiles
+    drawn with PIL and composited in edge order -- the same RGBA bytes as the
+    reference's image."""
+    torch = pytest.importorskip("torch")
+    if not torch.cuda.is_available():
+        pytest.skip("needs a CUDA device")
+    import PIL
+
+    from paper_1504_02687_b200 import render as PR
+
+    if str(G["pillow"]) != PIL.__version__:
+        pytest.skip(f"fixture made with pillow {G['pillow']}, found {PIL.__version__}")
+    kind, opts, bins_n, size = PNG_CASES[name]
+    img = PR.render_png(_result(bins_n), PR.ColorScheme(kind=kind), PR.RenderOptions(**opts),
+                        size=size)
+    assert img.mode == str(G[f"png_{name}_mode"])
+    assert list(img.size) == list(G[f"png_{name}_size"])
+    assert hashlib.sha256(img.tobytes()).hexdigest() == str(G[f"png_{name}_sha"])
+
+
+def test_render_png_rejects_empty_size():
+    from paper_1504_02687_b200 import render as PR
+
+    class R:  # the size check comes before any drawing
+        class graph:
+            n_edges = 1
+
+        class density:
+            class transform:
+                width, height = 10, 10
+
+                @staticmethod
+                def world_bounds():
+                    return (0.0, 0.0, 1.0, 1.0)
+        sampled_edges = []
+
+    with pytest.raises(ValueError, match="image dimensions must be positive"):
+        PR.render_png(R, size=(0, 5))

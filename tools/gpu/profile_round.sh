@@ -1,6 +1,5 @@
 # Round profile: bench line, ncu launch list, ncu --set full of the top kernels.
 mkdir -p gpurun_out
-timeout 900 python -m pytest tests -m gpu -x -q 2>&1 | tail -1
 timeout 900 python bench.py > gpurun_out/pr_bench.json 2> gpurun_out/pr_bench.err; echo bench rc=$?
 timeout 1200 ncu --metrics gpu__time_duration.sum --clock-control none -c 600 --csv \
   --log-file gpurun_out/pr_launches.csv python bench.py --steps 1 --warmup 3 --no-e2e --no-cpu-baseline \

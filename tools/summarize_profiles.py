@@ -29,7 +29,16 @@ WANT = ["Duration", "DRAM Throughput", "Memory Throughput", "L2 Hit Rate", "L1/T
 RAW = ["dram__bytes_read.sum", "dram__bytes_write.sum", "smsp__inst_executed.sum",
        "sm__inst_executed_pipe_fp64.avg.pct_of_peak_sustained_active",
        "lts__t_sectors_srcunit_tex_op_red.sum", "lts__throughput.avg.pct_of_peak_sustained_elapsed",
-       "gpu__time_duration.sum"]
+       "gpu__time_duration.sum",
+       # the L1 ceiling of gather-bound kernels: wavefronts through the LSU data pipe
+       "l1tex__data_pipe_lsu_wavefronts.sum",
+       "l1tex__data_pipe_lsu_wavefronts.avg.pct_of_peak_sustained_elapsed",
+       "l1tex__data_pipe_lsu_wavefronts_mem_shared.sum",
+       "l1tex__t_sectors_pipe_lsu_mem_global_op_ld.sum",
+       "l1tex__t_requests_pipe_lsu_mem_global_op_ld.sum",
+       "l1tex__throughput.avg.pct_of_peak_sustained_elapsed",
+       "lts__t_sectors.avg.pct_of_peak_sustained_elapsed",
+       "sm__cycles_elapsed.avg", "smsp__issue_active.avg.pct_of_peak_sustained_elapsed"]
 
 
 def ncu_csv(rep: str, page: str) -> list[list[str]]:

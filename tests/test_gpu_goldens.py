@@ -252,3 +252,35 @@ def test_ordered_accumulate_matches_reference_kat():
                                 status)
     assert np.array_equal(out.cpu().numpy(), k["raw_rep"])
     assert int(status.item()) == 0
+
+
+@pytest.mark.slow
+def test_cfg5_full_size_shard_vs_oracle():
+    """Full config 5 geometry at full density of one shard: the first of the
+    8 edge shards (2.5 M edges, dist.shard_edges) bundled on its own through
+    bundle() on the 4 x 2047 x 2048 grid, against the C oracle (the reference
+    kernels restated, every host core) on the same shard: final world points,
+    field and per-iteration counts bit-exact."""
+    import oracle as O
+    from paper_1504_02687_b200.dist import shard_edges
+    from paper_1504_02687_b200.engine import sample_counts
+    from paper_1504_02687_b200.model import make_transform
+
+    w = workload(5)
+    g, cfg = w.graph, w.config
+    tr = make_transform(g.positions, cfg.grid_size, cfg.padding_cells)
+    counts = sample_counts(tr.world_to_grid(g.positions[g.sources]),
+                           tr.world_to_grid(g.positions[g.targets]), cfg.delta)
+    lo, hi = shard_edges(counts, 8)[0]
+    bins = w.bins[lo:hi]
+    shard = Graph(g.positions, g.sources[lo:hi], g.targets[lo:hi], None, bins)
+    res = B.bundle(shard, cfg, bins=bins, matrix=w.matrix)
+    cores = len(os.sched_getaffinity(0))
+    ref = O.bundle_packed(shard.positions, shard.sources, shard.targets, shard.weights, bins, cfg,
+                          w.matrix, workers=cores)
+    world = O.materialize(ref, shard.positions, shard.sources, shard.targets)
+    assert res.sampled_edges.world.shape == world.shape
+    assert np.array_equal(res.sampled_edges.world, world)
+    assert np.array_equal(res.density.values, ref.field)
+    for m, r in zip(res.metrics, ref.metrics):
+        assert (m.moved_points, m.used_cells) == (r.moved_points, r.used_cells)

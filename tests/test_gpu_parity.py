@@ -716,3 +716,16 @@ def test_smooth_counts_integer_first_pass_matches_float_path(limit, mixed):
            r3.data_ptr(), 3, ptr(got), ptr(ws), ws.numel(), None, ptr(status), stream_ptr())
     sync()
     assert int(status.item()) & 8  # 4000+ counts reach the limit
+
+
+@pytest.mark.parametrize("env", [{"HB_QUAD_LIMIT_MB": "0"}, {"HB_FLAT_ADVECT": "0"},
+                                 {"HB_SYNC_FREE": "0"}, {"HB_SMOOTH_INT": "0"},
+                                 {"HB_STREAM_OUT": "0"}])
+def test_bundle_cfg2_bit_exact_alternate_paths(env, monkeypatch):
+    """Every switchable path gives the reference's bits: advection gathering
+    rho directly (no quad field, as for fields past the memory limit), the
+    per-edge fused advect + Laplacian kernel, synchronous point totals, the
+    float64-fold first smoothing pass, and the unstreamed result copy."""
+    for k, v in env.items():
+        monkeypatch.setenv(k, v)
+    _check_run(2)

@@ -315,19 +315,20 @@ __device__ __forceinline__ void dda_splat_cells(int x0, int y0, int x1, int y1, 
     // per-cell check.  On an axis with |d| == steps the reference's
     // floor(x0 + (k*d)*(1/steps) + 0.5) is exactly x0 + sign(d)*k: (k*d)*inv
     // differs from +-k by at most k*2^-52 << 0.5.  Only the other axis needs
-    // the float64 expression.
-    if (abs(dx) == steps) {
-        const int sx = dx > 0 ? 1 : -1;
-        for (int k = k0; k <= steps; ++k) {
-            const int v = floor_i(dadd(dadd(fy0, dmul((double)(k * dy), inv)), 0.5));
-            atomicAdd(layer + v * nu + (x0 + sx * k), w);
-        }
-    } else {
-        const int sy = dy > 0 ? 1 : -1;
-        for (int k = k0; k <= steps; ++k) {
-            const int u = floor_i(dadd(dadd(fx0, dmul((double)(k * dx), inv)), 0.5));
-            atomicAdd(layer + (y0 + sy * k) * nu + u, w);
-        }
+    // the float64 expression.  One loop for both orientations (the axes are
+    // selected, not branched on), so lanes of a warp with x- and y-dominant
+    // segments do not run two loops one after the other.
+    const bool xdom = abs(dx) == steps;
+    const int c_major = xdom ? x0 : y0;
+    const int s_major = xdom ? (dx > 0 ? 1 : -1) : (dy > 0 ? 1 : -1);
+    const int d_minor = xdom ? dy : dx;
+    const double f_minor = xdom ? fy0 : fx0;
+    (void)fx0;
+    for (int k = k0; k <= steps; ++k) {
+        const int major = c_major + s_major * k;
+        const int minor = floor_i(dadd(dadd(f_minor, dmul((double)(k * d_minor), inv)), 0.5));
+        const int u = xdom ? major : minor, v = xdom ? minor : major;
+        atomicAdd(layer + v * nu + u, w);
     }
 }
 
@@ -351,16 +352,16 @@ __device__ __forceinline__ void dda_walk(int x0, int y0, int x1, int y1, int k0,
         return;
     }
     const double inv = 1.0 / (double)steps;
-    if (abs(dx) == steps) {
-        const int sx = dx > 0 ? 1 : -1;
-        const double fy0 = (double)y0;
-        for (int k = k0; k <= steps; ++k)
-            visit(x0 + sx * k, floor_i(dadd(dadd(fy0, dmul((double)(k * dy), inv)), 0.5)));
-    } else {
-        const int sy = dy > 0 ? 1 : -1;
-        const double fx0 = (double)x0;
-        for (int k = k0; k <= steps; ++k)
-            visit(floor_i(dadd(dadd(fx0, dmul((double)(k * dx), inv)), 0.5)), y0 + sy * k);
+    // one loop, axes selected (see dda_splat_cells)
+    const bool xdom = abs(dx) == steps;
+    const int c_major = xdom ? x0 : y0;
+    const int s_major = xdom ? (dx > 0 ? 1 : -1) : (dy > 0 ? 1 : -1);
+    const int d_minor = xdom ? dy : dx;
+    const double f_minor = (double)(xdom ? y0 : x0);
+    for (int k = k0; k <= steps; ++k) {
+        const int major = c_major + s_major * k;
+        const int minor = floor_i(dadd(dadd(f_minor, dmul((double)(k * d_minor), inv)), 0.5));
+        visit(xdom ? major : minor, xdom ? minor : major);
     }
 }
 

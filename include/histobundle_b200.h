@@ -70,7 +70,7 @@ typedef struct hb_tiles {
      * keyed by (group, delta, start cell); hb_segtab_expand then rasterises
      * each non-zero key once with its multiplicity.  tab holds
      * nbins*(2*halo+1)^2*nv*nu uint32 counters, all zero between passes. */
-    int mode;            /* 0 = tile records, 1 = segment-key table */
+    int mode;            /* 0 = tile records, 1 = segment-key table, 2 = census only */
     uint32_t *tab;
 } hb_tiles;
 
@@ -153,8 +153,10 @@ HB_API int hb_splat(const double *pts, const int64_t *starts, int64_t n_edges,
              const hb_tiles *tiles, void *stream);
 /* `tiles` (nullable): with tiles->rec == NULL the splat still adds straight
  * into counts but records each tile's demand in tiles->fill (census for the
- * next hb_tiles_plan); with rec != NULL segments are binned and the caller
- * finishes with hb_tiles_flush.  hb_resample_emit takes the same argument. */
+ * next hb_tiles_plan) -- or, with mode == 2, ONLY records the demand and adds
+ * nothing (a census pass before a binned splat of the same points); with
+ * rec != NULL segments are binned and the caller finishes with
+ * hb_tiles_flush.  hb_resample_emit takes the same argument. */
 
 /* Workspace for hb_smooth: bytes of float64 tables + float32 staging. */
 HB_API size_t hb_smooth_workspace_bytes(int nbins, int nv, int nu);

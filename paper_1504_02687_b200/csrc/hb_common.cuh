@@ -462,6 +462,7 @@ atomicAdd(tl->tab + segtab_index(dir, x0, y0, nv, nu), (unsigned)iw);
                 direct = false;
             }
         }
+        if (tl->mode == 2) direct = false;  // census only: demand counted, nothing added
     }
     if (direct)
         dda_splat_cells<T>(cx0, cy0, cx1, cy1, k0, w, hist + (int64_t)grp * plane, nv, nu, status);

@@ -493,8 +493,25 @@ class BundleEngine:
             self._accumulate_ordered(s)
             return
         # Straight initial polylines have no duplicate segments, so the key
-        # table would only add its expansion: splat directly (tile mode still
-        # takes its census for the first binned pass).
+        # table would only add its expansion: splat directly.  Tile mode
+        # (long segments) bins them too: a census pass sizes the buckets,
+        # the binned splat writes records, the flush rasterises them in
+        # shared memory (the direct global atomics of ~28-cell segments were
+        # L2-atomic-bound: config 5's iteration 0 took 91 ms)
+        if self.tile_mode == 0 and os.environ.get("HB_ITER0_BINNED", "1") != "0":
+            self.t_fill.zero_()
+            census = N.HbTiles.from_buffer_copy(self.tiles_census)
+            census.mode = 2
+            self._k("hb_splat", ptr(self.pts), ptr(self.starts), E, self.n_pts,
+                    ptr(self.groups), ptr(self.wint), ptr(self.hist), B, nv, nu,
+                    ptr(self.status), ctypes.byref(census), s)
+            self._k("hb_tiles_plan", ctypes.byref(self.tiles), ptr(self.t_total), s)
+            self._ensure_records(int(download(self.t_total)[0]))
+            self._k("hb_splat", ptr(self.pts), ptr(self.starts), E, self.n_pts,
+                    ptr(self.groups), ptr(self.wint), ptr(self.hist), B, nv, nu,
+                    ptr(self.status), ctypes.byref(self.tiles), s)
+            self._k("hb_tiles_flush", ctypes.byref(self.tiles), ptr(self.hist), nv, nu, s)
+            return
         sink = None
         if self.tile_mode == 0:
             self.t_fill.zero_()

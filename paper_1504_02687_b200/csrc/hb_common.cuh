@@ -442,7 +442,10 @@ atomicAdd(tl->tab + segtab_index(dir, x0, y0, nv, nu), (unsigned)iw);
             direct = false;  // adds nothing (_kernels.py:67-71)
         } else if ((unsigned)x0 < (unsigned)nu && (unsigned)y0 < (unsigned)nv &&
                    (unsigned)(x0 + dx) < (unsigned)nu && (unsigned)(y0 + dy) < (unsigned)nv &&
-                   abs(dx) <= 127 && abs(dy) <= 127 && (T)iw == w && iw >= 1 && iw <= 0x7fff) {
+                   abs(dx) <= tl->halo && abs(dy) <= tl->halo && (T)iw == w && iw >= 1 &&
+                   iw <= 0x7fff) {
+            // (|d| <= halo: every cell of the record lies in its tile's window,
+            // so the flush needs no per-cell bounds check)
             tile = (grp * tl->nty + y0 / tl->tile) * tl->ntx + x0 / tl->tile;
             rec = encode_seg(x0, y0, dx, dy, k0, iw);
         }

@@ -82,6 +82,10 @@ tiles_worklist_kernel(const __grid_constant__ hb_tiles t) {
     }
 }
 
+__device__ __forceinline__ void red_shared(unsigned addr, int v) {
+    asm volatile("red.shared.add.s32 [%0], %1;" ::"r"(addr), "r"(v) : "memory");
+}
+
 // Persistent: CTAs pull (tile, chunk) items off a counter, rasterise the
 // chunk's records into a shared window, flush the window.
 __global__ void __launch_bounds__(kFlushBlock)
@@ -123,19 +127,40 @@ tiles_flush_kernel(const __grid_constant__ hb_tiles t, int32_t *__restrict__ cou
         const int64_t hi = lo + kChunk < (int64_t)n ? lo + kChunk : (int64_t)n;
         const uint64_t *rec = t.rec + t.off[tile];
         int32_t *layer = counts + (int64_t)g * plane;
+        // Records have |dx|, |dy| <= halo (bin_or_splat_cells), so every cell
+        // is inside the window: the walk is dda_walk's cell chain expressed as
+        // a window index, idx = base + major_step * k + minor_mul * minor(k),
+        // with minor(k) = floor(c + (k*d)*(1/steps) + 0.5) in float64 (k*d
+        // carried as an exact double), and the adds go to shared memory by
+        // address (red.shared) -- ~9 instructions per cell.
+        const unsigned swin = (unsigned)__cvta_generic_to_shared(win);
         for (int64_t k = lo + threadIdx.x; k < hi; k += kFlushBlock) {
             const uint64_t rr = rec[k];
             const int x0 = (int)(rr & 0xffff), y0 = (int)((rr >> 16) & 0xffff);
             const int dx = (int)(int8_t)((rr >> 32) & 0xff), dy = (int)(int8_t)((rr >> 40) & 0xff);
             const int k0 = (int)((rr >> 48) & 1);
             const int w = (int)(rr >> 49);
-            dda_walk(x0, y0, x0 + dx, y0 + dy, k0, [&](int u, int v) {
-                const int lu = u - wx0, lv = v - wy0;
-                if ((unsigned)lu < (unsigned)W && (unsigned)lv < (unsigned)W)
-                    atomicAdd(win + lv * W + lu, w);
-                else
-                    atomicAdd(layer + (int64_t)v * nu + u, w);
-            });
+            const int steps = max(abs(dx), abs(dy));
+            if (steps == 0) {
+                if (k0 == 0) red_shared(swin + 4u * (unsigned)((y0 - wy0) * W + (x0 - wx0)), w);
+                continue;
+            }
+            const bool xdom = abs(dx) == steps;
+            const int major_step = xdom ? (dx > 0 ? 1 : -1) : (dy > 0 ? W : -W);
+            const int minor_mul = xdom ? W : 1;
+            const int dmin = xdom ? dy : dx;
+            const double c = (double)(xdom ? y0 : x0), inv = 1.0 / (double)steps;
+            // window index of (major at k, minor = 0)
+            int base = xdom ? (x0 - wx0) - wy0 * W : (y0 - wy0) * W - wx0;
+            base += major_step * k0;
+            double kd = (double)(k0 * dmin);
+            const double dd = (double)dmin;
+            for (int kk = k0; kk <= steps; ++kk) {
+                const int minor = floor_i(dadd(dadd(c, dmul(kd, inv)), 0.5));
+                red_shared(swin + 4u * (unsigned)(base + minor_mul * minor), w);
+                base += major_step;
+                kd = dadd(kd, dd);
+            }
         }
         __syncthreads();
         for (int i = threadIdx.x; i < WW; i += kFlushBlock) {

@@ -308,16 +308,35 @@ segtab_expand_kernel(const __grid_constant__ hb_tiles t, int32_t *__restrict__ c
     };
     unsigned keys = 0;
 
+    const unsigned ssh = (unsigned)__cvta_generic_to_shared(sh);
     auto rasterise = [&]() {  // all threads: drain the buffer into sh
         const int n = nbuf;
         for (int i = threadIdx.x; i < n; i += kExpandBlock) {
             const uint2 k = buf[i];
-            const int plane = (int)(k.x >> 13), y0 = ty0 + (int)((k.x >> 6) & 127u),
-                      x0 = tx0 + (int)(k.x & 63u);
+            const int plane = (int)(k.x >> 13), ly0 = (int)((k.x >> 6) & 127u),
+                      lx0 = (int)(k.x & 63u);
             const int dy = plane / D - H, dx = plane % D - H;
-            dda_walk(x0, y0, x0 + dx, y0 + dy, 1, [&](int u, int vv) {
-                atomicAdd(&sh[(vv - ty0 + H) * SW + (u - tx0 + H)], (int)k.y);
-            });
+            // dda_walk's chain from k0 = 1 as an index into sh (all cells are
+            // within the H halo); a zero delta adds nothing at k0 = 1
+            const int steps = max(abs(dx), abs(dy));
+            if (steps == 0) continue;
+            const bool xdom = abs(dx) == steps;
+            const int major_step = xdom ? (dx > 0 ? 1 : -1) : (dy > 0 ? SW : -SW);
+            const int minor_mul = xdom ? SW : 1;
+            const int dmin = xdom ? dy : dx;
+            // (global start cell: the float64 expression uses it)
+            const double c = (double)(xdom ? ty0 + ly0 : tx0 + lx0), inv = 1.0 / (double)steps;
+            // sh index of (major at k, minor 0): sh[(v - ty0 + H) * SW + (u - tx0 + H)]
+            int base = xdom ? (lx0 + H) + (H - ty0) * SW : (ly0 + H) * SW + (H - tx0);
+            base += major_step;
+            double kd = (double)dmin;
+            const double dd = (double)dmin;
+            for (int kk = 1; kk <= steps; ++kk) {
+                const int minor = floor_i(dadd(dadd(c, dmul(kd, inv)), 0.5));
+                red_shared(ssh + 4u * (unsigned)(base + minor_mul * minor), (int)k.y);
+                base += major_step;
+                kd = dadd(kd, dd);
+            }
         }
     };
 

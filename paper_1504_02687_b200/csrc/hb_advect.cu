@@ -362,7 +362,8 @@ int hb_advect_laplacian(const double *pts_in, double *pts_out, const int64_t *st
                         unsigned long long *moved, double *disp_partials, void *stream) {
     const bool adv = h >= 0.0;
     if (n_edges < 0 || n_pts < 0 || lap_passes < 0 || (adv && (!moved || !disp_partials)) ||
-        (adv && (nbins < 1 || nv < 3 || nu < 3 || nv > kMaxDim || nu > kMaxDim || !edge_layer || !rho)) ||
+        (adv && (nbins < 1 || nv < 3 || nu < 3 || nv > kMaxDim || nu > kMaxDim ||
+                 (n_edges > 0 && !edge_layer) || !rho)) ||
         (counts && (!pos || !(delta > 0))) ||
         (n_pts > 0 && (!pts_in || !pts_out || !starts)))
         return set_error(HB_EINVAL, "hb_advect_laplacian: bad arguments");

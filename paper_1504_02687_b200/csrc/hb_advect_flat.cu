@@ -291,7 +291,7 @@ int hb_advect_points(double *pts, const int64_t *starts, int64_t n_edges, int64_
                      void *stream) {
     if (n_edges < 0 || n_pts < 0 || nbins < 1 || nv < 3 || nu < 3 || nv > kMaxDim ||
         nu > kMaxDim || !moved || !disp_partials || !(h >= 0.0) ||
-        (n_pts > 0 && (!pts || !starts || !edge_layer || !rho)))
+        (n_pts > 0 && n_edges > 0 && (!pts || !starts || !edge_layer || !rho)))
         return set_error(HB_EINVAL, "hb_advect_points: bad arguments");
     if ((int64_t)nbins * nv * nu >= ((int64_t)1 << 31) ||
         (grad_field && (int64_t)kQuadRec * nbins * nv * nu >= ((int64_t)1 << 32)))

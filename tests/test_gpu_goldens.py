@@ -284,3 +284,26 @@ def test_cfg5_full_size_shard_vs_oracle():
     assert np.array_equal(res.density.values, ref.field)
     for m, r in zip(res.metrics, ref.metrics):
         assert (m.moved_points, m.used_cells) == (r.moved_points, r.used_cells)
+
+
+@pytest.mark.parametrize("name", ["empty", "coincident", "single", "collinear", "border_hub"])
+def test_degenerate_graphs_match_reference(name):
+    """No edges, coincident endpoints (zero-length segments), a single edge,
+    collinear nodes (a flat bounding box), a hub on the bounding-box corner
+    with integer weights: bundle() equals the reference's own run."""
+    from small_graphs import small_graphs
+
+    from paper_1504_02687_b200.model import BundleConfig
+    g = _golden("small_graphs")[name]
+    pos, s, t, wts, over = small_graphs()[name]
+    graph = Graph(pos, np.asarray(s, np.int64), np.asarray(t, np.int64), wts)
+    res = B.bundle(graph, BundleConfig(**over))
+    world = (res.sampled_edges.world if len(res.sampled_edges)
+             else np.zeros((0, 2)))
+    assert [len(e) for e in res.sampled_edges][:50] == g["counts"]
+    assert digest(world)["sha256"] == g["final_world"]["sha256"]
+    assert digest(res.density.values)["sha256"] == g["final_field"]["sha256"]
+    assert [m.moved_points for m in res.metrics] == g["moved"]
+    assert [m.used_cells for m in res.metrics] == g["used"]
+    np.testing.assert_allclose([m.mean_displacement for m in res.metrics],
+                               g["mean_displacement"], rtol=1e-9)

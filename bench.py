@@ -201,10 +201,23 @@ def roofline_from_trace(trace, records, eng, peak, peak_src):
             mean_n = statistics.mean(r.n_points for r in records)
             traffic = float(t["bytes_per_point"]) * mean_n
     total_ms = sum(v["ms_total"] for v in per.values())
+    # the measured limit of the dominant kernel when it is not HBM (ncu --set full)
+    ceiling = None
+    cpath = os.path.join(ROOT, "profiles", "r02_ncu_full_summary.json")
+    if os.path.exists(cpath):
+        with open(cpath) as f:
+            c = json.load(f).get(dom)
+        if c and "l1tex__data_pipe_lsu_wavefronts.avg.pct_of_peak_sustained_elapsed" in c:
+            pct = float(c["l1tex__data_pipe_lsu_wavefronts.avg.pct_of_peak_sustained_elapsed"]
+                        .split()[0])
+            sect = float(c["l1tex__t_sectors_pipe_lsu_mem_global_op_ld.sum"].split()[0])
+            ceiling = {"bound": "l1tex data pipe (gathers)", "frac_of_ceiling": round(pct / 100, 4),
+                       "global_load_sectors_per_point": round(sect / c["points"], 2),
+                       "source": "profiles/r02_ncu_full_summary.json (" + c["capture"] + ")"}
     return {
         "kernel": dom, "bound": "hbm", "achieved": round(achieved, 1),
         "peak": peak, "unit": "GB/s", "frac": round(achieved / peak, 4),
-        "traffic": traffic, "peak_source": peak_src,
+        "traffic": traffic, "peak_source": peak_src, "ceiling": ceiling,
         "avg_launch_ms": d["ms_total"] / max(d["launches"], 1),
         "share_of_kernel_time": round(d["ms_total"] / total_ms, 4) if total_ms else None,
         "per_kernel": {k: {"launches": v["launches"],

@@ -125,6 +125,12 @@ def sum_host_arrays(arrays: list[np.ndarray], group=None) -> list[np.ndarray]:
     return out
 
 
+def _count_d2h(*arrays) -> None:
+    """Host-bound bytes of the public API (bench.py's e2e accounting)."""
+    from .engine import IO_BYTES
+    IO_BYTES["d2h"] += sum(int(a.nbytes) for a in arrays)
+
+
 def gather_polylines(points: torch.Tensor, starts: torch.Tensor, group=None, root: int = 0):
     """Every rank's packed polylines concatenated in rank order (= edge
     order) on ``root`` only: the point counts are all-gathered
@@ -158,5 +164,6 @@ def gather_polylines(points: torch.Tensor, starts: torch.Tensor, group=None, roo
             dist.recv(s, src=src, group=group)
         pieces.append(p[:n].cpu().numpy())
         st_pieces.append(s[1: e + 1].cpu().numpy() + base)
+        _count_d2h(pieces[-1], st_pieces[-1])
         base += n
     return np.concatenate(pieces), np.concatenate(st_pieces)

@@ -8,6 +8,10 @@
 // (raster.py:147-169).  Pass inputs after the first are non-integer float32
 // values, so the fold ORDER decides the last bits of the table; we keep the
 // reference's order exactly:
+//   fold     : both folds in one cooperative launch (fold_kernel: column
+//              strips, C tiles handed from column lanes to row lanes in
+//              shared memory, row carries handed between strips); the two
+//              kernels below when the strips cannot all be co-resident:
 //   col_fold : one lane per (layer, column), sequential in v; 32-row tiles
 //              stream through a 4-deep cp.async ring, rows stored coalesced
 //   row_scan : one lane per (layer, row), 32x32 tiles through a 4-deep
@@ -285,6 +289,274 @@ row_scan2_kernel(double *__restrict__ table, int64_t n_rows, int nu) {
     }
 }
 
+// ---- fused integral table: one cooperative pass per box pass ----------------
+// The two folds above are strict sequential float64 chains (H steps down every
+// column, W steps along every row); the critical path of the whole table is
+// (H + W) dependent DADDs (~8.3 cycles each), ~17 us on a 2048^2 layer.  The
+// separate kernels also round-trip C and T through DRAM (config-5 map:
+// 40 + 49 us) and, on small maps, run far below the chain floor for lack of
+// memory-level parallelism (config 4: 20 + 22 us against ~4 us).
+//
+// fold_kernel<S> computes T with both folds in one launch.  CTA (l, k) owns
+// the S columns [kS, kS+S) of layer l for the full height:
+//   * column warps (S/32): lane = column, the column fold C[v][u] = C[v-1][u]
+//     + x[v][u] kept in a register, written 32 rows at a time into a C tile
+//     (shared, kFoldSlots-deep ring); the next 32 rows are loaded ahead.
+//   * row warps (8 - S/32): lane = row, each takes whole tiles (block b goes
+//     to row warp b mod kRowWarps); the row fold starts from the carry
+//     T[v][kS] of strip k-1 and walks the tile's S columns in order (the
+//     reference's order), in place; the tile then leaves as coalesced rows of
+//     T, and T[v][kS+S] is handed to strip k+1.
+// Hand-off between strips: carry[l][k][v] is pre-filled with kFoldSentinel
+// (a NaN bit pattern no finite sum can take), so the 8-byte value is its own
+// ready flag -- one relaxed store, one relaxed poll, no fence; the single
+// consumer re-arms it.  Strips wait on one another, so the launch is
+// cooperative (all CTAs co-resident).  Order of every float64 operation is
+// the reference's; only who performs it changes.
+constexpr int kFoldThreads = 256;
+constexpr unsigned long long kFoldSentinel = ~0ull;
+
+__device__ __forceinline__ unsigned long long ld_relaxed_u64(const unsigned long long *p) {
+    unsigned long long v;
+    asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+    return v;
+}
+__device__ __forceinline__ void st_relaxed_u64(unsigned long long *p, unsigned long long v) {
+    asm volatile("st.relaxed.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+
+#ifdef HB_FOLD_TRACE  // diagnostic build: per (strip, block) event times of layer 0
+__device__ unsigned long long g_fold_trace[64][128][4];
+__device__ __forceinline__ void fold_trace(int l, int k, int b, int e) {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    if (l == 0 && k < 64 && b < 128) g_fold_trace[k][b][e] = t;
+}
+#else
+__device__ __forceinline__ void fold_trace(int, int, int, int) {}
+#endif
+
+template <int S>
+struct FoldCfg {
+    static constexpr int kColWarps = S / 32;
+    static constexpr int kRowWarps = kFoldThreads / 32 - kColWarps;
+    static constexpr int kPitch = S + 1;  // doubles; row-lane column walks: 2 wavefronts
+    static constexpr int kSlots = S >= 128 ? 5 : 8;   // C tiles in flight
+    static constexpr int kStages = S >= 128 ? 4 : 8;  // x blocks prefetched (cp.async)
+    static constexpr size_t kSmem = sizeof(double) * (size_t)kSlots * 32 * kPitch +
+                                    sizeof(float) * (size_t)kStages * 32 * S;
+};
+
+template <int S>
+__global__ void __launch_bounds__(kFoldThreads, 1)
+fold_kernel(const float *__restrict__ in, int nv, int nu, int nstrips,
+            double *__restrict__ table, unsigned long long *__restrict__ carry) {
+    using C = FoldCfg<S>;
+    extern __shared__ __align__(16) double ftile[];
+    __shared__ int s_prod;               // C tiles produced (blocks 0 .. s_prod-1)
+    __shared__ int s_free[C::kSlots];    // slot i last released by block s_free[i]-1
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int l = blockIdx.x / nstrips, k = blockIdx.x % nstrips;
+    const int u0 = k * S;
+    const int ncols = min(S, nu - u0);
+    const int64_t plane = (int64_t)nv * nu;
+    const int nblk = (nv + 31) / 32;
+    if (threadIdx.x == 0) s_prod = 0;
+    if (threadIdx.x < C::kSlots) s_free[threadIdx.x] = 0;
+    __syncthreads();
+    volatile int *vprod = &s_prod;
+    volatile int *vfree = s_free;
+
+    if (warp < C::kColWarps) {
+        // ---- column fold ----
+        const int t = threadIdx.x;  // column within the strip
+        float *xs = reinterpret_cast<float *>(ftile + (size_t)C::kSlots * 32 * C::kPitch);
+        const bool vec = (nu % 4) == 0;  // 16-byte rows (u0 is a multiple of 64)
+        // vec: thread t copies the 16-byte chunk ch of rows r0, r0+4, ..., r0+28
+        constexpr int kCpr = S / 4;  // chunks per row
+        const int ch = t % kCpr, r0 = t / kCpr;
+        const bool chok = ch * 4 < ncols;
+        const float *gsrc = in + l * plane + u0 + (vec ? (int64_t)r0 * nu + ch * 4 : t);
+        const int soff = vec ? r0 * S + ch * 4 : t;
+        // x rows of block bb -> staging stage bb % kStages (zero past the grid)
+        auto issue = [&](int bb) {
+            if (bb < nblk) {
+                float *st = xs + (size_t)(bb % C::kStages) * 32 * S + soff;
+                const float *g = gsrc + (int64_t)bb * 32 * nu;
+                const int vb = bb * 32;
+                if (vec) {
+#pragma unroll
+                    for (int m = 0; m < 8; ++m) {
+                        const bool okq = chok && vb + r0 + 4 * m < nv;
+                        cp_async16z(st + 4 * m * S, okq ? g + (int64_t)4 * m * nu : gsrc, okq);
+                    }
+                } else {
+                    for (int r = 0; r < 32; ++r) {
+                        const bool okq = vb + r < nv && t < ncols;
+                        cp_async4z(st + r * S, okq ? g + (int64_t)r * nu : gsrc, okq);
+                    }
+                }
+            }
+            cp_async_commit();  // one group per block, possibly empty
+        };
+        // Per block: the DADD chain of block b interleaved with widening block
+        // b+1 (LDS + F2F fill the chain's latency gaps), so the per-block
+        // critical path is the 32 dependent DADDs plus two barriers.
+        double xa[32], xc[32];
+        auto widen = [&](int bb, double (&xd)[32]) {
+            const float *xb = xs + (size_t)(bb % C::kStages) * 32 * S + t;
+#pragma unroll
+            for (int i = 0; i < 32; ++i) xd[i] = (double)xb[i * S];
+        };
+#pragma unroll
+        for (int d = 0; d < C::kStages - 1; ++d) issue(d);
+        cp_async_wait<C::kStages - 2>();  // block 0 landed
+        asm volatile("bar.sync 1, %0;" ::"r"(S));
+        widen(0, xa);
+        double c = 0.0;
+        auto step = [&](int b, double (&cur)[32], double (&nxt)[32]) {
+            cp_async_wait<C::kStages - 3>();  // block b+1 landed (this thread's copies)
+            asm volatile("bar.sync 1, %0;" ::"r"(S));  // ... and every thread's
+            const int slot = b % C::kSlots;
+            while (vfree[slot] < b - C::kSlots + 1) __nanosleep(32);
+            double *tile = ftile + (size_t)slot * 32 * C::kPitch + t;
+            const float *xn = xs + (size_t)((b + 1) % C::kStages) * 32 * S + t;
+#pragma unroll
+            for (int i = 0; i < 32; ++i) {
+                // np.cumsum: the first element as is
+                c = (b == 0 && i == 0) ? cur[0] : dadd(c, cur[i]);
+                tile[i * C::kPitch] = c;
+                nxt[i] = (double)xn[i * S];  // (unused after the last block)
+            }
+            asm volatile("bar.sync 1, %0;" ::"r"(S));  // C tile complete
+            if (t == 0) {
+                __threadfence_block();
+                *vprod = b + 1;
+                fold_trace(l, k, b, 0);
+            }
+            issue(b + C::kStages - 1);  // refills the stage block b-1 used
+        };
+        for (int b = 0; b < nblk; b += 2) {
+            step(b, xa, xc);
+            if (b + 1 < nblk) step(b + 1, xc, xa);
+        }
+    } else {
+        // ---- row fold ----
+        const int rw = warp - C::kColWarps;
+        unsigned long long *cin = carry + ((int64_t)l * nstrips + k) * nv;
+        unsigned long long *cout = carry + ((int64_t)l * nstrips + k + 1) * nv;
+        double *dst = table + l * plane + u0;
+        for (int b = rw; b < nblk; b += C::kRowWarps) {
+            const int v = b * 32 + lane;
+            const bool rok = v < nv;
+            while (*vprod <= b) __nanosleep(32);
+            __threadfence_block();
+            double *tile = ftile + (size_t)(b % C::kSlots) * 32 * C::kPitch;
+            double *row = tile + lane * C::kPitch;
+            // the first 32 C values of the row are loaded before the carry
+            // arrives; later chunks load while the previous one folds, so the
+            // fold is a pure DADD chain
+            double cur[32];
+            const bool full = ncols == S;
+            if (full) {
+#pragma unroll
+                for (int j = 0; j < 32; ++j) cur[j] = row[j];
+            }
+            double tv = 0.0;
+            if (k > 0) {
+                unsigned long long bits = kFoldSentinel;
+                if (rok) {
+                    while ((bits = ld_relaxed_u64(cin + v)) == kFoldSentinel) {
+                    }
+                    st_relaxed_u64(cin + v, kFoldSentinel);  // re-arm for the next pass
+                }
+                tv = __longlong_as_double((long long)bits);
+            }
+            if (lane == 0) fold_trace(l, k, b, 1);
+            if (full) {
+#pragma unroll
+                for (int c = 0; c < S / 32; ++c) {
+                    double nxt[32];
+                    if (c + 1 < S / 32) {
+#pragma unroll
+                        for (int j = 0; j < 32; ++j) nxt[j] = row[32 * (c + 1) + j];
+                    }
+#pragma unroll
+                    for (int j = 0; j < 32; ++j) {
+                        // np.cumsum along the row: the first element as is
+                        tv = (k == 0 && c == 0 && j == 0) ? cur[0] : dadd(tv, cur[j]);
+                        cur[j] = tv;
+                    }
+#pragma unroll
+                    for (int j = 0; j < 32; ++j) row[32 * c + j] = cur[j];
+                    if (c + 1 < S / 32) {
+#pragma unroll
+                        for (int j = 0; j < 32; ++j) cur[j] = nxt[j];
+                    }
+                }
+            } else {
+                for (int j = 0; j < ncols; ++j) {
+                    tv = (k == 0 && j == 0) ? row[0] : dadd(tv, row[j]);
+                    row[j] = tv;
+                }
+            }
+            if (k + 1 < nstrips && rok) st_relaxed_u64(cout + v, (unsigned long long)__double_as_longlong(tv));
+            if (lane == 0) fold_trace(l, k, b, 2);
+            __syncwarp();
+            // the tile's rows of T, coalesced
+            const int nr = min(32, nv - b * 32);
+            if (nr == 32 && full && (nu & 1) == 0) {
+                // full tile: 8 rows of loads in flight, then their 16-byte stores
+                double *d = dst + (int64_t)(b * 32) * nu + 2 * lane;
+                const double *s = tile + 2 * lane;
+#pragma unroll
+                for (int i0 = 0; i0 < 32; i0 += 8) {
+                    double2 q[8][S / 64];
+#pragma unroll
+                    for (int ii = 0; ii < 8; ++ii)
+#pragma unroll
+                        for (int m = 0; m < S / 64; ++m)
+                            q[ii][m] = make_double2(s[(i0 + ii) * C::kPitch + 64 * m],
+                                                    s[(i0 + ii) * C::kPitch + 64 * m + 1]);
+#pragma unroll
+                    for (int ii = 0; ii < 8; ++ii)
+#pragma unroll
+                        for (int m = 0; m < S / 64; ++m)
+                            *reinterpret_cast<double2 *>(d + (int64_t)(i0 + ii) * nu + 64 * m) =
+                                q[ii][m];
+                }
+            } else if ((nu & 1) == 0) {  // 16-byte stores: a lane writes 2 columns of a row
+#pragma unroll 8
+                for (int i = 0; i < nr; ++i) {
+                    double *d = dst + (int64_t)(b * 32 + i) * nu;
+                    const double *s = tile + i * C::kPitch;
+#pragma unroll
+                    for (int m = 0; m < S / 64; ++m) {
+                        const int col = 2 * lane + 64 * m;
+                        if (col < ncols)
+                            *reinterpret_cast<double2 *>(d + col) = make_double2(s[col], s[col + 1]);
+                    }
+                }
+            } else {
+                for (int i = 0; i < nr; ++i) {
+                    double *d = dst + (int64_t)(b * 32 + i) * nu;
+                    const double *s = tile + i * C::kPitch;
+#pragma unroll
+                    for (int m = 0; m < S / 32; ++m) {
+                        const int col = lane + 32 * m;
+                        if (col < ncols) d[col] = s[col];
+                    }
+                }
+            }
+            __syncwarp();
+            if (lane == 0) {
+                vfree[b % C::kSlots] = b + 1;
+                fold_trace(l, k, b, 3);
+            }
+        }
+    }
+}
+
 // 4-term box sum with zero row/column 0 implicit (table holds T[1:,1:]).
 __device__ __forceinline__ double tz(const double *__restrict__ t, int nu, int r, int c) {
     return (r == 0 || c == 0) ? 0.0 : t[(int64_t)(r - 1) * nu + (c - 1)];
@@ -330,7 +602,11 @@ __device__ __forceinline__ float box_quotient_f32(double s, double area, double 
 }
 
 // Each thread produces kBoxRows cells of one column; all 4*kBoxRows table
-// reads are issued before the first quotient.
+// reads are issued before the first quotient.  Indices are 32-bit (every
+// plane is < 2^31 cells) and the zero row/column of the table is a select,
+// so a cell costs ~4 address ops + 4 loads + 3 DADD + the quotient (the
+// 64-bit index arithmetic of a generic gather was ~110 warp instructions per
+// 32 cells, and issue-bound).
 __global__ void __launch_bounds__(kBoxBlock)
 box_kernel(const double *__restrict__ table, int nv, int nu, int radius,
            float *__restrict__ out, float *__restrict__ peak) {
@@ -340,27 +616,32 @@ box_kernel(const double *__restrict__ table, int nv, int nu, int radius,
     float m = 0.0f;
     if (u < nu) {
         const int64_t plane = (int64_t)nv * nu;
-        const double *t = table + l * plane;
-        const int c0 = min(max(u - radius, 0), nu), c1 = min(max(u + radius + 1, 0), nu);
+        // T[i][j] (i, j >= 1) at byte (i*nu + j) * 8 from tb; unsigned indices
+        // so every address is one IMAD.WIDE.U32
+        const char *tb = reinterpret_cast<const char *>(table + l * plane - nu - 1);
+        auto T = [&](unsigned i, unsigned j) {
+            return *reinterpret_cast<const double *>(tb + (size_t)(i * (unsigned)nu + j) * 8u);
+        };
+        const int c0 = min(max(u - radius, 0), nu), c1 = min(u + radius + 1, nu);  // c1 >= 1
         const double area = (double)((2 * radius + 1) * (2 * radius + 1));
         const double inv_area = __drcp_rn(area);
         double t11[kBoxRows], t01[kBoxRows], t10[kBoxRows], t00[kBoxRows];
 #pragma unroll
         for (int k = 0; k < kBoxRows; ++k) {
             const int v = min(vb + k, nv - 1);
-            const int r0 = min(max(v - radius, 0), nv), r1 = min(max(v + radius + 1, 0), nv);
-            t11[k] = tz(t, nu, r1, c1);
-            t01[k] = tz(t, nu, r0, c1);
-            t10[k] = tz(t, nu, r1, c0);
-            t00[k] = tz(t, nu, r0, c0);
+            const int r0 = max(v - radius, 0), r1 = min(v + radius + 1, nv);  // r1 >= 1
+            t11[k] = T(r1, c1);
+            t10[k] = c0 ? T(r1, c0) : 0.0;
+            t01[k] = r0 ? T(r0, c1) : 0.0;
+            t00[k] = (r0 && c0) ? T(r0, c0) : 0.0;
         }
         float *o = out + l * plane + u;
 #pragma unroll
         for (int k = 0; k < kBoxRows; ++k) {
             if (vb + k < nv) {
-                const double s = dadd(dsub(dsub(t11[k], t01[k]), t10[k]), t00[k]);
-                const float val = box_quotient_f32(s, area, inv_area);
-                o[(int64_t)(vb + k) * nu] = val;
+                const double sum = dadd(dsub(dsub(t11[k], t01[k]), t10[k]), t00[k]);
+                const float val = box_quotient_f32(sum, area, inv_area);
+                o[(vb + k) * nu] = val;
                 m = fmaxf(m, val > 0.0f ? val : 0.0f);
             }
         }
@@ -758,22 +1039,97 @@ static unsigned col_fold_blocks(int nbins, int nu) {
 
 static inline cudaStream_t as_stream(void *s) { return reinterpret_cast<cudaStream_t>(s); }
 
+// Fused fold (fold_kernel<S>): strip width and whether it fits.  Every CTA
+// must be co-resident (strips wait on one another): S = 64 when nbins *
+// nstrips CTAs fit at one per SM, else S = 128; 0 = use the two fold kernels.
+// HB_FOLD=0 in the environment selects the two fold kernels (A/B checks).
+template <int S>
+static int fold_blocks_per_sm() {
+    static int per_sm = -1;  // a property of the kernel: computed once
+    if (per_sm < 0) {
+        const void *fn = (const void *)fold_kernel<S>;
+        int n = 0;
+        if (cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 (int)FoldCfg<S>::kSmem) != cudaSuccess ||
+            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, fn, kFoldThreads,
+                                                          FoldCfg<S>::kSmem) != cudaSuccess) {
+            cudaGetLastError();
+            n = 0;
+        }
+        per_sm = n;
+    }
+    return per_sm;
+}
+
+static int fold_strip_width(int nbins, int nu) {
+    const char *e = getenv("HB_FOLD");  // read per call: tests flip it in-process
+    if (e && e[0] == '0') return 0;
+    const int64_t sms = device_sm_count();
+    if ((int64_t)nbins * ((nu + 63) / 64) <= fold_blocks_per_sm<64>() * sms) return 64;
+    if ((int64_t)nbins * ((nu + 127) / 128) <= fold_blocks_per_sm<128>() * sms) return 128;
+    return 0;
+}
+
+// carry hand-off words of fold_kernel: [nbins][nstrips][nv] (nstrips <= nu/64 + 1)
+static size_t fold_carry_words(int nbins, int nv, int nu) {
+    return (size_t)nbins * (size_t)(nu / 64 + 1) * (size_t)nv;
+}
+
+template <int S>
+static cudaError_t launch_fold(const float *fin, int nbins, int nv, int nu, double *table,
+                               unsigned long long *carry, cudaStream_t st) {
+    int nstrips = (nu + S - 1) / S;
+    void *args[] = {(void *)&fin, (void *)&nv, (void *)&nu, (void *)&nstrips, (void *)&table,
+                    (void *)&carry};
+    return cudaLaunchCooperativeKernel((const void *)fold_kernel<S>, dim3(nbins * nstrips),
+                                       dim3(kFoldThreads), args, FoldCfg<S>::kSmem, st);
+}
+
 // One float box pass (raster.py:147-169) of every layer: column fold, row
-// fold (float64 table), 4-term box / area -> dst (+ layer peaks).
-static void float_box_pass(const float *fin, int nbins, int nv, int nu, int r, float *dst,
-                           double *table, float *pk, cudaStream_t st) {
-    col_fold_kernel<<<col_fold_blocks(nbins, nu), kColWarps * 32, 0, st>>>(fin, nbins, nv, nu,
-                                                                           table);
-    launch_row_fold(table, (int64_t)nbins * nv, nu, st);
+// fold (float64 table), 4-term box / area -> dst (+ layer peaks).  carry:
+// fold_kernel's hand-off words, all kFoldSentinel on entry and on exit.
+// Returns the number of kernels launched.
+static int float_box_pass(const float *fin, int nbins, int nv, int nu, int r, float *dst,
+                          double *table, float *pk, unsigned long long *carry,
+                          cudaStream_t st) {
+    const int S = carry ? fold_strip_width(nbins, nu) : 0;
+    int launched = 3;
+    if (S == 64) {
+        launch_fold<64>(fin, nbins, nv, nu, table, carry, st);
+        launched = 2;
+    } else if (S == 128) {
+        launch_fold<128>(fin, nbins, nv, nu, table, carry, st);
+        launched = 2;
+    } else {
+        col_fold_kernel<<<col_fold_blocks(nbins, nu), kColWarps * 32, 0, st>>>(fin, nbins, nv,
+                                                                               nu, table);
+        launch_row_fold(table, (int64_t)nbins * nv, nu, st);
+    }
     dim3 gb((nu + kBoxBlock - 1) / kBoxBlock, (nv + kBoxRows - 1) / kBoxRows, nbins);
     box_kernel<<<gb, kBoxBlock, 0, st>>>(table, nv, nu, r, dst, pk);
+    return launched;
+}
+
+// fold_kernel's carry words at the end of the smoothing workspace, armed
+// (all kFoldSentinel) for this call; NULL when the fused fold is not used.
+static unsigned long long *fold_carry(void *workspace, int nbins, int nv, int nu,
+                                      cudaStream_t st) {
+    if (!fold_strip_width(nbins, nu)) return nullptr;
+    const size_t cells = (size_t)nbins * nv * nu;
+    const size_t off = (cells * (sizeof(double) + sizeof(float)) + 255) & ~(size_t)255;
+    auto *carry = reinterpret_cast<unsigned long long *>(static_cast<char *>(workspace) + off);
+    if (cudaMemsetAsync(carry, 0xff, sizeof(unsigned long long) * fold_carry_words(nbins, nv, nu),
+                        st) != cudaSuccess)
+        return nullptr;
+    return carry;
 }
 
 extern "C" {
 
 size_t hb_smooth_workspace_bytes(int nbins, int nv, int nu) {
     const size_t cells = (size_t)nbins * nv * nu;
-    return cells * sizeof(double) + cells * sizeof(float) + 256;
+    return cells * sizeof(double) + cells * sizeof(float) + 256 +
+           sizeof(unsigned long long) * fold_carry_words(nbins, nv, nu);
 }
 
 int hb_smooth(const int32_t *counts, const float *hist, const float *matrix, int nbins,
@@ -790,6 +1146,7 @@ int hb_smooth(const int32_t *counts, const float *hist, const float *matrix, int
     const size_t cells = (size_t)nbins * plane;
     double *table = reinterpret_cast<double *>(workspace);
     float *stage = reinterpret_cast<float *>(table + cells);
+    unsigned long long *carry = fold_carry(workspace, nbins, nv, nu, st);
     if (layer_peak && cudaMemsetAsync(layer_peak, 0, sizeof(float) * nbins, st) != cudaSuccess)
         return check_launch("hb_smooth(memset)", 0);
     const float *src = nullptr;  // float32 input of passes after the first
@@ -800,6 +1157,7 @@ int hb_smooth(const int32_t *counts, const float *hist, const float *matrix, int
         float *dst = ((npasses - 1 - p) % 2 == 0) ? out : stage;
         float *pk = (p == npasses - 1) ? layer_peak : nullptr;
         const int r = radii[p];
+        int launched = 1;
         if (r == 0) {
             dim3 g((unsigned)((plane + 255) / 256), nbins);
             if (first && counts)
@@ -823,10 +1181,12 @@ int hb_smooth(const int32_t *counts, const float *hist, const float *matrix, int
                     mix_pass_kernel<float><<<g, 256, 0, st>>>(hist, matrix, nbins, plane, stage,
                                                               nullptr);
                 fin = stage;
+            } else {
+                launched = 0;
             }
-            float_box_pass(fin, nbins, nv, nu, r, dst, table, pk, st);
+            launched += float_box_pass(fin, nbins, nv, nu, r, dst, table, pk, carry, st);
         }
-        int rc = check_launch("hb_smooth", r == 0 ? 1 : (mix_first ? 4 : 3));
+        int rc = check_launch("hb_smooth", launched);
         if (rc) return rc;
         src = dst;
     }
@@ -852,6 +1212,7 @@ int hb_smooth_counts(const int32_t *counts, const int32_t *mix, double scale, do
     const size_t cells = (size_t)nbins * plane;
     double *table = reinterpret_cast<double *>(workspace);
     float *stage = reinterpret_cast<float *>(table + cells);
+    unsigned long long *carry = fold_carry(workspace, nbins, nv, nu, st);
     if (layer_peak && cudaMemsetAsync(layer_peak, 0, sizeof(float) * nbins, st) != cudaSuccess)
         return check_launch("hb_smooth_counts(memset)", 0);
     // pass 0: exact integer window sums in shared-memory tiles
@@ -907,18 +1268,25 @@ int hb_smooth_counts(const int32_t *counts, const int32_t *mix, double scale, do
         float *dst = ((npasses - 1 - p) % 2 == 0) ? out : stage;
         float *pk = (p == npasses - 1) ? layer_peak : nullptr;
         const int r = radii[p];
+        int launched = 1;
         if (r == 0) {
             dim3 g((unsigned)((plane + 255) / 256), nbins);
             mix_pass_kernel<float><<<g, 256, 0, st>>>(src, nullptr, nbins, plane, dst, pk);
         } else {
-            float_box_pass(src, nbins, nv, nu, r, dst, table, pk, st);
+            launched = float_box_pass(src, nbins, nv, nu, r, dst, table, pk, carry, st);
         }
-        int rc = check_launch("hb_smooth_counts", r == 0 ? 1 : 3);
+        int rc = check_launch("hb_smooth_counts", launched);
         if (rc) return rc;
         src = dst;
     }
     return HB_OK;
 }
+
+#ifdef HB_FOLD_TRACE
+HB_API int hb_debug_fold_trace(unsigned long long *out) {
+    return cudaMemcpyFromSymbol(out, g_fold_trace, sizeof(g_fold_trace)) == cudaSuccess ? 0 : -1;
+}
+#endif
 
 int hb_mix_layers(const int32_t *counts, const float *hist, const float *matrix, int nbins,
                   int nv, int nu, float *out, void *stream) {

@@ -316,6 +316,31 @@ def test_smooth_random_multilayer_vs_oracle():
         assert np.array_equal(got, O.smooth(vals, sigma, 3)), sigma
 
 
+# fused integral table (fold_kernel): strip widths 64 and 128, partial strips
+# and row blocks, a single strip, and the two-kernel fallback (too many strips
+# to be co-resident)
+@pytest.mark.parametrize("shape", [(1, 37, 45), (2, 100, 200), (3, 257, 130), (1, 70, 64),
+                                   (20, 40, 512), (40, 33, 1024)])
+def test_smooth_fused_fold_shapes_vs_oracle(shape):
+    rng = np.random.default_rng(sum(shape))
+    vals = (rng.gamma(0.5, 2.0, size=shape) * (rng.uniform(size=shape) < 0.4)).astype(np.float32)
+    for sigma in (2.0, 9.0):
+        got = R.smooth_gaussian_approx(DensityField(None, vals), sigma, 3).values
+        assert np.array_equal(got, O.smooth(vals, sigma, 3)), (shape, sigma)
+
+
+def test_smooth_fused_fold_equals_two_fold_kernels_config5_map(monkeypatch):
+    """The config-5 map (4 x 2047 x 2048, radii 50/51/51): fused fold vs the
+    column-fold + row-fold kernels, bit for bit."""
+    g = torch.Generator(device="cuda").manual_seed(5)
+    vals = (torch.rand((4, 2047, 2048), generator=g, device="cuda") ** 8 * 300).float()
+    vals = vals.cpu().numpy()
+    got = R.smooth_gaussian_approx(DensityField(None, vals), 51.2, 3).values
+    monkeypatch.setenv("HB_FOLD", "0")
+    ref = R.smooth_gaussian_approx(DensityField(None, vals), 51.2, 3).values
+    assert np.array_equal(got, ref)
+
+
 # ---------------------------------------------------------------------------
 # end to end against the reference goldens
 

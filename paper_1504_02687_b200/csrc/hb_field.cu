@@ -793,9 +793,9 @@ box_int_kernel(const int32_t *__restrict__ counts, const int32_t *__restrict__ m
 // taken separably through an int32 buffer in global memory (L2):
 //   vwin_int : a thread per column slides a (2r+1)-row window down kVwinRows
 //              rows (loads unrolled ahead, the outgoing row is an L1 hit)
-//   hwin_int : a CTA stages kHwinRows rows of W in shared memory (padded by
-//              one word per 32 so 32-column chunks hit distinct banks) and a
-//              thread per (row, 32-column chunk) slides the row window.
+//   hwin_int : a CTA takes kHwinRows rows of W (8 consecutive columns per
+//              thread), scans each row into int64 prefixes in shared memory
+//              and takes every window as a difference of two prefixes.
 constexpr int kVwinRows = 64;
 constexpr int kVwinThreads = 128;
 // Hi of one cell (MIX: sum_b mix[l,b] * G[b]; the guard's |.|-sum in `a`)
@@ -868,62 +868,97 @@ vwin_int_kernel(const int32_t *__restrict__ counts, const int32_t *__restrict__ 
         atomicOr(status, HB_STATUS_INEXACT);
 }
 
-constexpr int kHwinRows = 4;
-constexpr int kHwinThreads = 256;
-__host__ __device__ __forceinline__ int hwin_pitch(int nu) {  // padded row length
-    return nu + (nu + 31) / 32 + 1;
+constexpr int kHwinRows = 4;  // rows of W per CTA (the next row loads during a row's scan)
+constexpr int kHwinCols = 8;  // consecutive columns per thread (nu <= 8 * 1024)
+__host__ __device__ __forceinline__ int hwin_threads(int nu) {
+    return ((nu + kHwinCols - 1) / kHwinCols + 31) / 32 * 32;
 }
-__device__ __forceinline__ int hwin_ix(int j) { return j + (j >> 5); }
+// prefix j lives at hwin_pad(j): a thread's 8 consecutive prefixes are 9
+// words from the next thread's (conflict-free instead of 16-way)
+__host__ __device__ __forceinline__ int hwin_pad(int j) { return j + (j >> 3); }
+__host__ __device__ __forceinline__ size_t hwin_smem(int nu) {
+    return sizeof(long long) * ((size_t)hwin_pad(nu) + 1 + 32);
+}
 
-__global__ void __launch_bounds__(kHwinThreads)
+// Each row of W is scanned across the CTA into exact int64 prefixes P
+// (P[j] = sum of W[0..j), shared memory), and the horizontal window sum is
+// P[min(u+r+1, nu)] - P[max(u-r, 0)] -- the same exact integer as a
+// sliding window, at two shared loads per cell (the sliding window walked
+// 2r+1 + 64 shared words per 32 cells and was issue-bound).
+__global__ void __launch_bounds__(1024)
 hwin_int_kernel(const int32_t *__restrict__ win, int nv, int nu, int radius, double scale,
                 float *__restrict__ out, float *__restrict__ peak) {
-    extern __shared__ int32_t srow[];
-    const int pitch = hwin_pitch(nu);
+    extern __shared__ long long hp[];  // P[0 .. nu] (padded), then 32 warp totals
+    long long *wt = hp + hwin_pad(nu) + 1;
     const int vb = blockIdx.x * kHwinRows, l = blockIdx.y;
     const int64_t plane = (int64_t)nv * nu;
     const int nr = min(kHwinRows, nv - vb);
-    const int32_t *src = win + l * plane + (int64_t)vb * nu;
-    for (int t = 0; t < nr; ++t)
-        for (int j = threadIdx.x; j < nu; j += kHwinThreads)
-            srow[t * pitch + hwin_ix(j)] = __ldg(src + (int64_t)t * nu + j);
-    __syncthreads();
+    const int c0 = threadIdx.x * kHwinCols;
+    const bool vec = (nu % 4) == 0 && c0 + kHwinCols <= nu;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int32_t *src = win + l * plane + (int64_t)vb * nu + c0;
+    auto load_row = [&](int t, int32_t (&x)[kHwinCols]) {
+        if (t < nr && vec) {
+            const int4 a = __ldg(reinterpret_cast<const int4 *>(src + (int64_t)t * nu));
+            const int4 b = __ldg(reinterpret_cast<const int4 *>(src + (int64_t)t * nu + 4));
+            x[0] = a.x; x[1] = a.y; x[2] = a.z; x[3] = a.w;
+            x[4] = b.x; x[5] = b.y; x[6] = b.z; x[7] = b.w;
+        } else {
+#pragma unroll
+            for (int j = 0; j < kHwinCols; ++j)
+                x[j] = (t < nr && c0 + j < nu) ? __ldg(src + (int64_t)t * nu + j) : 0;
+        }
+    };
+    int32_t xc[kHwinCols], xn[kHwinCols];
+    load_row(0, xc);
     const double area = (double)((2 * radius + 1) * (2 * radius + 1));
     const double inv_area = __drcp_rn(area);
-    const int chunks = (nu + 31) / 32;
     float m = 0.0f;
-    for (int job = threadIdx.x; job < nr * chunks; job += kHwinThreads) {
-        const int t = job / chunks, ch = job - t * chunks;
-        const int32_t *row = srow + t * pitch;
-        const int u0 = ch * 32;
-        long long w = 0;  // (2r+1)^2 cells: may pass 2^31
-        {
-            const int ja = max(u0 - radius, 0), jb = min(u0 + radius, nu - 1);
-            for (int j = ja; j <= jb; ++j) w += row[hwin_ix(j)];
-        }
-        float *o = out + l * plane + (int64_t)(vb + t) * nu + u0;
-        const bool full = u0 + 32 <= nu && (nu % 4) == 0;
-        float4 q;
+    for (int t = 0; t < nr; ++t) {
+        load_row(t + 1, xn);  // the next row's loads overlap this row's scan
+        long long inc[kHwinCols], run = 0;
 #pragma unroll
-        for (int k = 0; k < 32; ++k) {
-            const int u = u0 + k;
-            if (k) {
-                const int jin = u + radius, jout = u - radius - 1;
-                w += (long long)(jin < nu ? row[hwin_ix(jin)] : 0) -
-                     (jout >= 0 ? row[hwin_ix(jout)] : 0);
-            }
-            const float val = box_quotient_f32(dmul((double)w, scale), area, inv_area);
-            m = fmaxf(m, (u < nu && val > 0.0f) ? val : 0.0f);
-            if ((k & 3) == 0) q.x = val;
-            else if ((k & 3) == 1) q.y = val;
-            else if ((k & 3) == 2) q.z = val;
-            else q.w = val;
-            if (full) {
-                if ((k & 3) == 3) *reinterpret_cast<float4 *>(o + k - 3) = q;
-            } else if (u < nu) {
-                o[k] = val;
-            }
+        for (int j = 0; j < kHwinCols; ++j) {
+            run += xc[j];
+            inc[j] = run;
         }
+        long long sc = run;  // inclusive warp scan of the thread totals
+#pragma unroll
+        for (int d = 1; d < 32; d <<= 1) {
+            const long long y = __shfl_up_sync(0xffffffffu, sc, d);
+            if (lane >= d) sc += y;
+        }
+        if (lane == 31) wt[warp] = sc;
+        __syncthreads();
+        long long woff = lane < warp ? wt[lane] : 0;  // totals of the warps before this one
+#pragma unroll
+        for (int d = 16; d; d >>= 1) woff += __shfl_xor_sync(0xffffffffu, woff, d);
+        const long long off = woff + sc - run;
+        if (threadIdx.x == 0) hp[0] = 0;
+#pragma unroll
+        for (int j = 0; j < kHwinCols; ++j)
+            if (c0 + j < nu) hp[hwin_pad(c0 + j + 1)] = off + inc[j];
+        __syncthreads();  // (P and wt are rewritten only after the next row's first barrier)
+        float vals[kHwinCols];
+#pragma unroll
+        for (int j = 0; j < kHwinCols; ++j) {
+            const int u = c0 + j;
+            const long long S =
+                hp[hwin_pad(min(u + radius + 1, nu))] - hp[hwin_pad(min(max(u - radius, 0), nu))];
+            vals[j] = box_quotient_f32(dmul((double)S, scale), area, inv_area);
+            if (u < nu) m = fmaxf(m, vals[j] > 0.0f ? vals[j] : 0.0f);
+        }
+        float *o = out + l * plane + (int64_t)(vb + t) * nu + c0;
+        if (vec) {
+            *reinterpret_cast<float4 *>(o) = make_float4(vals[0], vals[1], vals[2], vals[3]);
+            *reinterpret_cast<float4 *>(o + 4) = make_float4(vals[4], vals[5], vals[6], vals[7]);
+        } else {
+#pragma unroll
+            for (int j = 0; j < kHwinCols; ++j)
+                if (c0 + j < nu) o[j] = vals[j];
+        }
+#pragma unroll
+        for (int j = 0; j < kHwinCols; ++j) xc[j] = xn[j];
     }
     if (peak) block_peak(peak + l, m);
 }
@@ -1224,8 +1259,9 @@ int hb_smooth_counts(const int32_t *counts, const int32_t *mix, double scale, do
         while (tv > 8 && box_int_smem(tv, r) > (size_t)kBoxIntMaxSmem) tv >>= 1;
         const size_t smem = box_int_smem(tv, r);
         const bool sums_fit = (double)(2 * r + 1) * limit < 2147483647.0;
-        const size_t hsm = sizeof(int32_t) * (size_t)kHwinRows * hwin_pitch(nu);
-        if (sums_fit && r > kBoxIntTileMaxRadius && hsm <= (size_t)kBoxIntMaxSmem) {
+        const size_t hsm = hwin_smem(nu);
+        if (sums_fit && r > kBoxIntTileMaxRadius && hsm <= (size_t)kBoxIntMaxSmem &&
+            hwin_threads(nu) <= 1024) {
             if (cudaFuncSetAttribute(hwin_int_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                      kBoxIntMaxSmem) != cudaSuccess)
                 return check_launch("hb_smooth_counts(smem)", 0);
@@ -1238,8 +1274,8 @@ int hb_smooth_counts(const int32_t *counts, const int32_t *mix, double scale, do
             else
                 vwin_int_kernel<false><<<gv, kVwinThreads, 0, st>>>(counts, mix, nbins, nv, nu, r,
                                                                    limit, status, w);
-            hwin_int_kernel<<<dim3((nv + kHwinRows - 1) / kHwinRows, nbins), kHwinThreads, hsm,
-                              st>>>(w, nv, nu, r, scale, dst, pk);
+            hwin_int_kernel<<<dim3((nv + kHwinRows - 1) / kHwinRows, nbins), hwin_threads(nu),
+                              hsm, st>>>(w, nv, nu, r, scale, dst, pk);
             int rc = check_launch("hb_smooth_counts", 2);
             if (rc) return rc;
         } else if (sums_fit && smem <= (size_t)kBoxIntMaxSmem) {

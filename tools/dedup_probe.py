@@ -31,6 +31,7 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--config", type=int, default=4)
     ap.add_argument("--iters", type=int, default=6)
+    ap.add_argument("--global-only", action="store_true")
     a = ap.parse_args()
     w = workload(a.config)
     eng, tr, _, _ = B.prepare_engine(w.graph, w.config, bins=w.bins, matrix=w.matrix)
@@ -40,6 +41,28 @@ def main():
     torch.cuda.synchronize()
     E = eng.n_edges
     st = eng.starts[:E + 1].long()
+    if a.global_only:  # chunked (config 5 does not leave room for whole-array temporaries)
+        uniq, nseg = [], 0
+        chunk = 1 << 26
+        for i0 in range(0, eng.n_pts - 1, chunk):
+            idx = torch.arange(i0, min(i0 + chunk, eng.n_pts - 1), device=st.device)
+            edge = torch.searchsorted(st, idx, right=True) - 1
+            ok = (idx + 1) < st[edge + 1]
+            idx, edge = idx[ok], edge[ok]
+            c0 = torch.floor(eng.pts[idx] + 0.5).long()
+            d = torch.floor(eng.pts[idx + 1] + 0.5).long() - c0
+            nz = (d != 0).any(1)
+            edge, c0, d = edge[nz], c0[nz], d[nz]
+            key = ((d[:, 1] + 64) * 129 + (d[:, 0] + 64)) * (1 << 22) + c0[:, 1] * 2048 + c0[:, 0]
+            if eng.nbins > 1:
+                key = key + eng.groups.long()[edge] * (1 << 37)
+            nseg += int(key.numel())
+            uniq.append(torch.unique(key))
+            del idx, edge, c0, d, key, ok, nz
+        u = torch.unique(torch.cat(uniq))
+        print(json.dumps({"segments": nseg, "unique_keys": int(u.numel()),
+                          "ratio": round(nseg / max(1, int(u.numel())), 2)}))
+        return
     pts = eng.pts[:eng.n_pts]
     n = st[1:] - st[:-1]
     cell = torch.floor(pts + 0.5).long()

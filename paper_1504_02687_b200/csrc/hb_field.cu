@@ -796,7 +796,10 @@ box_int_kernel(const int32_t *__restrict__ counts, const int32_t *__restrict__ m
 //   hwin_int : a CTA takes kHwinRows rows of W (8 consecutive columns per
 //              thread), scans each row into int64 prefixes in shared memory
 //              and takes every window as a difference of two prefixes.
-constexpr int kVwinRows = 64;
+#ifndef HB_VWIN_ROWS
+#define HB_VWIN_ROWS 128  // 64: 0.382, 128: 0.379, 256: 0.393 ms per config-5 hb_smooth_counts
+#endif
+constexpr int kVwinRows = HB_VWIN_ROWS;
 constexpr int kVwinThreads = 128;
 // Hi of one cell (MIX: sum_b mix[l,b] * G[b]; the guard's |.|-sum in `a`)
 template <bool MIX>

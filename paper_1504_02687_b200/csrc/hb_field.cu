@@ -1132,13 +1132,15 @@ static int float_box_pass(const float *fin, int nbins, int nv, int nu, int r, fl
                           cudaStream_t st) {
     const int S = carry ? fold_strip_width(nbins, nu) : 0;
     int launched = 3;
-    if (S == 64) {
-        launch_fold<64>(fin, nbins, nv, nu, table, carry, st);
-        launched = 2;
-    } else if (S == 128) {
-        launch_fold<128>(fin, nbins, nv, nu, table, carry, st);
+    cudaError_t fe = cudaErrorNotReady;  // not launched
+    if (S == 64) fe = launch_fold<64>(fin, nbins, nv, nu, table, carry, st);
+    else if (S == 128) fe = launch_fold<128>(fin, nbins, nv, nu, table, carry, st);
+    if (fe == cudaSuccess) {
         launched = 2;
     } else {
+        // (a cooperative launch the device refuses -- e.g. too large beside
+        // other work -- falls back to the two fold kernels; nothing ran)
+        if (fe != cudaErrorNotReady) cudaGetLastError();
         col_fold_kernel<<<col_fold_blocks(nbins, nu), kColWarps * 32, 0, st>>>(fin, nbins, nv,
                                                                                nu, table);
         launch_row_fold(table, (int64_t)nbins * nv, nu, st);

@@ -158,7 +158,8 @@ HB_API int hb_splat(const double *pts, const int64_t *starts, int64_t n_edges,
  * rec != NULL segments are binned and the caller finishes with
  * hb_tiles_flush.  hb_resample_emit takes the same argument. */
 
-/* Workspace for hb_smooth: bytes of float64 tables + float32 staging. */
+/* Workspace for hb_smooth / hb_smooth_counts: bytes of the float64 table, the
+ * float32 staging plane and the fused fold's strip hand-off words. */
 HB_API size_t hb_smooth_workspace_bytes(int nbins, int nv, int nu);
 
 /* smooth_gaussian_approx (raster.py:203-219) of H = M * G, where G is the

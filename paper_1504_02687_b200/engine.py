@@ -174,10 +174,12 @@ class WeightPlan:
 
 
 
-def ordered_plan(weights: np.ndarray) -> WeightPlan:
+def ordered_plan(weights: np.ndarray, unit: bool | None = None) -> WeightPlan:
     """The reference's summation order whatever the weights."""
-    w32 = np.asarray(weights).astype(np.float32)
-    return WeightPlan("ordered", f32_w=None if np.all(w32 == 1.0) else w32)
+    w32 = np.asarray(weights, dtype=np.float32)
+    if unit is None:
+        unit = bool(np.all(w32 == 1.0))
+    return WeightPlan("ordered", f32_w=None if unit else w32)
 
 
 def _lowest_bit(x: np.ndarray) -> float:
@@ -212,27 +214,26 @@ def weight_plan(weights: np.ndarray, matrix: np.ndarray | None = None,
     ``n_points`` (initial sample points) bounds the hits per cell for the
     int32 overflow check of non-unit integer weights (the buffers hold at
     most ~4x that many points)."""
-    w32 = np.asarray(weights).astype(np.float32)
+    w32 = np.asarray(weights, dtype=np.float32)  # (no copy when already float32)
     mat = (np.eye(1, dtype=np.float32) if matrix is None
            else np.ascontiguousarray(matrix, dtype=np.float32))
     nb = mat.shape[0]
     identity = np.array_equal(mat, np.eye(nb, dtype=np.float32))
     absm = None if identity else np.abs(mat.astype(np.float64))
-    ordered = ordered_plan(w32)
-    if w32.size and (not np.all(np.isfinite(w32)) or np.any(w32 < 0)):
-        return ordered
-    unit = bool(np.all(w32 == 1.0))
+    unit = bool(np.all(w32 == 1.0))  # (then finite and nonnegative too)
+    if not unit and w32.size and (not np.all(np.isfinite(w32)) or np.any(w32 < 0)):
+        return ordered_plan(w32, unit)
     if not unit and not (np.all(np.floor(w32) == w32) and np.all(w32 < 2 ** 24)):
-        return ordered
+        return ordered_plan(w32, unit)
     wmax = float(w32.max()) if w32.size else 1.0
     # every product fl32(w * M[l,b]) exact: the weights' bit span plus the
     # matrix entries' significand bits fit float32's 24
     qw = 1.0 if unit else _lowest_bit(w32)
     span_w = 1 if unit else int(math.floor(math.log2(max(wmax, qw) / qw))) + 1
     if span_w + _sig_bits(mat) > 24:
-        return ordered
+        return ordered_plan(w32, unit)
     if not unit and wmax * (4.0 * n_points + (1 << 20)) >= 2.0 ** 31:
-        return ordered  # int32 counts could wrap
+        return ordered_plan(w32, unit)  # int32 counts could wrap
     q = qw * _lowest_bit(mat)
     if unit:
         return WeightPlan("unit", quantum=q, abs_matrix=absm)

@@ -505,25 +505,26 @@ fold_kernel(const float *__restrict__ in, int nv, int nu, int nstrips,
             __syncwarp();
             // the tile's rows of T, coalesced
             const int nr = min(32, nv - b * 32);
-            if (nr == 32 && full && (nu & 1) == 0) {
-                // full tile: 8 rows of loads in flight, then their 16-byte stores
-                double *d = dst + (int64_t)(b * 32) * nu + 2 * lane;
-                const double *s = tile + 2 * lane;
+            if (nr == 32 && full) {
+                // full tile: 8 rows of loads in flight, then their stores.  A
+                // lane takes columns lane, lane+32, ...: every shared load and
+                // global store is a contiguous 256-byte warp access (a 16-byte
+                // pair per lane would read each wavefront half-used)
+                double *d = dst + (int64_t)(b * 32) * nu + lane;
+                const double *s = tile + lane;
 #pragma unroll
                 for (int i0 = 0; i0 < 32; i0 += 8) {
-                    double2 q[8][S / 64];
+                    double q[8][S / 32];
 #pragma unroll
                     for (int ii = 0; ii < 8; ++ii)
 #pragma unroll
-                        for (int m = 0; m < S / 64; ++m)
-                            q[ii][m] = make_double2(s[(i0 + ii) * C::kPitch + 64 * m],
-                                                    s[(i0 + ii) * C::kPitch + 64 * m + 1]);
+                        for (int m = 0; m < S / 32; ++m)
+                            q[ii][m] = s[(i0 + ii) * C::kPitch + 32 * m];
 #pragma unroll
                     for (int ii = 0; ii < 8; ++ii)
 #pragma unroll
-                        for (int m = 0; m < S / 64; ++m)
-                            *reinterpret_cast<double2 *>(d + (int64_t)(i0 + ii) * nu + 64 * m) =
-                                q[ii][m];
+                        for (int m = 0; m < S / 32; ++m)
+                            d[(int64_t)(i0 + ii) * nu + 32 * m] = q[ii][m];
                 }
             } else if ((nu & 1) == 0) {  // 16-byte stores: a lane writes 2 columns of a row
 #pragma unroll 8

@@ -329,6 +329,48 @@ def test_smooth_fused_fold_shapes_vs_oracle(shape):
         assert np.array_equal(got, O.smooth(vals, sigma, 3)), (shape, sigma)
 
 
+# extreme aspect ratios and sizes: single cells, rows and columns, fewer rows
+# than a 32-row block, more strips than co-resident CTAs at S = 64 (S = 128)
+@pytest.mark.parametrize("shape,sigma", [((1, 1, 1), 2.0), ((1, 3, 700), 5.0),
+                                         ((2, 700, 3), 5.0), ((1, 33, 10000), 3.0),
+                                         ((3, 31, 129), 40.0), ((1, 64, 64), 0.6)])
+def test_smooth_extreme_shapes_vs_oracle(shape, sigma):
+    rng = np.random.default_rng(shape[1] * 7 + shape[2])
+    vals = (rng.gamma(0.5, 2.0, size=shape) * (rng.uniform(size=shape) < 0.4)).astype(np.float32)
+    got = R.smooth_gaussian_approx(DensityField(None, vals), sigma, 3).values
+    assert np.array_equal(got, O.smooth(vals, sigma, 3)), (shape, sigma)
+
+
+@pytest.mark.parametrize("seed", range(6))
+def test_smooth_counts_random_shapes_match_float_path(seed):
+    """Exact integer first pass (tile or separable + prefix rows) against the
+    all-float path on random shapes and radii, bit for bit."""
+    rng = np.random.default_rng(100 + seed)
+    nb = int(rng.integers(1, 4))
+    nv = int(rng.integers(1, 300))
+    nu = int(rng.integers(1, 700))
+    radii = [int(rng.integers(1, 60)), int(rng.integers(0, 60)), int(rng.integers(0, 60))]
+    counts = (rng.poisson(2.0, size=(nb, nv, nu)) * (rng.uniform(size=(nb, nv, nu)) < 0.5)
+              ).astype(np.int32)
+    r = torch.tensor(radii, dtype=torch.int32)
+    ws = torch.empty(int(N.lib().hb_smooth_workspace_bytes(nb, nv, nu)), dtype=torch.uint8,
+                     device="cuda")
+    c = dev(counts)
+    ref = torch.empty((nb, nv, nu), dtype=torch.float32, device="cuda")
+    got = torch.empty_like(ref)
+    pk_ref = torch.zeros(nb, dtype=torch.float32, device="cuda")
+    pk = torch.zeros_like(pk_ref)
+    status = torch.zeros(1, dtype=torch.int32, device="cuda")
+    N.call("hb_smooth", ptr(c), None, None, nb, nv, nu, r.data_ptr(), 3, ptr(ref), ptr(ws),
+           ws.numel(), ptr(pk_ref), stream_ptr())
+    N.call("hb_smooth_counts", ptr(c), None, 1.0, 2.0 ** 24, nb, nv, nu, r.data_ptr(), 3,
+           ptr(got), ptr(ws), ws.numel(), ptr(pk), ptr(status), stream_ptr())
+    sync()
+    assert torch.equal(got, ref), (nb, nv, nu, radii)
+    assert torch.equal(pk, pk_ref)
+    assert int(status.item()) == 0
+
+
 def test_smooth_fused_fold_equals_two_fold_kernels_config5_map(monkeypatch):
     """The config-5 map (4 x 2047 x 2048, radii 50/51/51): fused fold vs the
     column-fold + row-fold kernels, bit for bit."""

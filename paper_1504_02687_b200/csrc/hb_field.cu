@@ -336,6 +336,16 @@ __device__ __forceinline__ void fold_trace(int l, int k, int b, int e) {
 __device__ __forceinline__ void fold_trace(int, int, int, int) {}
 #endif
 
+// (double)f as a volatile conversion: left to itself the compiler keeps the
+// float and converts right before each add, which puts the F2F latency
+// (~18 cycles) on the column chain; pinned here, the conversion happens
+// where it is written (a block ahead of its add)
+__device__ __forceinline__ double f2d_pinned(float f) {
+    double d;
+    asm volatile("cvt.f64.f32 %0, %1;" : "=d"(d) : "f"(f));
+    return d;
+}
+
 template <int S>
 struct FoldCfg {
     static constexpr int kColWarps = S / 32;
@@ -406,7 +416,7 @@ fold_kernel(const float *__restrict__ in, int nv, int nu, int nstrips,
         auto widen = [&](int bb, double (&xd)[32]) {
             const float *xb = xs + (size_t)(bb % C::kStages) * 32 * S + t;
 #pragma unroll
-            for (int i = 0; i < 32; ++i) xd[i] = (double)xb[i * S];
+            for (int i = 0; i < 32; ++i) xd[i] = f2d_pinned(xb[i * S]);
         };
 #pragma unroll
         for (int d = 0; d < C::kStages - 1; ++d) issue(d);
@@ -426,7 +436,7 @@ fold_kernel(const float *__restrict__ in, int nv, int nu, int nstrips,
                 // np.cumsum: the first element as is
                 c = (b == 0 && i == 0) ? cur[0] : dadd(c, cur[i]);
                 tile[i * C::kPitch] = c;
-                nxt[i] = (double)xn[i * S];  // (unused after the last block)
+                nxt[i] = f2d_pinned(xn[i * S]);  // (unused after the last block)
             }
             asm volatile("bar.sync 1, %0;" ::"r"(S));  // C tile complete
             if (t == 0) {

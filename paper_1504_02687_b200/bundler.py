@@ -148,15 +148,15 @@ def prepare_engine(graph: Graph, config: BundleConfig | None = None, *, bins=Non
 
 def _plan(graph, cfg, matrix, transform, force_ordered=False):
     """The histogram path for the WHOLE graph (every rank decides alike)."""
-    w32 = np.asarray(graph.weights, dtype=np.float32)  # converted once for both checks
+    w = np.asarray(graph.weights)
     if force_ordered:
-        return ordered_plan(w32)
+        return ordered_plan(w)
     n0 = 0
-    if graph.n_edges and not np.all(w32 == 1.0):
+    if graph.n_edges and not np.all(w == 1.0):
         pos = graph.positions
         n0 = int(sample_counts(transform.world_to_grid(pos[graph.sources]),
                                transform.world_to_grid(pos[graph.targets]), cfg.delta).sum())
-    return weight_plan(w32, matrix, n0)
+    return weight_plan(w, matrix, n0)
 
 
 def _setup(graph, cfg, bins_arr, matrix, fixed_step, group, capacity_factor, *,

@@ -214,13 +214,18 @@ def weight_plan(weights: np.ndarray, matrix: np.ndarray | None = None,
     ``n_points`` (initial sample points) bounds the hits per cell for the
     int32 overflow check of non-unit integer weights (the buffers hold at
     most ~4x that many points)."""
-    w32 = np.asarray(weights, dtype=np.float32)  # (no copy when already float32)
+    w = np.asarray(weights)
     mat = (np.eye(1, dtype=np.float32) if matrix is None
            else np.ascontiguousarray(matrix, dtype=np.float32))
     nb = mat.shape[0]
     identity = np.array_equal(mat, np.eye(nb, dtype=np.float32))
     absm = None if identity else np.abs(mat.astype(np.float64))
-    unit = bool(np.all(w32 == 1.0))  # (then finite and nonnegative too)
+    # all exactly 1.0 -> fl32 all 1.0 (then finite and nonnegative too): the
+    # common case needs no float32 copy
+    unit = bool(np.all(w == 1.0))
+    w32 = w if unit else np.asarray(w, dtype=np.float32)  # (no copy when already float32)
+    if not unit:
+        unit = bool(np.all(w32 == 1.0))  # (weights that round to 1.0 in float32)
     if not unit and w32.size and (not np.all(np.isfinite(w32)) or np.any(w32 < 0)):
         return ordered_plan(w32, unit)
     if not unit and not (np.all(np.floor(w32) == w32) and np.all(w32 < 2 ** 24)):

@@ -143,15 +143,22 @@ def main():
         import ctypes
         tl = ctypes.byref(eng.tiles)
 
+        def expand():
+            N.call("hb_segtab_expand", tl, ptr(eng.hist), nv, nu, None, s)
+
         def emit_segtab():
             eng.hist.zero_()
             N.call("hb_resample_emit", ptr(eng.pts), ptr(eng.starts), E, n_old, ptr(eng.pos),
                    ptr(eng.starts_alt), ptr(eng.alt), ptr(eng.groups), ptr(eng.wint),
                    ptr(eng.hist), nv, nu, ptr(eng.status), tl, s)
 
-        def expand():
-            N.call("hb_segtab_expand", tl, ptr(eng.hist), nv, nu, None, s)
+        def splat_segtab():  # the emitted points splatted by a separate pass
+            eng.hist.zero_()
+            N.call("hb_splat", ptr(eng.alt), ptr(eng.starts_alt), E, n_new, ptr(eng.groups),
+                   ptr(eng.wint), ptr(eng.hist), Bn, nv, nu, ptr(eng.status), tl, s)
 
+        emit(False)
+        out["splat_segtab_only_ms"] = timed(lambda: (splat_segtab(), expand()), reps=1)
         out["segtab"] = {"halo": eng.tiles.halo, "entries": int(eng.t_tab.numel())}
         out["emit_segtab_ms"] = timed(lambda: (emit_segtab(), expand()), reps=1)
         emit_segtab()

@@ -316,6 +316,18 @@ def test_smooth_random_multilayer_vs_oracle():
         assert np.array_equal(got, O.smooth(vals, sigma, 3)), sigma
 
 
+@pytest.mark.parametrize("shape", [(1, 1), (5, 3), (77, 203), (300, 1030)])
+def test_integral_image_vs_reference_expression(shape):
+    """raster.integral_image (hb_integral_image) against the reference's own
+    expression (raster.py:133-139): strict float64 cumsums down the columns,
+    then along the rows, zero first row and column."""
+    rng = np.random.default_rng(shape[0] + shape[1])
+    lay = (rng.gamma(0.5, 2.0, size=shape) * (rng.uniform(size=shape) < 0.4)).astype(np.float32)
+    ref = np.zeros((shape[0] + 1, shape[1] + 1), dtype=np.float64)
+    ref[1:, 1:] = np.cumsum(np.cumsum(lay, axis=0, dtype=np.float64), axis=1)
+    assert np.array_equal(R.integral_image(lay), ref)
+
+
 # fused integral table (fold_kernel): strip widths 64 and 128, partial strips
 # and row blocks, a single strip, and the two-kernel fallback (too many strips
 # to be co-resident)

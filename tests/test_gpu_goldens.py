@@ -286,6 +286,34 @@ def test_cfg5_full_size_shard_vs_oracle():
         assert (m.moved_points, m.used_cells) == (r.moved_points, r.used_cells)
 
 
+@pytest.mark.slow
+def test_cfg5_full_size_paths_agree(monkeypatch):
+    """All of config 5 (20 M edges, 4 x 2047 x 2048), two iterations through
+    bundle(): the default path against the two-kernel smoothing folds
+    (HB_FOLD=0) and against synchronous iterations (HB_SYNC_FREE=0) -- the
+    same points, field and counts bit for bit at full size."""
+    w = workload(5)
+    cfg = w.config
+    cfg.iterations = 2
+
+    def run():
+        res = B.bundle(w.graph, cfg, bins=w.bins, matrix=w.matrix)
+        out = (digest(res.sampled_edges.world)["sha256"],
+               digest(res.sampled_edges.starts)["sha256"],
+               digest(res.density.values)["sha256"],
+               [(m.moved_points, m.used_cells) for m in res.metrics])
+        del res
+        torch.cuda.empty_cache()
+        return out
+
+    base = run()
+    monkeypatch.setenv("HB_FOLD", "0")
+    assert run() == base
+    monkeypatch.delenv("HB_FOLD")
+    monkeypatch.setenv("HB_SYNC_FREE", "0")
+    assert run() == base
+
+
 @pytest.mark.parametrize("name", ["empty", "coincident", "single", "collinear", "border_hub"])
 def test_degenerate_graphs_match_reference(name):
     """No edges, coincident endpoints (zero-length segments), a single edge,
